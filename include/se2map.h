@@ -1,0 +1,140 @@
+/*
+ * se2map.h — C ABI of the B200-native SE(2) traversability library (libse2map.so).
+ *
+ * The library implements the data-parallel hot path of SEB-Naver's local mapping
+ * (arXiv 2503.02412, §V): the robot-centric elevation window of Eq. 4
+ * and Algorithm 1 evaluated for every SE(2) state
+ * (x, y, yaw) of the window "in parallel", plus the incremental recompute of
+ * the states whose footprint changed when the window moved.
+ *
+ * Conventions (readings R1-R21):
+ *   - window cells: x = columns (fastest), y = rows; world cell I covers [I*r, (I+1)*r) (R6);
+ *   - the window is [floor(x/r) - nx/2, ... + nx) x [floor(y/r) - ny/2, ... + ny) (Eq. 4, R6/R7);
+ *   - yaw bin k has theta_k = -pi + 2*pi*k/n_yaw (R3); the footprint is the ellipse with
+ *     semi-axes (e_x along x_yaw, e_y across) centred on the state (R2/R4), cell centres with
+ *     q <= 1 + 1e-9 (R5), clipped to the window's known cells (R8/R9);
+ *   - outputs per state: risk in [0,1] (Alg. 1 lines 10-18), signed pitch = asin(b3^T x_b) and
+ *     roll = asin(b3^T y_b) (line 13, R13), z = fitted-plane height at the state centre (R14),
+ *     traversable bit = no early return and not unknown (R17).  States with fewer than 3
+ *     footprint cells or a degenerate covariance are "unknown": risk 1, trav 0, pitch/roll/z NaN.
+ *
+ * Ownership: the caller owns every pointer it passes; the library copies inputs before the
+ * call returns (stream-ordered for device pointers) and retains nothing.  The library owns
+ * all device memory it allocates (freed by se2m_destroy).
+ * Concurrency: a handle has one owner and is not thread-safe; all work is ordered on the
+ * handle's CUDA stream.  se2m_query / se2m_download synchronise that stream.
+ * Errors: status codes only; no call aborts and no C++ exception crosses the ABI.  On
+ * SE2M_ERR_INVALID_ARG the handle is unchanged.  se2m_last_error() gives a message.
+ * Per-state degeneracy is not an error.
+ */
+#ifndef SE2MAP_H
+#define SE2MAP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct se2m_map se2m_map; /* opaque handle */
+
+typedef enum {
+  SE2M_OK = 0,
+  SE2M_ERR_INVALID_ARG = 1,   /* bad dims / params / pointers (handle unchanged) */
+  SE2M_ERR_OOM = 2,           /* device or host allocation failed */
+  SE2M_ERR_CUDA = 3,          /* a CUDA runtime call or kernel launch failed */
+  SE2M_ERR_UNSUPPORTED = 4,   /* parameter combination not built into this library */
+  SE2M_ERR_OUT_OF_RANGE = 5,  /* a query / rectangle lies (partly) outside the window */
+  SE2M_ERR_STATE = 6          /* call order violated, e.g. assess before any elevation */
+} se2m_status;
+
+enum { SE2M_FULL = 0, SE2M_INCREMENTAL = 1 };          /* se2m_assess_se2 mode */
+enum { SE2M_MEM_HOST = 0, SE2M_MEM_DEVICE = 1 };       /* pointer kinds */
+enum { SE2M_SHARD_NONE = 0, SE2M_SHARD_YAW = 1, SE2M_SHARD_ROWS = 2 };
+
+typedef struct {
+  int32_t nx, ny;          /* window cells, >= 1 each, nx*ny <= 2^31 */
+  int32_t n_yaw;           /* yaw bins over [-pi, pi), >= 1 ("grids in SO(2)") */
+  int32_t shard_mode;      /* SE2M_SHARD_*: which states this rank computes */
+  double resolution;       /* l_res, m per cell, > 0 (Eq. 4; PAPER.md:248 uses 0.1) */
+  double ellipse_ex;       /* footprint semi-axis along the heading, m, > 0 (Alg. 1 input e_x) */
+  double ellipse_ey;       /* footprint semi-axis across the heading, m, > 0 (Alg. 1 input e_y) */
+  double w_r[3];           /* risk weights w_r >= 0 (Alg. 1 input; default 0.4, 0.3, 0.3) */
+  double kappa_max;        /* curvature limit > 0 (default 0.1) */
+  double phi_x_max;        /* pitch limit, rad > 0 (0.52) */
+  double phi_y_max;        /* roll limit, rad > 0 (0.52) */
+  double robot_x, robot_y; /* initial robot position (m): window origin by Eq. 4 */
+  int32_t rank, world_size;/* shard index / count (1 = single GPU) */
+  int32_t device;          /* CUDA device ordinal */
+  int32_t reserved0;
+  void* cuda_stream;       /* cudaStream_t to order all work on, or NULL: the library creates one */
+} se2m_params;
+
+/* Fill *p with the defaults above (thresholds from PAPER.md:291 / SPEC S:300). */
+void se2m_default_params(se2m_params* p);
+
+/* Create a map: validates p, allocates the ring-buffered elevation window and output planes
+ * on p->device, builds the per-yaw footprint tables.  All cells start unknown.
+ * *out is set only on SE2M_OK. */
+se2m_status se2m_init(const se2m_params* p, se2m_map** out);
+
+/* Free everything (synchronises the stream).  NULL-safe. */
+void se2m_destroy(se2m_map* m);
+
+/* Write elevations for the window-local rectangle [i0, i0+w) x [j0, j0+h) (columns x rows),
+ * the inpainted map M of Alg. 1.  heights: row-major, leading dimension
+ * ld >= w floats; known: same layout in bytes (1 = known), or NULL = all known.  mem says
+ * whether both pointers are host or device memory.  The rectangle must lie inside the window
+ * (else SE2M_ERR_OUT_OF_RANGE, nothing written).  Marks the rectangle dirty for INCREMENTAL. */
+se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w, int32_t h,
+                                  const float* heights, int64_t ld, const uint8_t* known,
+                                  int32_t mem);
+
+/* Eq. 4: recentre the window on the robot at (robot_x, robot_y): the new
+ * origin is floor(x/r) - nx/2 (IEEE double, reading R7); cells that leave the window become
+ * unknown ("removed in parallel").  No data moves (ring buffer).  Returns the
+ * origin displacement in cells through out_di / out_dj (either may be NULL).  Marks the
+ * exposed and the vacated strips dirty. */
+se2m_status se2m_shift_window(se2m_map* m, double robot_x, double robot_y, int32_t* out_di,
+                              int32_t* out_dj);
+
+/* Algorithm 1 for every SE(2) state of this rank's share (mode SE2M_FULL), or only for the
+ * states whose footprint touches a cell changed since the last assess (SE2M_INCREMENTAL;
+ * results are bit-identical to FULL).  Asynchronous on the handle's stream.
+ * SE2M_ERR_STATE if no elevation was ever written. */
+se2m_status se2m_assess_se2(se2m_map* m, int32_t mode);
+
+/* n world-frame queries xyt[3*q + {0,1,2}] = (x, y, theta): the state of the window cell
+ * containing (x, y) at the nearest yaw bin (reading R3/R6).  Any output pointer may be NULL;
+ * outputs are host memory of n entries.  Entries outside the window (or of yaw bins this
+ * rank does not own) get NaN / trav 0 and the call returns SE2M_ERR_OUT_OF_RANGE after
+ * filling all others.  Synchronises the stream. */
+se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, float* pitch,
+                       float* roll, float* z, uint8_t* trav);
+
+/* Whole output planes in LOGICAL window order, layout [k][j][i] (n_yaw * ny * nx entries per
+ * non-NULL pointer; trav as bytes 0/1).  mem says whether the output pointers are host or
+ * device memory.  States of yaw bins not owned by this rank are NaN / 0.  Synchronises. */
+se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z,
+                          uint8_t* trav, int32_t mem);
+
+/* Window origin (world cell of logical (0,0)) and the owned representative-yaw range. */
+se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
+
+/* Number of footprint cells |P_k| for yaw bin k (0 <= k < n_yaw) and the stencil radius R. */
+se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, int32_t* radius);
+
+/* Block until all work queued on the handle's stream is done. */
+se2m_status se2m_synchronize(se2m_map* m);
+
+/* Kernel launches issued by this handle since creation (for the bench's gpu_launches). */
+int64_t se2m_launch_count(const se2m_map* m);
+
+/* Per-handle message for the last failing call; valid until the next call on m.
+ * se2m_last_error(NULL) returns the message of the last failed se2m_init. */
+const char* se2m_last_error(const se2m_map* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SE2MAP_H */

@@ -1,0 +1,593 @@
+// se2map.cu — C-ABI runtime of libse2map.so (see include/se2map.h for the contract).
+//
+// Owns the device state of one robot-centric map: the ring-buffered elevation window
+// (Eq. 4), the per-yaw footprint tables (reading R5), the output planes,
+// the dirty-region tracker for INCREMENTAL assessment, and the TMA descriptor of the map.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/se2map.h"
+#include "se2m_internal.h"
+
+using namespace se2m;
+
+namespace {
+
+struct Rect {  // world cells [I0, I1) x [J0, J1)
+  long long I0, I1, J0, J1;
+};
+
+long long floor_div(long long a, long long b) {
+  long long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+int pmod(long long a, int n) {
+  long long m = a % n;
+  return (int)(m < 0 ? m + n : m);
+}
+
+std::string g_init_error;  // message of the last failed se2m_init
+
+}  // namespace
+
+struct se2m_map {
+  se2m_params prm;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int H = 0, paired = 0, R = 0, R_T = 0, ldh = 0, trav_words = 0;
+  int k_lo = 0, k_hi = 0;  // owned representative bins [k_lo, k_hi)
+  long long I_M = 0, J_M = 0;
+  float* d_h = nullptr;
+  float *d_risk = nullptr, *d_pitch = nullptr, *d_roll = nullptr, *d_z = nullptr;
+  uint32_t* d_trav = nullptr;
+  int2* d_runs = nullptr;
+  float4* d_geo = nullptr;
+  float2* d_cs = nullptr;
+  std::vector<int> ncells;  // |P_k| per rep bin
+  int* d_tiles = nullptr;
+  int* h_tiles = nullptr;  // pinned
+  size_t tiles_cap = 0;
+  float* d_stage = nullptr;  // update / download staging
+  size_t stage_bytes = 0;
+  int4* d_qidx = nullptr;
+  float* d_qout = nullptr;
+  size_t q_cap = 0;
+  CUtensorMap tmap;
+  bool tma_ok = false;
+  bool have_data = false;
+  bool all_dirty = true;
+  std::vector<Rect> dirty;
+  long long launches = 0;
+  std::string err;
+};
+
+// ------------------------------------------------------------------------------------------
+static se2m_status fail(se2m_map* m, se2m_status st, const std::string& msg) {
+  if (m) m->err = msg;
+  else g_init_error = msg;
+  return st;
+}
+static se2m_status cuda_fail(se2m_map* m, cudaError_t e, const char* what) {
+  return fail(m, SE2M_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_TRY(m, call, what)                         \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(m, e_, what); \
+  } while (0)
+
+static int pick_radius(int R) {
+  for (int r : kRadii)
+    if (r >= R) return r;
+  return -1;
+}
+
+// Footprint stencil, reading R5 (rule C5 of SURVEY.md §8(c)): cell centres, q in cell units with the
+// representative angle theta_k (k < H), include iff q <= 1 + 1e-9.  FP64 on the host, once.
+static bool build_stencils(se2m_map* m, std::vector<int2>& runs, std::vector<float4>& geo, std::vector<float2>& cs) {
+  const se2m_params& P = m->prm;
+  const double a = P.ellipse_ex / P.resolution, b = P.ellipse_ey / P.resolution;
+  const int Rs = (int)ceil(std::max(a, b)) + 1;
+  struct Run { int lo, hi; };
+  std::vector<std::vector<Run>> rr(m->H, std::vector<Run>(2 * Rs + 1, Run{0, -1}));
+  int R = 0;
+  m->ncells.assign(m->H, 0);
+  std::vector<long long> Sxx(m->H, 0), Sxy(m->H, 0), Syy(m->H, 0);
+  cs.resize(m->H);
+  for (int k = 0; k < m->H; ++k) {
+    const double th = -M_PI + 2.0 * M_PI * (double)k / (double)P.n_yaw;
+    const double c = cos(th), s = sin(th);
+    cs[k] = make_float2((float)c, (float)s);
+    for (int dj = -Rs; dj <= Rs; ++dj) {
+      int lo = 1 << 30, hi = -(1 << 30), cnt = 0;
+      for (int di = -Rs; di <= Rs; ++di) {
+        const double u = di * c + dj * s, v = -di * s + dj * c;
+        const double q = (u / a) * (u / a) + (v / b) * (v / b);
+        if (q <= 1.0 + 1e-9) {
+          lo = std::min(lo, di); hi = std::max(hi, di); ++cnt;
+          m->ncells[k]++;
+          Sxx[k] += (long long)di * di; Sxy[k] += (long long)di * dj; Syy[k] += (long long)dj * dj;
+          R = std::max(R, std::max(std::abs(di), std::abs(dj)));
+        }
+      }
+      if (cnt) {
+        if (cnt != hi - lo + 1) return false;  // an ellipse row must be one run (convexity)
+        rr[k][dj + Rs] = Run{lo, hi};
+      }
+    }
+  }
+  m->R = R;
+  m->R_T = pick_radius(std::max(R, 1));
+  if (m->R_T < 0) return false;
+  const int NR = 2 * m->R_T + 1;
+  runs.assign((size_t)m->H * NR, make_int2(0, -1));
+  geo.resize(m->H);
+  for (int k = 0; k < m->H; ++k) {
+    for (int dj = -std::min(Rs, m->R_T); dj <= std::min(Rs, m->R_T); ++dj) {
+      const Run& q = rr[k][dj + Rs];
+      if (q.hi >= q.lo) runs[(size_t)k * NR + dj + m->R_T] = make_int2(q.lo, q.hi);
+    }
+    geo[k] = make_float4((float)m->ncells[k], (float)Sxx[k], (float)Sxy[k], (float)Syy[k]);
+  }
+  return true;
+}
+
+static bool make_tensor_map(se2m_map* m) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qres;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres) != cudaSuccess || !fn ||
+      qres != cudaDriverEntryPointSuccess)
+    return false;
+  const int HX = TX + 2 * m->R_T, HY = TY + 2 * m->R_T;
+  if (HX > 256 || HY > 256 || HX > m->prm.nx || HY > m->prm.ny) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)m->prm.nx, (cuuint64_t)m->prm.ny};
+  cuuint64_t strides[1] = {(cuuint64_t)m->ldh * 4};
+  cuuint32_t box[2] = {(cuuint32_t)HX, (cuuint32_t)HY};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ((EncodeFn)fn)(&m->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, m->d_h, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static AssessParams make_params(const se2m_map* m) {
+  AssessParams p;
+  memset(&p, 0, sizeof p);
+  p.nx = m->prm.nx; p.ny = m->prm.ny; p.ldh = m->ldh;
+  p.I_M = m->I_M; p.J_M = m->J_M;
+  p.h = m->d_h;
+  p.risk = m->d_risk; p.pitch = m->d_pitch; p.roll = m->d_roll; p.z = m->d_z; p.trav = m->d_trav;
+  p.trav_words = m->trav_words;
+  p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
+  p.runs = m->d_runs; p.geo = m->d_geo; p.cs = m->d_cs;
+  p.r = (float)m->prm.resolution;
+  p.kappa_max = (float)m->prm.kappa_max; p.phi_x_max = (float)m->prm.phi_x_max; p.phi_y_max = (float)m->prm.phi_y_max;
+  p.wk = (float)(m->prm.w_r[0] / m->prm.kappa_max);
+  p.wx = (float)(m->prm.w_r[1] / m->prm.phi_x_max);
+  p.wy = (float)(m->prm.w_r[2] / m->prm.phi_y_max);
+  p.k_begin = m->k_lo; p.k_end = m->k_hi; p.k_chunk = 1;
+  p.use_tma = m->tma_ok ? 1 : 0;
+  return p;
+}
+
+static se2m_status ensure_stage(se2m_map* m, size_t bytes) {
+  if (m->stage_bytes >= bytes) return SE2M_OK;
+  if (m->d_stage) { cudaStreamSynchronize(m->stream); cudaFree(m->d_stage); m->d_stage = nullptr; m->stage_bytes = 0; }
+  CUDA_TRY(m, cudaMalloc(&m->d_stage, bytes), "cudaMalloc(staging)");
+  m->stage_bytes = bytes;
+  return SE2M_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" void se2m_default_params(se2m_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof *p);
+  p->nx = 100; p->ny = 100; p->n_yaw = 36;
+  p->resolution = 0.1;
+  p->ellipse_ex = 0.8; p->ellipse_ey = 0.5;
+  p->w_r[0] = 0.4; p->w_r[1] = 0.3; p->w_r[2] = 0.3;
+  p->kappa_max = 0.1; p->phi_x_max = 0.52; p->phi_y_max = 0.52;
+  p->world_size = 1;
+}
+
+static se2m_status validate(const se2m_params* p) {
+  if (!p) return fail(nullptr, SE2M_ERR_INVALID_ARG, "params is NULL");
+  if (p->nx < 1 || p->ny < 1 || (long long)p->nx * p->ny > (1ll << 31)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "nx, ny must be >= 1 and nx*ny <= 2^31");
+  if (p->n_yaw < 1) return fail(nullptr, SE2M_ERR_INVALID_ARG, "n_yaw must be >= 1");
+  if (!(p->resolution > 0) || !isfinite(p->resolution)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "resolution must be > 0");
+  if (!(p->ellipse_ex > 0) || !(p->ellipse_ey > 0)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "ellipse semi-axes must be > 0");
+  for (int i = 0; i < 3; ++i)
+    if (!(p->w_r[i] >= 0)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "w_r must be >= 0");
+  if (!(p->kappa_max > 0) || !(p->phi_x_max > 0) || !(p->phi_y_max > 0)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "limits must be > 0");
+  if (!isfinite(p->robot_x) || !isfinite(p->robot_y)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "robot position must be finite");
+  if (p->world_size < 1 || p->rank < 0 || p->rank >= p->world_size) return fail(nullptr, SE2M_ERR_INVALID_ARG, "need 0 <= rank < world_size");
+  if (p->shard_mode < 0 || p->shard_mode > 2) return fail(nullptr, SE2M_ERR_INVALID_ARG, "shard_mode must be 0, 1 or 2");
+  if (p->ellipse_ex / p->resolution > 32 || p->ellipse_ey / p->resolution > 32)
+    return fail(nullptr, SE2M_ERR_UNSUPPORTED, "footprint radius > 32 cells is not built into this library");
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
+  if (!out) return fail(nullptr, SE2M_ERR_INVALID_ARG, "out is NULL");
+  se2m_status st = validate(p);
+  if (st != SE2M_OK) return st;
+  se2m_map* m = new (std::nothrow) se2m_map();
+  if (!m) return fail(nullptr, SE2M_ERR_OOM, "host allocation failed");
+  m->prm = *p;
+  auto bail = [&](se2m_status s) {
+    g_init_error = m->err;
+    se2m_destroy(m);
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) { cuda_fail(m, e, "cudaSetDevice"); return bail(SE2M_ERR_CUDA); }
+  if (p->cuda_stream) m->stream = (cudaStream_t)p->cuda_stream;
+  else {
+    e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { cuda_fail(m, e, "cudaStreamCreate"); return bail(SE2M_ERR_CUDA); }
+    m->own_stream = true;
+  }
+  const int n = p->n_yaw;
+  m->paired = (n % 2 == 0) ? 1 : 0;
+  m->H = m->paired ? n / 2 : n;
+  m->k_lo = 0; m->k_hi = m->H;
+  if (p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1) {
+    m->k_lo = (int)((long long)m->H * p->rank / p->world_size);
+    m->k_hi = (int)((long long)m->H * (p->rank + 1) / p->world_size);
+  }
+  std::vector<int2> runs;
+  std::vector<float4> geo;
+  std::vector<float2> cs;
+  if (!build_stencils(m, runs, geo, cs)) {
+    fail(m, SE2M_ERR_UNSUPPORTED, "footprint stencil could not be built (radius or shape)");
+    return bail(SE2M_ERR_UNSUPPORTED);
+  }
+  // Eq. 4 (reading R6/R7): window origin = floor(x/r) - nx/2 in IEEE double
+  m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
+  m->J_M = (long long)floor(p->robot_y / p->resolution) - p->ny / 2;
+  m->ldh = (p->nx + 3) / 4 * 4;
+  m->trav_words = (p->nx + 31) / 32;
+  const size_t plane = (size_t)p->nx * p->ny;
+  const size_t nst = plane * n;
+  struct { void** ptr; size_t bytes; const char* what; } allocs[] = {
+      {(void**)&m->d_h, (size_t)m->ldh * p->ny * 4, "heights"},
+      {(void**)&m->d_risk, nst * 4, "risk"},
+      {(void**)&m->d_pitch, nst * 4, "pitch"},
+      {(void**)&m->d_roll, nst * 4, "roll"},
+      {(void**)&m->d_z, nst * 4, "z"},
+      {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
+      {(void**)&m->d_runs, runs.size() * sizeof(int2), "runs"},
+      {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
+      {(void**)&m->d_cs, cs.size() * sizeof(float2), "cs"},
+  };
+  for (auto& a : allocs) {
+    e = cudaMalloc(a.ptr, a.bytes);
+    if (e != cudaSuccess) {
+      fail(m, e == cudaErrorMemoryAllocation ? SE2M_ERR_OOM : SE2M_ERR_CUDA, std::string("cudaMalloc(") + a.what + ")");
+      return bail(e == cudaErrorMemoryAllocation ? SE2M_ERR_OOM : SE2M_ERR_CUDA);
+    }
+  }
+  if ((e = cudaMemcpyAsync(m->d_runs, runs.data(), runs.size() * sizeof(int2), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_geo, geo.data(), geo.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemsetAsync(m->d_h, 0xff, (size_t)m->ldh * p->ny * 4, m->stream)) ||  // 0xffffffff = NaN: unknown
+      (e = cudaMemsetAsync(m->d_trav, 0, (size_t)n * p->ny * m->trav_words * 4, m->stream)) ||
+      (e = cudaStreamSynchronize(m->stream))) {
+    cuda_fail(m, e, "init upload");
+    return bail(SE2M_ERR_CUDA);
+  }
+  m->tma_ok = make_tensor_map(m);
+  *out = m;
+  return SE2M_OK;
+}
+
+extern "C" void se2m_destroy(se2m_map* m) {
+  if (!m) return;
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  void* ptrs[] = {m->d_h, m->d_risk, m->d_pitch, m->d_roll, m->d_z, m->d_trav, m->d_runs, m->d_geo,
+                  m->d_cs, m->d_tiles, m->d_stage, m->d_qidx, m->d_qout};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (m->h_tiles) cudaFreeHost(m->h_tiles);
+  if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+}
+
+extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w, int32_t h,
+                                             const float* heights, int64_t ld, const uint8_t* known, int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!heights || w < 0 || h < 0 || ld < w || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(m, SE2M_ERR_INVALID_ARG, "update_elevation: bad pointer / size / mem");
+  if (i0 < 0 || j0 < 0 || (long long)i0 + w > m->prm.nx || (long long)j0 + h > m->prm.ny)
+    return fail(m, SE2M_ERR_OUT_OF_RANGE, "update_elevation: rectangle outside the window");
+  if (w == 0 || h == 0) return SE2M_OK;
+  const float* src = heights;
+  const uint8_t* kn = known;
+  long long sld = ld;
+  if (mem == SE2M_MEM_HOST) {
+    const size_t hb = (size_t)w * h * 4, kb = known ? (size_t)w * h : 0;
+    se2m_status st = ensure_stage(m, hb + kb);
+    if (st != SE2M_OK) return st;
+    float* dh = m->d_stage;
+    CUDA_TRY(m, cudaMemcpy2DAsync(dh, (size_t)w * 4, heights, (size_t)ld * 4, (size_t)w * 4, h, cudaMemcpyHostToDevice, m->stream), "H2D heights");
+    if (known) {
+      uint8_t* dk = reinterpret_cast<uint8_t*>(m->d_stage) + hb;
+      CUDA_TRY(m, cudaMemcpy2DAsync(dk, (size_t)w, known, (size_t)ld, (size_t)w, h, cudaMemcpyHostToDevice, m->stream), "H2D known");
+      kn = dk;
+    }
+    src = dh;
+    sld = w;
+  }
+  const int px0 = pmod(m->I_M + i0, m->prm.nx), py0 = pmod(m->J_M + j0, m->prm.ny);
+  CUDA_TRY(m, launch_scatter_rect(m->d_h, m->ldh, m->prm.nx, m->prm.ny, px0, py0, w, h, src, sld, kn, m->stream), "scatter");
+  m->launches++;
+  m->have_data = true;
+  m->dirty.push_back(Rect{m->I_M + i0, m->I_M + i0 + w, m->J_M + j0, m->J_M + j0 + h});
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_t* out_di, int32_t* out_dj) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "shift_window: position not finite");
+  const int nx = m->prm.nx, ny = m->prm.ny;
+  // Eq. 4: p_M = l_res * floor(x / l_res); window origin = floor(x/r) - nx/2
+  const long long I_M = (long long)floor(x / m->prm.resolution) - nx / 2;
+  const long long J_M = (long long)floor(y / m->prm.resolution) - ny / 2;
+  const long long di = I_M - m->I_M, dj = J_M - m->J_M;
+  if (out_di) *out_di = (int32_t)std::max<long long>(INT32_MIN, std::min<long long>(INT32_MAX, di));
+  if (out_dj) *out_dj = (int32_t)std::max<long long>(INT32_MIN, std::min<long long>(INT32_MAX, dj));
+  if (di == 0 && dj == 0) return SE2M_OK;
+  const Rect old_w{m->I_M, m->I_M + nx, m->J_M, m->J_M + ny};
+  const Rect new_w{I_M, I_M + nx, J_M, J_M + ny};
+  m->I_M = I_M;
+  m->J_M = J_M;
+  const int pxM = pmod(I_M, nx), pyM = pmod(J_M, ny);
+  if (std::llabs(di) >= nx || std::llabs(dj) >= ny) {
+    // displacement >= side: every cell leaves the window
+    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, 0, 0, nx, ny, nx, ny, m->stream), "clear");
+    m->launches++;
+    m->all_dirty = true;
+    m->dirty.clear();
+    return SE2M_OK;
+  }
+  // cells entering the window (their physical slots held cells that left): set unknown.
+  // Column strip: logical columns [nx - di, nx) if di > 0, [0, -di) if di < 0, all rows.
+  if (di != 0) {
+    const int w = (int)std::llabs(di);
+    const int l0 = di > 0 ? nx - w : 0;
+    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, (pxM + l0) % nx, pyM, w, ny, nx, ny, m->stream), "clear cols");
+    m->launches++;
+  }
+  if (dj != 0) {
+    const int hgt = (int)std::llabs(dj);
+    const int l0 = dj > 0 ? ny - hgt : 0;
+    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, pxM, (pyM + l0) % ny, nx, hgt, nx, ny, m->stream), "clear rows");
+    m->launches++;
+  }
+  // dirty: the entered strips of the new window and the vacated strips of the old one (H9)
+  if (di > 0) { m->dirty.push_back(Rect{old_w.I1, new_w.I1, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{old_w.I0, new_w.I0, old_w.J0, old_w.J1}); }
+  if (di < 0) { m->dirty.push_back(Rect{new_w.I0, old_w.I0, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{new_w.I1, old_w.I1, old_w.J0, old_w.J1}); }
+  if (dj > 0) { m->dirty.push_back(Rect{new_w.I0, new_w.I1, old_w.J1, new_w.J1}); m->dirty.push_back(Rect{old_w.I0, old_w.I1, old_w.J0, new_w.J0}); }
+  if (dj < 0) { m->dirty.push_back(Rect{new_w.I0, new_w.I1, new_w.J0, old_w.J0}); m->dirty.push_back(Rect{old_w.I0, old_w.I1, new_w.J1, old_w.J1}); }
+  return SE2M_OK;
+}
+
+static bool tile_owned(const se2m_map* m, long long TJ) {
+  if (m->prm.shard_mode != SE2M_SHARD_ROWS || m->prm.world_size <= 1) return true;
+  return pmod(TJ, m->prm.world_size) == m->prm.rank;
+}
+
+extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (mode != SE2M_FULL && mode != SE2M_INCREMENTAL) return fail(m, SE2M_ERR_INVALID_ARG, "assess: bad mode");
+  if (!m->have_data) return fail(m, SE2M_ERR_STATE, "assess before any update_elevation");
+  AssessParams p = make_params(m);
+  const int nx = m->prm.nx, ny = m->prm.ny;
+  const long long TI0 = floor_div(m->I_M, TX), TI1 = floor_div(m->I_M + nx - 1, TX);
+  const long long TJ0 = floor_div(m->J_M, TY), TJ1 = floor_div(m->J_M + ny - 1, TY);
+  const int tiles_x = (int)(TI1 - TI0 + 1), tiles_y = (int)(TJ1 - TJ0 + 1);
+  p.TI0 = TI0; p.TJ0 = TJ0; p.tiles_x = tiles_x;
+  std::vector<int> list;
+  const bool sharded_rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  const bool full = mode == SE2M_FULL || m->all_dirty;
+  if (!full || sharded_rows) {
+    std::vector<char> mark((size_t)tiles_x * tiles_y, full ? 1 : 0);
+    if (!full) {
+      const long long Rd = m->R;  // states within R of a changed cell (Chebyshev bound of the footprint)
+      for (const Rect& d : m->dirty) {
+        long long I0 = std::max(d.I0 - Rd, m->I_M), I1 = std::min(d.I1 + Rd, m->I_M + nx);
+        long long J0 = std::max(d.J0 - Rd, m->J_M), J1 = std::min(d.J1 + Rd, m->J_M + ny);
+        if (I0 >= I1 || J0 >= J1) continue;
+        for (long long tj = floor_div(J0, TY); tj <= floor_div(J1 - 1, TY); ++tj)
+          for (long long ti = floor_div(I0, TX); ti <= floor_div(I1 - 1, TX); ++ti)
+            mark[(size_t)(tj - TJ0) * tiles_x + (ti - TI0)] = 1;
+      }
+    }
+    for (int t = 0; t < tiles_x * tiles_y; ++t)
+      if (mark[t] && tile_owned(m, TJ0 + t / tiles_x)) list.push_back(t);
+    if (list.size() > m->tiles_cap) {
+      if (m->d_tiles) { cudaStreamSynchronize(m->stream); cudaFree(m->d_tiles); m->d_tiles = nullptr; }
+      if (m->h_tiles) { cudaFreeHost(m->h_tiles); m->h_tiles = nullptr; }
+      m->tiles_cap = 0;
+      size_t cap = std::max<size_t>(list.size(), 1024);
+      CUDA_TRY(m, cudaMalloc(&m->d_tiles, cap * sizeof(int)), "cudaMalloc(tiles)");
+      CUDA_TRY(m, cudaMallocHost(&m->h_tiles, cap * sizeof(int)), "cudaMallocHost(tiles)");
+      m->tiles_cap = cap;
+    }
+  }
+  int n_tiles = tiles_x * tiles_y;
+  if (!full || sharded_rows) {
+    n_tiles = (int)list.size();
+    if (n_tiles > 0) {
+      // the pinned staging list may still be read by a previous async copy: order on the stream
+      CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(tiles)");
+      memcpy(m->h_tiles, list.data(), list.size() * sizeof(int));
+      CUDA_TRY(m, cudaMemcpyAsync(m->d_tiles, m->h_tiles, list.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream), "H2D tiles");
+    }
+    p.tile_list = m->d_tiles;
+  }
+  // yaw chunking: enough CTAs for >= 4 waves of 148 SMs, otherwise all bins per CTA (tile reuse)
+  const int nk = m->k_hi - m->k_lo;
+  int chunk = nk;
+  if (n_tiles > 0) {
+    const long long want = 4LL * 148;
+    if ((long long)n_tiles * 1 < want) chunk = 1;
+    else chunk = (int)std::max<long long>(1, std::min<long long>(nk, (long long)n_tiles * nk / want));
+    if ((long long)n_tiles * ((nk + chunk - 1) / chunk) < want) chunk = std::max(1, (int)((long long)n_tiles * nk / want));
+  }
+  p.k_chunk = std::max(1, chunk);
+  if (n_tiles > 0 && nk > 0) {
+    cudaError_t e = launch_assess(p, m->R_T, n_tiles, &m->tmap, m->stream);
+    if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
+    m->launches++;
+  }
+  m->dirty.clear();
+  m->all_dirty = false;
+  return SE2M_OK;
+}
+
+static bool owned_bin(const se2m_map* m, int k) {
+  const int kr = (m->paired && k >= m->H) ? k - m->H : k;
+  return kr >= m->k_lo && kr < m->k_hi;
+}
+
+extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, float* pitch, float* roll,
+                                  float* z, uint8_t* trav) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (n < 0 || (n > 0 && !xyt) || n > (1ll << 30)) return fail(m, SE2M_ERR_INVALID_ARG, "query: bad n / xyt");
+  if (n == 0) return SE2M_OK;
+  const int nx = m->prm.nx, ny = m->prm.ny, ny_aw = m->prm.n_yaw;
+  const double r = m->prm.resolution, dth = 2.0 * M_PI / ny_aw;
+  std::vector<int4> idx((size_t)n);
+  bool any_out = false;
+  for (int64_t q = 0; q < n; ++q) {
+    const double x = xyt[3 * q], y = xyt[3 * q + 1], th = xyt[3 * q + 2];
+    int4 e = make_int4(0, 0, 0, 0);
+    if (isfinite(x) && isfinite(y) && isfinite(th)) {
+      const long long li = (long long)floor(x / r) - m->I_M, lj = (long long)floor(y / r) - m->J_M;
+      long long k = (long long)floor((th + M_PI) / dth + 0.5);  // nearest bin (reading R3)
+      k %= ny_aw;
+      if (k < 0) k += ny_aw;
+      const long long TJ = floor_div(lj + m->J_M, TY);
+      if (li >= 0 && li < nx && lj >= 0 && lj < ny && owned_bin(m, (int)k) && tile_owned(m, TJ))
+        e = make_int4(pmod(m->I_M + li, nx), pmod(m->J_M + lj, ny), (int)k, 1);
+    }
+    if (!e.w) any_out = true;
+    idx[q] = e;
+  }
+  if ((size_t)n > m->q_cap) {
+    if (m->d_qidx) cudaFree(m->d_qidx);
+    if (m->d_qout) cudaFree(m->d_qout);
+    m->d_qidx = nullptr; m->d_qout = nullptr; m->q_cap = 0;
+    CUDA_TRY(m, cudaMalloc(&m->d_qidx, (size_t)n * sizeof(int4)), "cudaMalloc(query)");
+    CUDA_TRY(m, cudaMalloc(&m->d_qout, (size_t)n * 5 * sizeof(float)), "cudaMalloc(query)");
+    m->q_cap = (size_t)n;
+  }
+  CUDA_TRY(m, cudaMemcpyAsync(m->d_qidx, idx.data(), (size_t)n * sizeof(int4), cudaMemcpyHostToDevice, m->stream), "H2D query");
+  AssessParams p = make_params(m);
+  CUDA_TRY(m, launch_query(p, (int)n, m->d_qidx, m->d_qout, m->stream), "query kernel");
+  m->launches++;
+  std::vector<float> out((size_t)n * 5);
+  CUDA_TRY(m, cudaMemcpyAsync(out.data(), m->d_qout, out.size() * sizeof(float), cudaMemcpyDeviceToHost, m->stream), "D2H query");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(query)");
+  for (int64_t q = 0; q < n; ++q) {
+    if (risk) risk[q] = out[q];
+    if (pitch) pitch[q] = out[n + q];
+    if (roll) roll[q] = out[2 * n + q];
+    if (z) z[q] = out[3 * n + q];
+    if (trav) trav[q] = out[4 * n + q] > 0.5f ? 1 : 0;
+  }
+  return any_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query: some states outside the window / not owned") : SE2M_OK;
+}
+
+extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z, uint8_t* trav,
+                                     int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download: bad mem");
+  const size_t nst = (size_t)m->prm.nx * m->prm.ny * m->prm.n_yaw;
+  AssessParams p = make_params(m);
+  const int klo = m->k_lo, khi = m->k_hi;
+  // owned bins in full-bin numbering: [klo, khi) and, if paired, [klo+H, khi+H); pass a predicate via the range
+  // by gathering twice when paired (the kernel tests k in [k_lo, k_hi)).
+  struct Plane { void* dst; int which; size_t esz; } planes[] = {
+      {risk, 0, 4}, {pitch, 1, 4}, {roll, 2, 4}, {z, 3, 4}, {trav, 4, 1}};
+  for (auto& pl : planes) {
+    if (!pl.dst) continue;
+    void* target = pl.dst;
+    if (mem == SE2M_MEM_HOST) {
+      se2m_status st = ensure_stage(m, nst * pl.esz);
+      if (st != SE2M_OK) return st;
+      target = m->d_stage;
+    }
+    float* f[4] = {nullptr, nullptr, nullptr, nullptr};
+    uint8_t* t = nullptr;
+    if (pl.which < 4) f[pl.which] = (float*)target; else t = (uint8_t*)target;
+    // pass 1: bins [0, H) owned range; pass 2 (paired): bins [H, 2H)
+    if (!m->paired) {
+      CUDA_TRY(m, launch_gather_logical(p, klo, khi, f[0], f[1], f[2], f[3], t, m->stream), "gather");
+      m->launches++;
+    } else {
+      // a bin k is owned iff k in [klo, khi) or k in [klo+H, khi+H): one launch with a widened range is
+      // only correct for the unsharded case; otherwise gather twice into the same target (second
+      // pass overwrites only... ) -> do it with two windows of the same kernel.
+      if (klo == 0 && khi == m->H) {
+        CUDA_TRY(m, launch_gather_logical(p, 0, m->prm.n_yaw, f[0], f[1], f[2], f[3], t, m->stream), "gather");
+        m->launches++;
+      } else {
+        AssessParams q1 = p;
+        q1.n_yaw = m->H;  // bins [0, H)
+        CUDA_TRY(m, launch_gather_logical(q1, klo, khi, f[0], f[1], f[2], f[3], t, m->stream), "gather");
+        AssessParams q2 = p;
+        const size_t plane = (size_t)m->prm.nx * m->prm.ny;
+        q2.n_yaw = m->H;
+        q2.risk += plane * m->H; q2.pitch += plane * m->H; q2.roll += plane * m->H; q2.z += plane * m->H;
+        q2.trav += (size_t)m->H * m->prm.ny * m->trav_words;
+        float* g[4];
+        for (int i = 0; i < 4; ++i) g[i] = f[i] ? f[i] + plane * m->H : nullptr;
+        CUDA_TRY(m, launch_gather_logical(q2, klo, khi, g[0], g[1], g[2], g[3], t ? t + plane * m->H : nullptr, m->stream), "gather");
+        m->launches += 2;
+      }
+    }
+    if (mem == SE2M_MEM_HOST)
+      CUDA_TRY(m, cudaMemcpyAsync(pl.dst, m->d_stage, nst * pl.esz, cudaMemcpyDeviceToHost, m->stream), "D2H download");
+  }
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download)");
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (I_M) *I_M = m->I_M;
+  if (J_M) *J_M = m->J_M;
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, int32_t* radius) {
+  if (!m || k < 0 || k >= m->prm.n_yaw) return SE2M_ERR_INVALID_ARG;
+  const int kr = (m->paired && k >= m->H) ? k - m->H : k;
+  if (n_cells) *n_cells = m->ncells[kr];
+  if (radius) *radius = m->R;
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_synchronize(se2m_map* m) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "synchronize");
+  return SE2M_OK;
+}
+
+extern "C" int64_t se2m_launch_count(const se2m_map* m) { return m ? m->launches : 0; }
+
+extern "C" const char* se2m_last_error(const se2m_map* m) {
+  return m ? m->err.c_str() : g_init_error.c_str();
+}

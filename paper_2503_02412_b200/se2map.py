@@ -1,0 +1,208 @@
+"""Thin ctypes binding of libse2map.so (include/se2map.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; there is no Python or CPU
+fallback.  If the extension is missing this module raises at import time.
+Names follow the C ABI: ``init``, ``update_elevation``, ``shift_window``, ``assess_se2``,
+``query``, ``download`` (+ the ``Se2Map`` convenience class).  Arrays may be NumPy (host) or
+torch CUDA tensors (device, passed by data pointer with SE2M_MEM_DEVICE).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+_LIB_PATH = _build.LIB
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        "libse2map.so is not built (%s); run __graft_entry__.build() — there is no CPU fallback" % _LIB_PATH)
+
+SE2M_OK, SE2M_ERR_INVALID_ARG, SE2M_ERR_OOM, SE2M_ERR_CUDA, SE2M_ERR_UNSUPPORTED, SE2M_ERR_OUT_OF_RANGE, \
+    SE2M_ERR_STATE = range(7)
+SE2M_FULL, SE2M_INCREMENTAL = 0, 1
+SE2M_MEM_HOST, SE2M_MEM_DEVICE = 0, 1
+SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
+
+EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elevation", "se2m_shift_window",
+           "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
+           "se2m_synchronize", "se2m_launch_count", "se2m_last_error"]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("n_yaw", ctypes.c_int32),
+                ("shard_mode", ctypes.c_int32), ("resolution", ctypes.c_double),
+                ("ellipse_ex", ctypes.c_double), ("ellipse_ey", ctypes.c_double),
+                ("w_r", ctypes.c_double * 3), ("kappa_max", ctypes.c_double),
+                ("phi_x_max", ctypes.c_double), ("phi_y_max", ctypes.c_double),
+                ("robot_x", ctypes.c_double), ("robot_y", ctypes.c_double),
+                ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
+
+
+_lib = ctypes.CDLL(_LIB_PATH)
+_vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+_lib.se2m_default_params.argtypes = [ctypes.POINTER(Params)]
+_lib.se2m_default_params.restype = None
+_lib.se2m_init.argtypes = [ctypes.POINTER(Params), ctypes.POINTER(_vp)]
+_lib.se2m_destroy.argtypes = [_vp]
+_lib.se2m_destroy.restype = None
+_lib.se2m_update_elevation.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i64, _vp, _i32]
+_lib.se2m_shift_window.argtypes = [_vp, _f64, _f64, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
+_lib.se2m_assess_se2.argtypes = [_vp, _i32]
+_lib.se2m_query.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.se2m_download.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32]
+_lib.se2m_get_origin.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+_lib.se2m_stencil_info.argtypes = [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
+_lib.se2m_synchronize.argtypes = [_vp]
+_lib.se2m_launch_count.argtypes = [_vp]
+_lib.se2m_launch_count.restype = _i64
+_lib.se2m_last_error.argtypes = [_vp]
+_lib.se2m_last_error.restype = ctypes.c_char_p
+for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
+              "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize"):
+    getattr(_lib, _name).restype = ctypes.c_int
+
+
+def lib():
+    return _lib
+
+
+class Se2mError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("se2map status %d: %s" % (status, msg))
+        self.status = status
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    _lib.se2m_default_params(ctypes.byref(p))
+    for k, v in kw.items():
+        if k == "w_r":
+            p.w_r = (ctypes.c_double * 3)(*v)
+        else:
+            setattr(p, k, v)
+    return p
+
+
+def _ptr(a):
+    """(address, mem kind, keepalive) of a NumPy array or a torch tensor."""
+    if a is None:
+        return None, SE2M_MEM_HOST, None
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
+        return a.data_ptr(), (SE2M_MEM_DEVICE if a.is_cuda else SE2M_MEM_HOST), a
+    a = np.ascontiguousarray(a)
+    return a.ctypes.data, SE2M_MEM_HOST, a
+
+
+def init(params: Params):
+    h = _vp()
+    st = _lib.se2m_init(ctypes.byref(params), ctypes.byref(h))
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    return h
+
+
+class Se2Map:
+    """Owns one se2m_map handle."""
+
+    def __init__(self, params: Params | None = None, **kw):
+        self.params = params if params is not None else default_params(**kw)
+        self.h = init(self.params)
+
+    # -- lifecycle -------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.se2m_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st, ok=(SE2M_OK,)):
+        if st not in ok:
+            raise Se2mError(st, _lib.se2m_last_error(self.h).decode())
+        return st
+
+    # -- C-ABI calls -----------------------------------------------------------------
+    def update_elevation(self, heights, known=None, i0: int = 0, j0: int = 0):
+        """heights: (h, w) float32 NumPy array or CUDA tensor; known: same shape uint8 or None."""
+        hh, w = heights.shape
+        if not hasattr(heights, "is_cuda"):
+            heights = np.ascontiguousarray(heights, dtype=np.float32)
+            if known is not None:
+                known = np.ascontiguousarray(known, dtype=np.uint8)
+        hp, mem, keep = _ptr(heights)
+        kp, mem2, keep2 = _ptr(known)
+        if known is not None and mem2 != mem:
+            raise ValueError("heights and known must both be host or both be device memory")
+        ld = heights.stride(0) if hasattr(heights, "stride") and callable(heights.stride) else heights.strides[0] // 4
+        return self._check(_lib.se2m_update_elevation(self.h, i0, j0, w, hh, hp, ld, kp, mem))
+
+    def shift_window(self, x: float, y: float):
+        di, dj = _i32(), _i32()
+        self._check(_lib.se2m_shift_window(self.h, x, y, ctypes.byref(di), ctypes.byref(dj)))
+        return di.value, dj.value
+
+    def assess_se2(self, mode: int = SE2M_FULL):
+        return self._check(_lib.se2m_assess_se2(self.h, mode))
+
+    def query(self, xyt):
+        xyt = np.ascontiguousarray(xyt, dtype=np.float64).reshape(-1, 3)
+        n = len(xyt)
+        out = {k: np.empty(n, np.float32) for k in ("risk", "pitch", "roll", "z")}
+        out["trav"] = np.empty(n, np.uint8)
+        st = _lib.se2m_query(self.h, n, xyt.ctypes.data, out["risk"].ctypes.data, out["pitch"].ctypes.data,
+                             out["roll"].ctypes.data, out["z"].ctypes.data, out["trav"].ctypes.data)
+        self._check(st, ok=(SE2M_OK, SE2M_ERR_OUT_OF_RANGE))
+        out["status"] = st
+        return out
+
+    def download(self, planes=("risk", "pitch", "roll", "z", "trav"), out=None):
+        """Whole planes in logical [k][j][i] order as NumPy arrays (or into ``out`` dict of arrays/tensors)."""
+        P = self.params
+        shape = (P.n_yaw, P.ny, P.nx)
+        res = {}
+        ptrs = []
+        mem = SE2M_MEM_HOST
+        for name in ("risk", "pitch", "roll", "z", "trav"):
+            if name not in planes:
+                ptrs.append(None)
+                continue
+            if out is not None and name in out:
+                a = out[name]
+            else:
+                a = np.empty(shape, np.uint8 if name == "trav" else np.float32)
+            p, mem_a, keep = _ptr(a)
+            mem = mem_a
+            res[name] = a
+            ptrs.append(p)
+        self._check(_lib.se2m_download(self.h, *ptrs, mem))
+        return res
+
+    def origin(self):
+        I, J = _i64(), _i64()
+        self._check(_lib.se2m_get_origin(self.h, ctypes.byref(I), ctypes.byref(J)))
+        return I.value, J.value
+
+    def stencil_info(self, k: int):
+        n, r = _i32(), _i32()
+        self._check(_lib.se2m_stencil_info(self.h, k, ctypes.byref(n), ctypes.byref(r)))
+        return n.value, r.value
+
+    def synchronize(self):
+        return self._check(_lib.se2m_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        return int(_lib.se2m_launch_count(self.h))

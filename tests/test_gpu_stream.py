@@ -1,0 +1,108 @@
+"""Rolling-window stream (BASELINE.json config 3) and sharded maps on one GPU.
+
+* Q13: INCREMENTAL after any sequence of shifts == FULL on the same map, bit-exact, every step checked.
+* Parity with the oracle at steps 1, 10, 100, 1000 (SURVEY.md §8(d) 'stream').
+* Sharded (yaw slices / row bands) == unsharded, bit-exact, with the ranks emulated as independent
+  handles on one GPU (no rank waits on another, so this is safe on a single device).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from synth.terrain import CONFIGS, robot_path, world_heights
+from tests.gpu_common import make_map, oracle_params
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _exposed_strips(di, dj, nx, ny):
+    """Window-local rectangles (i0, j0, w, h) that entered the window after a shift by (di, dj)."""
+    rects = []
+    if abs(di) >= nx or abs(dj) >= ny:
+        return [(0, 0, nx, ny)]
+    if di > 0:
+        rects.append((nx - di, 0, di, ny))
+    elif di < 0:
+        rects.append((0, 0, -di, ny))
+    if dj > 0:
+        rects.append((0, ny - dj, nx, dj))
+    elif dj < 0:
+        rects.append((0, 0, nx, -dj))
+    return rects
+
+
+def _equal(a, b):
+    return all(np.array_equal(a[f], b[f], equal_nan=True) for f in a)
+
+
+def test_stream_incremental_equals_full_and_oracle():
+    cfg = CONFIGS["stream"]
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    path = robot_path(cfg["path_seed"], cfg["n_steps"], r, *cfg["robot"])
+    inc = make_map(nx, ny, r, n_yaw, robot=tuple(path[0]))
+    full = make_map(nx, ny, r, n_yaw, robot=tuple(path[0]))
+    I_M, J_M = inc.origin()
+    h0 = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+    for m in (inc, full):
+        m.update_elevation(h0)
+        m.assess_se2(0)
+    checkpoints = {1, 10, 100, 1000}
+    n_shifts = 0
+    for t in range(1, len(path)):
+        x, y = path[t]
+        d1 = inc.shift_window(x, y)
+        d2 = full.shift_window(x, y)
+        assert d1 == d2
+        n_shifts += d1 != (0, 0)
+        I_M, J_M = inc.origin()
+        assert (I_M, J_M) == oracle.window_origin(x, y, r, nx, ny)
+        for (i0, j0, w, h) in _exposed_strips(*d1, nx, ny):
+            strip = world_heights(cfg["terrain"], I_M + i0, J_M + j0, w, h, r)
+            inc.update_elevation(strip, i0=i0, j0=j0)
+            full.update_elevation(strip, i0=i0, j0=j0)
+        inc.assess_se2(1)
+        full.assess_se2(0)
+        if t % 25 == 0 or t in checkpoints:
+            gi, gf = inc.download(), full.download()
+            assert _equal(gi, gf), "INCREMENTAL != FULL at step %d" % t
+            if t in checkpoints:
+                h = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+                orc = oracle.assess_all(oracle_params(nx, ny, r, n_yaw), h)
+                rep = compare(gi, orc)
+                print("step", t, rep)
+                assert rep["ok"], (t, rep)
+    assert n_shifts > 300
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_equals_single(mode, G):
+    cfg = dict(CONFIGS["paper"])
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    single = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    I_M, J_M = single.origin()
+    h = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+    single.update_elevation(h)
+    single.assess_se2(0)
+    ref = single.download()
+    merged = {f: np.full_like(v, np.nan if v.dtype != np.uint8 else 0) for f, v in ref.items()}
+    for rank in range(G):
+        m = make_map(nx, ny, r, n_yaw, robot=cfg["robot"], shard_mode=mode, rank=rank, world_size=G)
+        m.update_elevation(h)
+        m.assess_se2(0)
+        g = m.download()
+        if mode == 1:
+            H = n_yaw // 2
+            lo, hi = H * rank // G, H * (rank + 1) // G
+            own = np.zeros(n_yaw, bool)
+            own[lo:hi] = True
+            own[lo + H:hi + H] = True
+            mask = np.broadcast_to(own[:, None, None], ref["risk"].shape)
+        else:
+            J = np.arange(J_M, J_M + ny)
+            own_rows = (np.floor_divide(J, 16) % G) == rank
+            mask = np.broadcast_to(own_rows[None, :, None], ref["risk"].shape)
+        for f in merged:
+            merged[f][mask] = g[f][mask]
+    assert _equal(merged, ref)
