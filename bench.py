@@ -1,0 +1,474 @@
+#!/usr/bin/env python
+"""Benchmark of the SE(2) traversability hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config large] [--impl ours|reference]
+
+A step = one pass of the whole hot path over the configuration's
+map: shift_window (Eq. 4, the robot moves along a path), update_elevation (the full window,
+from an HBM-resident world buffer for `value`, from pinned host memory for `e2e`), assess_se2
+FULL (Alg. 1 for every SE(2) state), and a batch query of planner states.  Prints ONE JSON line
+on rank 0.  Under torchrun (N > 1) the states are sharded by interleaved tile rows
+(SE2M_SHARD_ROWS), no data-path collective; value = all ranks' states / max-over-ranks time.
+
+`--impl reference`: the FP64 CPU oracle (oracle/, the test reference) timed as it stands on this
+host's cores on a bounded random sample of the same workload per step (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.terrain import CONFIGS, DEFAULT_RISK, world_heights  # noqa: E402
+
+METRIC = "SE(2) cells assessed/sec (full local-map update)"
+UNIT = "states/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="large", choices=["large", "highres", "paper", "tiny"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--queries", type=int, default=4096)
+    return ap.parse_args()
+
+
+def stencil_cells(cfg):
+    """Mean |P_k| (footprint cells) over yaw bins: for the roofline's per-state work.
+    Counted from the oracle-independent rule R5 re-stated here (host arithmetic, no library code)."""
+    r, ex, ey, n = cfg["r"], cfg["ex"], cfg["ey"], cfg["n_yaw"]
+    a, b = ex / r, ey / r
+    R = int(math.ceil(max(a, b))) + 1
+    di, dj = np.meshgrid(np.arange(-R, R + 1), np.arange(-R, R + 1))
+    tot = 0
+    for k in range(n):
+        kr = k % (n // 2) if n % 2 == 0 else k
+        th = -math.pi + 2 * math.pi * kr / n
+        u = di * math.cos(th) + dj * math.sin(th)
+        v = -di * math.sin(th) + dj * math.cos(th)
+        tot += int(((u / a) ** 2 + (v / b) ** 2 <= 1 + 1e-9).sum())
+    return tot / n
+
+
+def robot_positions(cfg, n):
+    """A deterministic back-and-forth path (2-3 cells per step) so the window really shifts."""
+    x0, y0 = cfg["robot"]
+    r = cfg["r"]
+    out = []
+    for t in range(n):
+        ph = t % 16
+        s = ph if ph < 8 else 16 - ph
+        out.append((x0 + 0.23 * s + 0.013, y0 + 0.17 * s + 0.011))
+    return out, int(math.ceil(0.23 * 8 / r)) + 2
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (pynvml) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------------
+def cpu_oracle_rate(cfg, h, budget_s=15.0, seed=0, nthreads=None):
+    """The FP64 oracle as it stands, on a bounded uniform random sample of the workload's states."""
+    import oracle
+    P = oracle.Params(nx=cfg["nx"], ny=cfg["ny"], resolution=cfg["r"], n_yaw=cfg["n_yaw"], ex=cfg["ex"],
+                      ey=cfg["ey"], **DEFAULT_RISK)
+    nthreads = nthreads or oracle.default_threads()
+    rng = np.random.default_rng(seed)
+    n, done, t_tot = 20000, 0, 0.0
+    while t_tot < budget_s:
+        ijk = np.stack([rng.integers(0, cfg["nx"], n), rng.integers(0, cfg["ny"], n),
+                        rng.integers(0, cfg["n_yaw"], n)], axis=1).astype(np.int32)
+        t0 = time.perf_counter()
+        oracle.assess_states(P, h, ijk, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+        t_tot += dt
+        done += n
+        n = int(min(max(n * 2, 1), max(20000, done / max(t_tot, 1e-9) * (budget_s - t_tot) + 1)))
+    return done / t_tot, done, t_tot, nthreads
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    x, y = cfg["robot"]
+    import oracle
+    I_M, J_M = oracle.window_origin(x, y, cfg["r"], cfg["nx"], cfg["ny"])
+    h = world_heights(cfg["terrain"], I_M, J_M, cfg["nx"], cfg["ny"], cfg["r"])
+    per_step = float(os.environ.get("BENCH_REF_STEP_S", "6"))
+    for _ in range(args.warmup):
+        cpu_oracle_rate(cfg, h, budget_s=min(1.0, per_step / 4))
+    rates, states, secs = [], 0, 0.0
+    thr = None
+    for s in range(args.steps):
+        rate, n, t, thr = cpu_oracle_rate(cfg, h, budget_s=per_step, seed=s + 1)
+        rates.append(rate)
+        states += n
+        secs += t
+    value = states / secs
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (T_hills seed 5, SURVEY.md §8(d)); random-init-free: no weights",
+            "config": {"workload": args.config, "nx": cfg["nx"], "ny": cfg["ny"], "n_yaw": cfg["n_yaw"],
+                       "resolution_m": cfg["r"], "footprint_m": [cfg["ex"], cfg["ey"]]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                             "sample": "per step: uniform random (i,j,k) states of the %s window, ~%.0f s of "
+                                       "FP64 oracle work (%d states total)" % (args.config, per_step, states)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_02412_b200 import se2map as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    n_states = nx * ny * n_yaw
+    K, W = args.steps, max(args.warmup, 3)
+    positions, margin = robot_positions(cfg, K + W + 2)
+
+    import oracle  # window arithmetic only (Eq. 4 origin) and the cpu_baseline leg
+    I_M0, J_M0 = oracle.window_origin(*cfg["robot"], r, nx, ny)
+    # world buffer covering every window of the path, resident in HBM (inputs of `value`)
+    WX, WY = nx + 2 * margin, ny + 2 * margin
+    WI0, WJ0 = I_M0 - margin, J_M0 - margin
+    t0 = time.time()
+    world_h = world_heights(cfg["terrain"], WI0, WJ0, WX, WY, r)
+    gen_s = time.time() - t0
+    world_d = torch.from_numpy(world_h).to(dev)
+    world_pinned = torch.from_numpy(world_h).pin_memory()
+
+    shard = S.SE2M_SHARD_ROWS if world > 1 else S.SE2M_SHARD_NONE
+    m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
+                 robot_x=cfg["robot"][0], robot_y=cfg["robot"][1], device=local, shard_mode=shard,
+                 rank=rank, world_size=world, cuda_stream=stream.cuda_stream)
+    rng = np.random.default_rng(1)
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def window_view(src, I_M, J_M):
+        oi, oj = I_M - WI0, J_M - WJ0
+        return src[oj:oj + ny, oi:oi + nx]
+
+    def queries(I_M, J_M):
+        nq = args.queries
+        return np.stack([rng.uniform(I_M * r, (I_M + nx) * r, nq), rng.uniform(J_M * r, (J_M + ny) * r, nq),
+                         rng.uniform(-math.pi, math.pi, nq)], axis=1)
+
+    def step(t, src):
+        m.shift_window(*positions[t])
+        I_M, J_M = m.origin()
+        m.update_elevation(window_view(src, I_M, J_M))
+        m.assess_se2(S.SE2M_FULL)
+        return I_M, J_M
+
+    # ---- device-resident `value` ----------------------------------------------------------------
+    with torch.cuda.stream(stream):
+        for t in range(W):
+            I_M, J_M = step(t, world_d)
+            m.query(queries(I_M, J_M))
+        stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        qs = [None] * K
+        launches0 = m.launch_count()
+        with ClockSampler(local) as clk:
+            for t in range(K):
+                l2_flush.zero_()                    # L2 flush between timed steps (outside the events)
+                tt = W + t
+                ev[t][0].record(stream)
+                m.shift_window(*positions[tt])
+                I_M, J_M = m.origin()
+                m.update_elevation(window_view(world_d, I_M, J_M))
+                evk[t][0].record(stream)
+                m.assess_se2(S.SE2M_FULL)
+                evk[t][1].record(stream)
+                q = m.query(queries(I_M, J_M))     # H10 (synchronises: the planner reads the map)
+                ev[t][1].record(stream)
+                qs[t] = q
+            stream.synchronize()
+        launches = m.launch_count() - launches0
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        kern_ms = [a.elapsed_time(b) for a, b in evk]
+    tot_s = sum(step_ms) / 1e3
+    kern_s = sum(kern_ms) / 1e3
+    if world > 1:
+        tt_ = torch.tensor([tot_s, kern_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        tot_s, kern_s = tt_.tolist()
+    value = n_states * K / tot_s
+
+    # ---- e2e: public API with host buffers (H2D of the step's map from pinned memory, D2H of the
+    #      risk map to pinned memory: the paper sends the risk map back to the CPU) -----
+    e2e = None
+    if not args.no_e2e:
+        risk_host = torch.empty((n_yaw, ny, nx), dtype=torch.float32).pin_memory()
+        ke = max(2, min(K, 5))
+        with torch.cuda.stream(stream):
+            for t in range(2):                      # warm the staging buffers
+                m.shift_window(*positions[t])
+                I_M, J_M = m.origin()
+                m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
+                m.assess_se2(S.SE2M_FULL)
+                m.download(planes=("risk",), out={"risk": risk_host})
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for t in range(ke):
+                m.shift_window(*positions[W + t])
+                I_M, J_M = m.origin()
+                m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
+                m.assess_se2(S.SE2M_FULL)
+                m.download(planes=("risk",), out={"risk": risk_host})
+            e1.record(stream)
+            stream.synchronize()
+            e2e_s = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            tt_ = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+            e2e_s = tt_.item()
+        e2e = {"value": n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
+               "d2h_bytes_per_step": n_states * 4, "ms_per_step": e2e_s / ke * 1e3, "steps": ke,
+               "note": "H2D of the full window from pinned host memory + assess FULL + D2H of the risk map "
+                       "(logical order) to pinned host memory, per step"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (assess_kernel) -----------------------------------------------
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = n_sm * 128 * sm_max * 1e6 / 1e12      # FP32-pipe lane-ops/s (FMA = 1 op), Tops/s
+    Pk = stencil_cells(cfg)
+    W_state = 4 * Pk + 200                           # SURVEY.md §8(d) algorithmic ops per state
+    states_per_launch = n_states / world
+    t_kernel = kern_s / K                            # per launch (update scatter included: < 1%)
+    achieved = states_per_launch * W_state / t_kernel / 1e12
+    bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
+    hbm_gbs = states_per_launch * bytes_state / t_kernel / 1e9
+    hbm_peak = peaks.get("hbm_gbs", 6450.6)
+    prof = {}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")))
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Tops/s (FP32-pipe ops, FMA=1)",
+                "frac": achieved / alu_peak, "traffic": prof.get("dram_bytes_per_launch"),
+                "kernel": "assess_kernel", "ms_per_launch": t_kernel * 1e3,
+                "ops_per_state": W_state, "mean_footprint_cells": Pk,
+                "peak_source": "148 SMs x 128 FP32 lanes x sm_max_mhz (B200_PROFILING.md unit counts; "
+                               "FFMA2/FADD measured at 128 lanes/clk/SM in profiles/r01_pipes_microbench.json)",
+                "effective": True,
+                "note": "achieved counts the paper-algorithm work W = 4|P_k| + 200 FP32 ops/state (SURVEY.md §8(d)); "
+                        "the kernel computes the same sums with prefix differences over <= 2R+1 stencil rows and "
+                        "shares one eigen-solve between yaw bins k and k + n/2, so frac can exceed 1",
+                "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
+                        "bytes_per_state": bytes_state}}
+    if prof:
+        roofline["ncu"] = {k: v for k, v in prof.items() if k != "dram_bytes_per_launch"}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        h = world_heights(cfg["terrain"], *m.origin(), nx, ny, r)
+        rate, n_done, secs, thr = cpu_oracle_rate(cfg, h, budget_s=float(os.environ.get("BENCH_CPU_S", "15")))
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": "%d uniform random (i,j,k) states of the %s window (FP64 C oracle, %.1f s)"
+                         % (n_done, args.config, secs)}
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        extras = small_configs(S, stream, torch)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: T_hills seed 5 (sinusoid hills, slope_rms 0.5, rocks, 1 cm noise; SURVEY.md §8(d)); "
+                    "no weights",
+            "config": {"workload": args.config, "nx": nx, "ny": ny, "n_yaw": n_yaw, "resolution_m": r,
+                       "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": n_states,
+                       "parallelism": "rows%d" % world if world > 1 else "single",
+                       "l2": "256 MB buffer written between timed steps (outside the step events); "
+                             "each step also writes %.2f GB of outputs" % (n_states * 16.125 / 1e9),
+                       "step": "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
+                               "query(%d states)" % args.queries},
+            "ms_per_full_update": kern_s / K * 1e3,
+            "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline, "e2e": e2e,
+            "cpu_baseline": cpu, "extras": extras,
+            "setup": {"terrain_gen_s": round(gen_s, 2)}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def exposed_strips(di, dj, nx, ny):
+    """Window-local rectangles (i0, j0, w, h) that entered the window after a shift by (di, dj)."""
+    if abs(di) >= nx or abs(dj) >= ny:
+        return [(0, 0, nx, ny)]
+    rects = []
+    if di > 0:
+        rects.append((nx - di, 0, di, ny))
+    elif di < 0:
+        rects.append((0, 0, -di, ny))
+    if dj > 0:
+        rects.append((0, ny - dj, nx, dj))
+    elif dj < 0:
+        rects.append((0, 0, nx, -dj))
+    return rects
+
+
+def small_configs(S, stream, torch):
+    """paper-like FULL update time and the rolling-window stream step (INCREMENTAL), in microseconds."""
+    out = {}
+    from synth.terrain import robot_path
+    import oracle
+    for name in ("paper", "stream"):
+        cfg = CONFIGS[name]
+        nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+        m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
+                     robot_x=cfg["robot"][0], robot_y=cfg["robot"][1], cuda_stream=stream.cuda_stream)
+        I_M, J_M = m.origin()
+        h = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+        with torch.cuda.stream(stream):
+            hd = torch.from_numpy(h).cuda()
+            m.update_elevation(hd)
+            if name == "paper":
+                for _ in range(10):
+                    m.assess_se2(0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(100):
+                    m.assess_se2(0)
+                e1.record(stream)
+                stream.synchronize()
+                out["paper_full_us"] = e0.elapsed_time(e1) * 10.0
+                out["paper_states"] = nx * ny * n_yaw
+            else:
+                path = robot_path(cfg["path_seed"], 300, r, *cfg["robot"])
+                # strips come from a pre-generated world patch covering the path
+                xs, ys = path[:, 0], path[:, 1]
+                I0 = int(math.floor(xs.min() / r)) - nx // 2 - 2
+                J0 = int(math.floor(ys.min() / r)) - ny // 2 - 2
+                Wd = int(math.ceil((xs.max() - xs.min()) / r)) + nx + 6
+                Hd = int(math.ceil((ys.max() - ys.min()) / r)) + ny + 6
+                wh = torch.from_numpy(world_heights(cfg["terrain"], I0, J0, Wd, Hd, r)).cuda()
+                m.assess_se2(0)
+                ts = []
+                warm = 20                            # first steps: allocations / first-launch setup
+                for t in range(1, len(path)):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    di, dj = m.shift_window(*path[t])
+                    I_M, J_M = m.origin()
+                    for (i0, j0, w, hh) in exposed_strips(di, dj, nx, ny):
+                        m.update_elevation(wh[J_M - J0 + j0:J_M - J0 + j0 + hh, I_M - I0 + i0:I_M - I0 + i0 + w],
+                                           i0=i0, j0=j0)
+                    m.assess_se2(1)
+                    e1.record(stream)
+                    if t > warm:
+                        ts.append((e0, e1))
+                stream.synchronize()
+                us = sorted(a.elapsed_time(b) * 1e3 for a, b in ts)
+                out["stream_us_per_step_mean"] = sum(us) / len(us)
+                out["stream_us_per_step_p99"] = us[int(0.99 * (len(us) - 1))]
+                out["stream_steps"] = len(us)
+        m.close()
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,10 @@ se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
 /* Number of footprint cells |P_k| for yaw bin k (0 <= k < n_yaw) and the stencil radius R. */
 se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, int32_t* radius);
 
+/* World-aligned tile of states one CTA assesses: TX columns x TY rows (SE2M_SHARD_ROWS gives world
+ * tile row TJ = floor(J / TY) to rank TJ mod world_size). */
+se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_t* tile_y);
+
 /* Block until all work queued on the handle's stream is done. */
 se2m_status se2m_synchronize(se2m_map* m);
 

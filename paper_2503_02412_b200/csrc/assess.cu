@@ -15,7 +15,7 @@
 //      refinement (GetMinEigenVecWithCurv, line 9), kappa, Eqs. 2-3 frame, pitch/roll (lines
 //      12-13), thresholds and weighted risk (lines 10-18), written for bin k AND bin k + n/2
 //      (x_yaw negated: pitch/roll negated, everything else identical — pin Q3);
-//   5. coalesced stores to SoA planes + ballot-packed traversable bits.
+//   5. coalesced 16-B stores of (risk, pitch, roll, z) state records + ballot-packed traversable bits.
 // No tensor cores: the path is not a dense contraction.
 #include <math.h>
 #include <stdint.h>
@@ -67,6 +67,50 @@ __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
   return v;
 }
 
+// Packed FP32x2 (sm_100a FADD2): two lanes of arithmetic per issue slot.
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 bits_f2(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
+}
+// MUFU approximations (relative error ~1 ulp); the eigenvector refinement absorbs them.
+__device__ __forceinline__ float frcp(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float fsqrt(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+// acos on [-1, 1]: Abramowitz & Stegun 4.4.46, acos(a) = sqrt(1 - a) * P7(a) for a in [0, 1].
+__device__ __forceinline__ float acos_fast(float x) {
+  const float a = fabsf(x);
+  float pz = fmaf(-0.0012624911f, a, 0.0066700901f);
+  pz = fmaf(pz, a, -0.0170881256f);
+  pz = fmaf(pz, a, 0.0308918810f);
+  pz = fmaf(pz, a, -0.0501743046f);
+  pz = fmaf(pz, a, 0.0889789874f);
+  pz = fmaf(pz, a, -0.2145988016f);
+  pz = fmaf(pz, a, 1.5707963050f);
+  const float r = fsqrt(1.f - a) * pz;
+  return x < 0.f ? 3.14159265358979f - r : r;
+}
+// asin on [-1, 1], branch-free Cephes asinf (odd: asin(-x) = -asin(x), asin(0) = 0 exactly).
+__device__ __forceinline__ float asin_fast(float x) {
+  const float a = fabsf(x);
+  const bool big = a > 0.5f;
+  const float z = big ? 0.5f * (1.f - a) : a * a;
+  const float s = big ? fsqrt(z) : a;
+  float pz = fmaf(4.2163199048e-2f, z, 2.4181311049e-2f);
+  pz = fmaf(pz, z, 4.5470025998e-2f);
+  pz = fmaf(pz, z, 7.4953002686e-2f);
+  pz = fmaf(pz, z, 1.6666752422e-1f);
+  float r = fmaf(s * z, pz, s);
+  r = big ? fmaf(-2.f, r, 1.57079632679489662f) : r;
+  return copysignf(r, x);
+}
+
 struct StateOut {
   float risk, pitch, roll, z;
   int trav;
@@ -84,7 +128,7 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
   o.pitch = o.roll = o.z = __int_as_float(0x7fc00000);
   o.trav = 0;
   if (N < 2.5f) return o;  // |P| < 3: unknown (reading R8)
-  const float invN = 1.f / N;
+  const float invN = frcp(N);
   const float mx = Sx * invN, my = Sy * invN, mh = S0 * invN;
   if (general) {
     // collinear footprint cells (exact integer moments): degenerate covariance (reading R11)
@@ -104,31 +148,31 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
   const float tr = C00 + C11 + C22;
   const float q = tr * (1.f / 3.f);
   const float b00 = C00 - q, b11 = C11 - q, b22 = C22 - q;
-  const float p2 = b00 * b00 + b11 * b11 + b22 * b22 + 2.f * (C01 * C01 + C02 * C02 + C12 * C12);
+  const float p2 = (b00 * b00 + b11 * b11 + b22 * b22 + 2.f * (C01 * C01 + C02 * C02 + C12 * C12)) * (1.f / 6.f);
   if (!(p2 > 0.f)) return o;  // isotropic: no unique normal
-  const float pp = sqrtf(p2 * (1.f / 6.f));
-  const float ip = 1.f / pp;
+  const float ip = rsqrtf(p2);
+  const float pp = p2 * ip;
   const float d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = C01 * ip, e02 = C02 * ip, e12 = C12 * ip;
   const float detB = d00 * (d11 * d22 - e12 * e12) - e01 * (e01 * d22 - e12 * e02) + e02 * (e01 * e12 - d11 * e02);
   const float hr = fminf(1.f, fmaxf(-1.f, 0.5f * detB));
-  const float phi = acosf(hr) * (1.f / 3.f);
-  const float lam0 = fmaf(2.f * pp, cosf(phi + 2.09439510239319549f), q);
+  const float phi = acos_fast(hr) * (1.f / 3.f);
+  float sphi, cphi;
+  __sincosf(phi, &sphi, &cphi);
+  const float lam0 = fmaf(-pp, fmaf(1.73205080756887729f, sphi, cphi), q);  // q + 2p cos(phi + 2pi/3)
   // eigenvector: largest cross product of two rows of M = C - lam0 I (columns of adj(M))
   const float m00 = C00 - lam0, m11 = C11 - lam0, m22 = C22 - lam0;
   const float a0 = C01 * C12 - C02 * m11, a1 = C02 * C01 - m00 * C12, a2 = m00 * m11 - C01 * C01;  // r0 x r1
   const float b0 = C01 * m22 - C02 * C12, b1 = C02 * C02 - m00 * m22, b2 = m00 * C12 - C01 * C02;  // r0 x r2
   const float c0 = m11 * m22 - C12 * C12, c1 = C12 * C02 - C01 * m22, c2 = C01 * C12 - m11 * C02;  // r1 x r2
   const float na = a0 * a0 + a1 * a1 + a2 * a2, nb = b0 * b0 + b1 * b1 + b2 * b2, nc = c0 * c0 + c1 * c1 + c2 * c2;
-  float v0, v1, v2;
-  if (na >= nb && na >= nc) { v0 = a0; v1 = a1; v2 = a2; }
-  else if (nb >= nc) { v0 = b0; v1 = b1; v2 = b2; }
-  else { v0 = c0; v1 = c1; v2 = c2; }
+  const bool pa = na >= nb && na >= nc, pb = !pa && nb >= nc;
+  const float v0 = pa ? a0 : (pb ? b0 : c0), v1 = pa ? a1 : (pb ? b1 : c1), v2 = pa ? a2 : (pb ? b2 : c2);
   // one inverse-iteration step with the same shift: x = adj(M) v = v0 (r1 x r2) + v1 (r2 x r0) + v2 (r0 x r1)
   float x0 = v0 * c0 - v1 * b0 + v2 * a0;
   float x1 = v0 * c1 - v1 * b1 + v2 * a1;
   float x2 = v0 * c2 - v1 * b2 + v2 * a2;
   float nx2 = x0 * x0 + x1 * x1 + x2 * x2;
-  if (!(nx2 > 0.f) || !isfinite(nx2)) {
+  if (!(nx2 > 0.f) || !(nx2 < 3.0e38f)) {
     x0 = v0; x1 = v1; x2 = v2;
     nx2 = x0 * x0 + x1 * x1 + x2 * x2;
     if (!(nx2 > 0.f)) return o;
@@ -142,9 +186,9 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
   const float t1 = C01 * n0 + C11 * n1 + C12 * n2;
   const float t2 = C02 * n0 + C12 * n1 + C22 * n2;
   const float lmin = fmaxf(0.f, n0 * t0 + n1 * t1 + n2 * t2);
-  const float kappa = lmin / tr;
+  const float kappa = lmin * frcp(tr);
   // z = f_1: fitted plane at the state centre (reading R14)
-  o.z = href + mh + r * (n0 * mx + n1 * my) / n2;
+  o.z = href + fmaf(r * (n0 * mx + n1 * my), frcp(n2), mh);
   // Eqs. 2-3 reduced by the vector triple product: b3.x_b = -n_z u / |n x x_yaw|,
   // b3.y_b = (n_x sin - n_y cos) / |n x x_yaw|, |n x x_yaw|^2 = n_z^2 + (n_x sin - n_y cos)^2
   const float u = n0 * csk.x + n1 * csk.y;
@@ -152,8 +196,8 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
   const float rs = rsqrtf(fmaf(n2, n2, t * t));
   const float sp = fminf(1.f, fmaxf(-1.f, -n2 * u * rs));
   const float sr = fminf(1.f, fmaxf(-1.f, t * rs));
-  o.pitch = asinf(sp);
-  o.roll = asinf(sr);
+  o.pitch = asin_fast(sp);
+  o.roll = asin_fast(sr);
   const float ax = fabsf(o.pitch), ay = fabsf(o.roll);
   // Alg. 1 lines 10-18 (strict >, reading R15); risk = w . [k/kmax, phx/phxmax, phy/phymax]
   const bool early = (kappa > p.kappa_max) || (ax > p.phi_x_max) || (ay > p.phi_y_max);
@@ -167,27 +211,28 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
 // ------------------------------------------------------------------------------------------
 template <int R_T>
 struct Geom {
-  static constexpr int HX = TX + 2 * R_T;   // halo width (cells)
-  static constexpr int HY = TY + 2 * R_T;   // halo height
-  static constexpr int PW = HX + 1;         // prefix row length (exclusive prefix, entry 0 = 0)
-  static constexpr int NR = 2 * R_T + 1;    // stencil rows
+  static constexpr int TY = tile_rows(R_T);
+  static constexpr int RPW = TY / NWARPS;    // tile rows (states) per thread per yaw bin
+  static constexpr int HX = TX + 2 * R_T;    // halo width (cells)
+  static constexpr int HY = TY + 2 * R_T;    // halo height
+  static constexpr int PW = HX + 1;          // prefix row length (exclusive prefix, entry 0 = 0)
+  static constexpr int NR = 2 * R_T + 1;     // stencil rows
   static constexpr int CPL = (HX + 31) / 32;  // halo cells per lane in the row scan
   static constexpr size_t raw_bytes = ((size_t)HX * HY * 4 + 127) / 128 * 128;
-  static constexpr size_t p02_off = raw_bytes;
-  static constexpr size_t px_off = p02_off + (size_t)HY * PW * 8;
-  static constexpr size_t pv_off = px_off + (size_t)HY * PW * 4;
-  static constexpr size_t pvxx_off = pv_off + (size_t)HY * PW * 8;
+  static constexpr size_t p02_off = raw_bytes;                              // float2 {P0, P2}
+  static constexpr size_t px_off = p02_off + (size_t)HY * PW * 8;           // float  PX
+  static constexpr size_t pv_off = px_off + (size_t)HY * PW * 4;            // float2 {PV, PVX}
+  static constexpr size_t pvxx_off = pv_off + (size_t)HY * PW * 8;          // float  PVXX
   static constexpr size_t misc_off = (pvxx_off + (size_t)HY * PW * 4 + 15) / 16 * 16;
-  // misc: mbarrier (8 B) + reduction scratch (3 x 8 words) + runs (k_chunk * NR int2)
-  static constexpr size_t runs_off = misc_off + 128;
-  static size_t bytes(int k_chunk) { return runs_off + (size_t)k_chunk * NR * 8; }
+  static constexpr size_t runs_off = misc_off + 128;  // int4 byte offsets per (bin, stencil row)
+  static size_t bytes(int k_chunk) { return runs_off + (size_t)k_chunk * NR * 16; }
 };
 
 template <int R_T>
 __global__ void __launch_bounds__(NTHREADS, 2)
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
-  constexpr int HX = G::HX, HY = G::HY, PW = G::PW, NR = G::NR, CPL = G::CPL;
+  constexpr int HX = G::HX, HY = G::HY, PW = G::PW, NR = G::NR, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
   extern __shared__ __align__(128) unsigned char smem[];
   float* raw = reinterpret_cast<float*>(smem);
   float2* p02 = reinterpret_cast<float2*>(smem + G::p02_off);
@@ -196,26 +241,31 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   float* pvxx = reinterpret_cast<float*>(smem + G::pvxx_off);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
   float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8]
-  int2* runs_s = reinterpret_cast<int2*>(smem + G::runs_off);
+  int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tlin = p.tile_list ? p.tile_list[blockIdx.x] : (int)blockIdx.x;
-  const long long TI = p.TI0 + tlin % p.tiles_x;
-  const long long TJ = p.TJ0 + tlin / p.tiles_x;
+  const int tx_rel = (int)(blockIdx.x % (unsigned)p.tiles_x);
+  const int ty_rel = p.row_first + (int)(blockIdx.x / (unsigned)p.tiles_x) * p.row_mod;
+  if (p.n_rects) {  // INCREMENTAL: only tiles that hold a state within R of a changed cell (CTA-uniform exit)
+    bool hit = false;
+    for (int q = 0; q < p.n_rects; ++q)
+      hit |= tx_rel >= p.rects[q].x && tx_rel < p.rects[q].y && ty_rel >= p.rects[q].z && ty_rel < p.rects[q].w;
+    if (!hit) return;
+  }
+  const long long TI = p.TI0 + tx_rel;
+  const long long TJ = p.TJ0 + ty_rel;
   const long long li0 = TI * TX - R_T - p.I_M;  // logical (window) index of halo column 0
   const long long lj0 = TJ * TY - R_T - p.J_M;
   const int kb = p.k_begin + blockIdx.y * p.k_chunk;
   const int ke = min(kb + p.k_chunk, p.k_end);
   if (kb >= ke) return;
-  const int pxM = (int)(((p.I_M % p.nx) + p.nx) % p.nx);  // physical column of logical 0
-  const int pyM = (int)(((p.J_M % p.ny) + p.ny) % p.ny);
 
   // ---- 1. halo -> shared memory ----------------------------------------------------------
   const bool box_in = li0 >= 0 && li0 + HX <= p.nx && lj0 >= 0 && lj0 + HY <= p.ny;
   int bx = 0, by = 0;
   if (box_in) {
-    bx = pxM + (int)li0; if (bx >= p.nx) bx -= p.nx;
-    by = pyM + (int)lj0; if (by >= p.ny) by -= p.ny;
+    bx = p.pxM + (int)li0; if (bx >= p.nx) bx -= p.nx;
+    by = p.pyM + (int)lj0; if (by >= p.ny) by -= p.ny;
   }
   const bool via_tma = p.use_tma && box_in && bx + HX <= p.nx && by + HY <= p.ny;
   if (via_tma) {
@@ -230,14 +280,20 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const long long li = li0 + col, lj = lj0 + row;
       float v = __int_as_float(0x7fc00000);
       if (li >= 0 && li < p.nx && lj >= 0 && lj < p.ny) {
-        int px = pxM + (int)li; if (px >= p.nx) px -= p.nx;
-        int py = pyM + (int)lj; if (py >= p.ny) py -= p.ny;
+        int px = p.pxM + (int)li; if (px >= p.nx) px -= p.nx;
+        int py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny;
         v = __ldg(p.h + (size_t)py * p.ldh + px);
       }
       raw[idx] = v;
     }
   }
-  for (int idx = tid; idx < (ke - kb) * NR; idx += NTHREADS) runs_s[idx] = p.runs[(size_t)kb * NR + idx];
+  // stencil rows of this CTA's bins as byte offsets into the prefix arrays (halo row d, column R_T + a)
+  for (int idx = tid; idx < (ke - kb) * NR; idx += NTHREADS) {
+    const int d = idx % NR;
+    const int2 ab = p.runs[(size_t)kb * NR + idx];
+    const int ea = d * PW + R_T + ab.x, eb = d * PW + R_T + ab.y + 1;
+    runs_s[idx] = make_int4(ea * 8, eb * 8, ea * 4, eb * 4);
+  }
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
 
@@ -260,13 +316,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   mn = red[0]; mxv = red[8];
   float allvf = red[16];
 #pragma unroll
-  for (int w = 1; w < NTHREADS / 32; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); allvf = fminf(allvf, red[16 + w]); }
+  for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); allvf = fminf(allvf, red[16 + w]); }
   const bool fast = allvf > 0.5f;
   const float href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   constexpr float XC = (float)(R_T + TX / 2);  // x' = col - XC; the state at lane l has x' = l - TX/2
-  for (int row = warp; row < HY; row += NTHREADS / 32) {
+  for (int row = warp; row < HY; row += NWARPS) {
     float e[CPL], e2[CPL], ex[CPL], vv[CPL], vx[CPL], vxx[CPL];
     float s0 = 0.f, s2 = 0.f, sx = 0.f, sv = 0.f, svx = 0.f, svxx = 0.f;
 #pragma unroll
@@ -284,7 +340,6 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         vv[c] = sv; vx[c] = svx; vxx[c] = svxx;
       }
     }
-    // lane totals -> exclusive lane offsets
     const float o0 = warp_incl_scan(s0, lane) - s0;
     const float o2 = warp_incl_scan(s2, lane) - s2;
     const float ox = warp_incl_scan(sx, lane) - sx;
@@ -315,76 +370,88 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   // ---- 4./5. states ------------------------------------------------------------------------
   const size_t plane = (size_t)p.nx * p.ny;
   const float xs = (float)(lane - TX / 2);
-  const long long Iw = TI * TX + lane;
-  const long long li = Iw - p.I_M;
+  const long long li = TI * TX + lane - p.I_M;
   const bool col_in = li >= 0 && li < p.nx;
   int pxs = 0;
-  if (col_in) { pxs = pxM + (int)li; if (pxs >= p.nx) pxs -= p.nx; }
-  int rowv[ROWS_PER_WARP], pys[ROWS_PER_WARP];
-  bool in[ROWS_PER_WARP];
+  if (col_in) { pxs = p.pxM + (int)li; if (pxs >= p.nx) pxs -= p.nx; }
+  const bool col_any = __any_sync(0xffffffffu, col_in);
+  int off[RPW], pys[RPW];
+  bool in[RPW];
 #pragma unroll
-  for (int s = 0; s < ROWS_PER_WARP; ++s) {
-    rowv[s] = warp + s * (NTHREADS / 32);  // tile row
-    const long long lj = TJ * TY + rowv[s] - p.J_M;
-    in[s] = col_in && lj >= 0 && lj < p.ny;
+  for (int s = 0; s < RPW; ++s) {
+    const long long lj = TJ * TY + warp + s * NWARPS - p.J_M;
+    const bool row_in = lj >= 0 && lj < p.ny;
+    in[s] = col_in && row_in;
     int py = 0;
-    if (lj >= 0 && lj < p.ny) { py = pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
-    pys[s] = py;
+    if (row_in) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
+    pys[s] = row_in ? py : -1;
+    off[s] = py * p.nx + pxs;
   }
-  const bool aligned_words = (p.nx % 32) == 0;
+  const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
+  // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, column lane)
+  const char* b8 = reinterpret_cast<const char*>(p02) + (size_t)(warp * PW + lane) * 8;
+  const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(warp * PW + lane) * 4;
+  const char* bv8 = reinterpret_cast<const char*>(pv) + (size_t)(warp * PW + lane) * 8;
+  const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(warp * PW + lane) * 4;
+  constexpr int RS8 = NWARPS * PW * 8, RS4 = NWARPS * PW * 4;  // state s -> s * NWARPS halo rows lower
 
   for (int k = kb; k < ke; ++k) {
-    const int2* rk = runs_s + (k - kb) * NR;
+    const int4* rk = runs_s + (k - kb) * NR;
     const float4 g = __ldg(p.geo + k);
     const float2 csk = __ldg(p.cs + k);
-    float S0[ROWS_PER_WARP], S2[ROWS_PER_WARP], SXH[ROWS_PER_WARP], SYH[ROWS_PER_WARP];
-    float N[ROWS_PER_WARP], Sx[ROWS_PER_WARP], Sy[ROWS_PER_WARP], Sxx[ROWS_PER_WARP], Sxy[ROWS_PER_WARP],
-        Syy[ROWS_PER_WARP];
+    float2 S02[RPW];
+    float SXH[RPW], SYH[RPW];
+    float N[RPW], Sx[RPW], Sy[RPW], Sxx[RPW], Sxy[RPW], Syy[RPW];
 #pragma unroll
-    for (int s = 0; s < ROWS_PER_WARP; ++s) {
-      S0[s] = S2[s] = SXH[s] = SYH[s] = 0.f;
-      N[s] = Sx[s] = Sy[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f;
+    for (int s = 0; s < RPW; ++s) {
+      S02[s] = make_float2(0.f, 0.f);
+      SXH[s] = SYH[s] = 0.f;
+      N[s] = g.x; Sx[s] = 0.f; Sy[s] = 0.f; Sxx[s] = g.y; Sxy[s] = g.z; Syy[s] = g.w;
     }
     if (fast) {
 #pragma unroll
       for (int d = 0; d < NR; ++d) {
-        const int2 ab = rk[d];
+        const int4 o = rk[d];
         const float dj = (float)(d - R_T);
-        const int c0 = lane + R_T + ab.x, c1 = lane + R_T + ab.y + 1;
+        const char* pa8 = b8 + o.x;
+        const char* pb8 = b8 + o.y;
+        const char* pa4 = b4 + o.z;
+        const char* pb4 = b4 + o.w;
 #pragma unroll
-        for (int s = 0; s < ROWS_PER_WARP; ++s) {
-          const int row = rowv[s] + d;  // halo row of stencil row dj = d - R_T
-          const float2 A = p02[row * PW + c0], B = p02[row * PW + c1];
-          const float ax = pxh[row * PW + c0], bxv = pxh[row * PW + c1];
-          const float d0 = B.x - A.x, d2 = B.y - A.y, dx = bxv - ax;
-          S0[s] += d0;
-          S2[s] += d2;
-          SXH[s] += fmaf(-xs, d0, dx);
-          SYH[s] = fmaf(dj, d0, SYH[s]);
+        for (int s = 0; s < RPW; ++s) {
+          const float2 A = *reinterpret_cast<const float2*>(pa8 + s * RS8);
+          const float2 B = *reinterpret_cast<const float2*>(pb8 + s * RS8);
+          const float ax = *reinterpret_cast<const float*>(pa4 + s * RS4);
+          const float bxv = *reinterpret_cast<const float*>(pb4 + s * RS4);
+          const float2 dd = sub2(B, A);  // (run sum of h^, run sum of h^2)
+          S02[s] = add2(S02[s], dd);
+          SXH[s] += fmaf(-xs, dd.x, bxv - ax);
+          SYH[s] = fmaf(dj, dd.x, SYH[s]);
         }
       }
-#pragma unroll
-      for (int s = 0; s < ROWS_PER_WARP; ++s) { N[s] = g.x; Sxx[s] = g.y; Sxy[s] = g.z; Syy[s] = g.w; }
     } else {
 #pragma unroll
-      for (int d = 0; d < NR; ++d) {
-        const int2 ab = rk[d];
-        const float dj = (float)(d - R_T);
-        const int c0 = lane + R_T + ab.x, c1 = lane + R_T + ab.y + 1;
+      for (int s = 0; s < RPW; ++s) { N[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f; }
 #pragma unroll
-        for (int s = 0; s < ROWS_PER_WARP; ++s) {
-          const int row = rowv[s] + d;
-          const float2 A = p02[row * PW + c0], B = p02[row * PW + c1];
-          const float ax = pxh[row * PW + c0], bxv = pxh[row * PW + c1];
-          const float2 VA = pv[row * PW + c0], VB = pv[row * PW + c1];
-          const float wa = pvxx[row * PW + c0], wb = pvxx[row * PW + c1];
-          const float d0 = B.x - A.x, d2 = B.y - A.y, dx = bxv - ax;
+      for (int d = 0; d < NR; ++d) {
+        const int4 o = rk[d];
+        const float dj = (float)(d - R_T);
+#pragma unroll
+        for (int s = 0; s < RPW; ++s) {
+          const float2 A = *reinterpret_cast<const float2*>(b8 + o.x + s * RS8);
+          const float2 B = *reinterpret_cast<const float2*>(b8 + o.y + s * RS8);
+          const float ax = *reinterpret_cast<const float*>(b4 + o.z + s * RS4);
+          const float bxv = *reinterpret_cast<const float*>(b4 + o.w + s * RS4);
+          const float2 VA = *reinterpret_cast<const float2*>(bv8 + o.x + s * RS8);
+          const float2 VB = *reinterpret_cast<const float2*>(bv8 + o.y + s * RS8);
+          const float wa = *reinterpret_cast<const float*>(bv4 + o.z + s * RS4);
+          const float wb = *reinterpret_cast<const float*>(bv4 + o.w + s * RS4);
+          const float2 dd = sub2(B, A);
           const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
           const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
-          S0[s] += d0;
-          S2[s] += d2;
-          SXH[s] += fmaf(-xs, d0, dx);
-          SYH[s] = fmaf(dj, d0, SYH[s]);
+          S02[s] = add2(S02[s], dd);
+          SXH[s] += fmaf(-xs, dd.x, bxv - ax);
+          SYH[s] = fmaf(dj, dd.x, SYH[s]);
           N[s] += cnt;
           Sx[s] += sdi;
           Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
@@ -394,40 +461,23 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         }
       }
     }
+    float4* outk = p.out + (size_t)k * plane;
+    float4* outk2 = p.out + (size_t)(k + p.H) * plane;
+    uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words + gword;
+    uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words + gword;
 #pragma unroll
-    for (int s = 0; s < ROWS_PER_WARP; ++s) {
-      const StateOut o = epilogue(N[s], Sx[s], Sy[s], Sxx[s], Sxy[s], Syy[s], S0[s], S2[s], SXH[s], SYH[s], href,
-                                  csk, p, !fast);
-      const size_t off = (size_t)pys[s] * p.nx + pxs;
+    for (int s = 0; s < RPW; ++s) {
+      const StateOut o = epilogue(N[s], Sx[s], Sy[s], Sxx[s], Sxy[s], Syy[s], S02[s].x, S02[s].y, SXH[s], SYH[s],
+                                  href, csk, p, !fast);
       if (in[s]) {
-        p.risk[(size_t)k * plane + off] = o.risk;
-        p.pitch[(size_t)k * plane + off] = o.pitch;
-        p.roll[(size_t)k * plane + off] = o.roll;
-        p.z[(size_t)k * plane + off] = o.z;
-        if (p.paired) {
-          const size_t k2 = (size_t)(k + p.H);
-          p.risk[k2 * plane + off] = o.risk;
-          p.pitch[k2 * plane + off] = -o.pitch;
-          p.roll[k2 * plane + off] = -o.roll;
-          p.z[k2 * plane + off] = o.z;
-        }
+        outk[off[s]] = make_float4(o.risk, o.pitch, o.roll, o.z);
+        if (p.paired) outk2[off[s]] = make_float4(o.risk, -o.pitch, -o.roll, o.z);
       }
-      const unsigned inmask = __ballot_sync(0xffffffffu, in[s]);
+      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
       const unsigned tmask = __ballot_sync(0xffffffffu, in[s] && o.trav);
-      if (inmask == 0xffffffffu && aligned_words) {
-        if (lane == 0) {
-          const size_t w = ((size_t)k * p.ny + pys[s]) * p.trav_words + (pxs >> 5);
-          p.trav[w] = tmask;
-          if (p.paired) p.trav[((size_t)(k + p.H) * p.ny + pys[s]) * p.trav_words + (pxs >> 5)] = tmask;
-        }
-      } else if (in[s]) {
-        const unsigned bit = 1u << (pxs & 31);
-        const size_t w = ((size_t)k * p.ny + pys[s]) * p.trav_words + (pxs >> 5);
-        if (o.trav) atomicOr(p.trav + w, bit); else atomicAnd(p.trav + w, ~bit);
-        if (p.paired) {
-          const size_t w2 = ((size_t)(k + p.H) * p.ny + pys[s]) * p.trav_words + (pxs >> 5);
-          if (o.trav) atomicOr(p.trav + w2, bit); else atomicAnd(p.trav + w2, ~bit);
-        }
+      if (lane == 0 && col_any && pys[s] >= 0) {
+        travk[(size_t)pys[s] * p.trav_words] = tmask;
+        if (p.paired) travk2[(size_t)pys[s] * p.trav_words] = tmask;
       }
     }
   }
@@ -503,31 +553,38 @@ cudaError_t launch_scatter_rect(float* h, int ldh, int nx, int ny, int px0, int 
   return cudaGetLastError();
 }
 
-__global__ void gather_logical_kernel(const AssessParams p, int k_lo, int k_hi, int pxM, int pyM, float* risk,
-                                      float* pitch, float* roll, float* z, uint8_t* trav) {
+__device__ __forceinline__ long long floor_div32(long long a) { return a >= 0 ? a / 32 : -((-a + 31) / 32); }
+
+__global__ void gather_logical_kernel(const AssessParams p, int k_lo, int k_hi, float* risk, float* pitch,
+                                      float* roll, float* z, uint8_t* trav) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   const int k = blockIdx.z;
   if (i >= p.nx) return;
-  int px = pxM + i; if (px >= p.nx) px -= p.nx;
-  int py = pyM + j; if (py >= p.ny) py -= p.ny;
+  int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
+  int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
   const size_t src = ((size_t)k * p.ny + py) * p.nx + px;
   const size_t dst = ((size_t)k * p.ny + j) * p.nx + i;
   const bool owned = k >= k_lo && k < k_hi;
   const float qnan = __int_as_float(0x7fc00000);
-  if (risk) risk[dst] = owned ? p.risk[src] : qnan;
-  if (pitch) pitch[dst] = owned ? p.pitch[src] : qnan;
-  if (roll) roll[dst] = owned ? p.roll[src] : qnan;
-  if (z) z[dst] = owned ? p.z[src] : qnan;
-  if (trav) trav[dst] = owned ? (uint8_t)((p.trav[((size_t)k * p.ny + py) * p.trav_words + (px >> 5)] >> (px & 31)) & 1u) : 0;
+  const float4 v = owned ? p.out[src] : make_float4(qnan, qnan, qnan, qnan);
+  if (risk) risk[dst] = v.x;
+  if (pitch) pitch[dst] = v.y;
+  if (roll) roll[dst] = v.z;
+  if (z) z[dst] = v.w;
+  if (trav) {
+    const long long I = p.I_M + i;
+    const long long gw = floor_div32(I);
+    const int w = (int)(((gw % p.trav_words) + p.trav_words) % p.trav_words);
+    const int bit = (int)(I - gw * 32);
+    trav[dst] = owned ? (uint8_t)((p.trav[((size_t)k * p.ny + py) * p.trav_words + w] >> bit) & 1u) : 0;
+  }
 }
 
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk, float* pitch, float* roll,
                                   float* z, uint8_t* trav, cudaStream_t s) {
-  const int pxM = (int)(((p.I_M % p.nx) + p.nx) % p.nx);
-  const int pyM = (int)(((p.J_M % p.ny) + p.ny) % p.ny);
   dim3 grid((p.nx + 255) / 256, p.ny, p.n_yaw);
-  gather_logical_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, pxM, pyM, risk, pitch, roll, z, trav);
+  gather_logical_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk, pitch, roll, z, trav);
   return cudaGetLastError();
 }
 
@@ -536,13 +593,14 @@ __global__ void query_kernel(const AssessParams p, int n, const int4* __restrict
   if (q >= n) return;
   const int4 e = idx[q];
   const float qnan = __int_as_float(0x7fc00000);
-  float r = qnan, pi = qnan, ro = qnan, zz = qnan, tv = 0.f;
+  float4 v = make_float4(qnan, qnan, qnan, qnan);
+  float tv = 0.f;
   if (e.w) {
-    const size_t o = ((size_t)e.z * p.ny + e.y) * p.nx + e.x;
-    r = p.risk[o]; pi = p.pitch[o]; ro = p.roll[o]; zz = p.z[o];
-    tv = (float)((p.trav[((size_t)e.z * p.ny + e.y) * p.trav_words + (e.x >> 5)] >> (e.x & 31)) & 1u);
+    v = p.out[((size_t)e.z * p.ny + e.y) * p.nx + e.x];
+    const int wb = e.w - 1;
+    tv = (float)((p.trav[((size_t)e.z * p.ny + e.y) * p.trav_words + (wb >> 5)] >> (wb & 31)) & 1u);
   }
-  out[q] = r; out[n + q] = pi; out[2 * (size_t)n + q] = ro; out[3 * (size_t)n + q] = zz; out[4 * (size_t)n + q] = tv;
+  out[q] = v.x; out[n + q] = v.y; out[2 * (size_t)n + q] = v.z; out[3 * (size_t)n + q] = v.w; out[4 * (size_t)n + q] = tv;
 }
 
 cudaError_t launch_query(const AssessParams& p, int n, const int4* idx, float* out, cudaStream_t s) {

@@ -7,14 +7,16 @@
 
 namespace se2m {
 
-// Spatial tile of states handled by one CTA: world-aligned, TX = one warp.
+// Spatial tile of states handled by one CTA: world-aligned, TX = one warp wide,
+// tile_rows(R_T) rows (32 for R_T <= 12, else 16, to fit >= 2 CTAs per SM in shared memory).
 constexpr int TX = 32;
-constexpr int TY = 16;
-constexpr int NTHREADS = 256;              // 8 warps; warp w owns tile rows w and w + 8
-constexpr int ROWS_PER_WARP = TY / (NTHREADS / 32);
+constexpr int NTHREADS = 256;              // 8 warps; warp w owns tile rows w, w + 8, w + 16, ...
+constexpr int NWARPS = NTHREADS / 32;
+constexpr int tile_rows(int R_T) { return R_T <= 12 ? 32 : 16; }
 
 // Stencil radii the assess kernel is instantiated for (R_T >= the footprint radius R).
 constexpr int kRadii[] = {4, 8, 12, 16, 24, 32};
+constexpr int kMaxRects = 8;  // dirty rectangles passed by value to an INCREMENTAL launch
 
 struct AssessParams {
   // window / ring buffer: world cell (I, J) lives at physical (I mod nx, J mod ny)
@@ -22,13 +24,12 @@ struct AssessParams {
   int ldh;               // heights row pitch in floats (multiple of 4: 16-B TMA stride)
   long long I_M, J_M;    // window origin, world cells (Eq. 4)
   const float* h;        // [ny][ldh] physical, NaN = unknown
-  // outputs, physical layout [k][ny][nx]; trav bits [k][ny][trav_words]
-  float* risk;
-  float* pitch;
-  float* roll;
-  float* z;
+  int pxM, pyM;          // physical column / row of logical (0, 0) = I_M mod nx, J_M mod ny
+  // outputs: state records [k][ny][nx] float4 (risk, pitch, roll, z), physical (ring) layout;
+  // traversable bits [k][ny][trav_words], word = floor(I/32) mod trav_words, bit = I mod 32 (world I)
+  float4* out;
   uint32_t* trav;
-  int trav_words;
+  int trav_words;        // ceil(nx/32) + 1: the window's 32-groups map to distinct words
   // yaw: rep bins k in [0, H); bin k + H (if paired) is the same footprint, x_yaw negated
   int n_yaw, H, paired;
   int R;                 // true footprint radius (cells); kernel template R_T >= R
@@ -39,10 +40,15 @@ struct AssessParams {
   // risk (Alg. 1 lines 10-18), all float
   float kappa_max, phi_x_max, phi_y_max;
   float wk, wx, wy;      // w_r[0]/kappa_max, w_r[1]/phi_x_max, w_r[2]/phi_y_max
-  // tiles: world tile (TI, TJ) covers I in [TI*TX, TI*TX+TX), J in [TJ*TY, TJ*TY+TY)
-  long long TI0, TJ0;    // first world tile of the dense tile grid
-  int tiles_x;           // tile columns of the dense grid
-  const int* tile_list;  // if non-null: linear indices (ty*tiles_x + tx) of the tiles to run
+  // tiles: world tile (TI, TJ) covers I in [TI*TX, TI*TX+TX), J in [TJ*TY, TJ*TY+TY), TY = tile_rows(R_T)
+  // CTA b runs world tile (TI0 + b % tiles_x, TJ0 + row_first + (b / tiles_x) * row_mod): row_mod > 1
+  // shards tile rows across ranks (SE2M_SHARD_ROWS); n_rects > 0 restricts the launch to the tiles
+  // inside rects (INCREMENTAL), [x0, x1) x [y0, y1) in tiles relative to (TI0, TJ0).
+  long long TI0, TJ0;
+  int tiles_x;
+  int row_first, row_mod;
+  int n_rects;
+  int4 rects[kMaxRects];
   int k_begin, k_end;    // representative-bin range this launch covers
   int k_chunk;           // rep bins per CTA (grid.y = ceil((k_end-k_begin)/k_chunk))
   int use_tma;           // tensor map valid
@@ -59,7 +65,7 @@ cudaError_t launch_scatter_rect(float* h, int ldh, int nx, int ny, int px0, int 
                                 const float* src, long long ld, const uint8_t* known, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
-cudaError_t launch_query(const AssessParams& p, int n, const int4* idx /* (px, py, k, valid) */,
+cudaError_t launch_query(const AssessParams& p, int n, const int4* idx /* (px, py, k, 1 + 32*word + bit | 0) */,
                          float* out /* 5 x n: risk, pitch, roll, z, trav */, cudaStream_t s);
 
 }  // namespace se2m

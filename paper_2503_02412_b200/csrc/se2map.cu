@@ -45,15 +45,12 @@ struct se2m_map {
   int k_lo = 0, k_hi = 0;  // owned representative bins [k_lo, k_hi)
   long long I_M = 0, J_M = 0;
   float* d_h = nullptr;
-  float *d_risk = nullptr, *d_pitch = nullptr, *d_roll = nullptr, *d_z = nullptr;
+  float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
   int2* d_runs = nullptr;
   float4* d_geo = nullptr;
   float2* d_cs = nullptr;
   std::vector<int> ncells;  // |P_k| per rep bin
-  int* d_tiles = nullptr;
-  int* h_tiles = nullptr;  // pinned
-  size_t tiles_cap = 0;
   float* d_stage = nullptr;  // update / download staging
   size_t stage_bytes = 0;
   int4* d_qidx = nullptr;
@@ -148,7 +145,7 @@ static bool make_tensor_map(se2m_map* m) {
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres) != cudaSuccess || !fn ||
       qres != cudaDriverEntryPointSuccess)
     return false;
-  const int HX = TX + 2 * m->R_T, HY = TY + 2 * m->R_T;
+  const int HX = TX + 2 * m->R_T, HY = tile_rows(m->R_T) + 2 * m->R_T;
   if (HX > 256 || HY > 256 || HX > m->prm.nx || HY > m->prm.ny) return false;
   cuuint64_t dims[2] = {(cuuint64_t)m->prm.nx, (cuuint64_t)m->prm.ny};
   cuuint64_t strides[1] = {(cuuint64_t)m->ldh * 4};
@@ -166,7 +163,8 @@ static AssessParams make_params(const se2m_map* m) {
   p.nx = m->prm.nx; p.ny = m->prm.ny; p.ldh = m->ldh;
   p.I_M = m->I_M; p.J_M = m->J_M;
   p.h = m->d_h;
-  p.risk = m->d_risk; p.pitch = m->d_pitch; p.roll = m->d_roll; p.z = m->d_z; p.trav = m->d_trav;
+  p.pxM = pmod(m->I_M, m->prm.nx); p.pyM = pmod(m->J_M, m->prm.ny);
+  p.out = m->d_out; p.trav = m->d_trav;
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
   p.runs = m->d_runs; p.geo = m->d_geo; p.cs = m->d_cs;
@@ -256,15 +254,12 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
   m->J_M = (long long)floor(p->robot_y / p->resolution) - p->ny / 2;
   m->ldh = (p->nx + 3) / 4 * 4;
-  m->trav_words = (p->nx + 31) / 32;
+  m->trav_words = (p->nx + 31) / 32 + 1;  // world 32-groups of the window map to distinct words
   const size_t plane = (size_t)p->nx * p->ny;
   const size_t nst = plane * n;
   struct { void** ptr; size_t bytes; const char* what; } allocs[] = {
       {(void**)&m->d_h, (size_t)m->ldh * p->ny * 4, "heights"},
-      {(void**)&m->d_risk, nst * 4, "risk"},
-      {(void**)&m->d_pitch, nst * 4, "pitch"},
-      {(void**)&m->d_roll, nst * 4, "roll"},
-      {(void**)&m->d_z, nst * 4, "z"},
+      {(void**)&m->d_out, nst * sizeof(float4), "state records"},
       {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
       {(void**)&m->d_runs, runs.size() * sizeof(int2), "runs"},
       {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
@@ -294,11 +289,10 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_h, m->d_risk, m->d_pitch, m->d_roll, m->d_z, m->d_trav, m->d_runs, m->d_geo,
-                  m->d_cs, m->d_tiles, m->d_stage, m->d_qidx, m->d_qout};
+  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_runs, m->d_geo,
+                  m->d_cs, m->d_stage, m->d_qidx, m->d_qout};
   for (void* q : ptrs)
     if (q) cudaFree(q);
-  if (m->h_tiles) cudaFreeHost(m->h_tiles);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -382,7 +376,7 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
   return SE2M_OK;
 }
 
-static bool tile_owned(const se2m_map* m, long long TJ) {
+static bool tile_owned(const se2m_map* m, long long TJ) {  // TJ: world tile row (tile_rows(R_T) rows)
   if (m->prm.shard_mode != SE2M_SHARD_ROWS || m->prm.world_size <= 1) return true;
   return pmod(TJ, m->prm.world_size) == m->prm.rank;
 }
@@ -393,57 +387,50 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   if (!m->have_data) return fail(m, SE2M_ERR_STATE, "assess before any update_elevation");
   AssessParams p = make_params(m);
   const int nx = m->prm.nx, ny = m->prm.ny;
+  const int TY = tile_rows(m->R_T);
+  // dense grid of world tiles intersecting the window
   const long long TI0 = floor_div(m->I_M, TX), TI1 = floor_div(m->I_M + nx - 1, TX);
   const long long TJ0 = floor_div(m->J_M, TY), TJ1 = floor_div(m->J_M + ny - 1, TY);
-  const int tiles_x = (int)(TI1 - TI0 + 1), tiles_y = (int)(TJ1 - TJ0 + 1);
-  p.TI0 = TI0; p.TJ0 = TJ0; p.tiles_x = tiles_x;
-  std::vector<int> list;
-  const bool sharded_rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  long long gx0 = 0, gx1 = TI1 - TI0 + 1, gy0 = 0, gy1 = TJ1 - TJ0 + 1;  // launch box, tiles rel. to (TI0, TJ0)
   const bool full = mode == SE2M_FULL || m->all_dirty;
-  if (!full || sharded_rows) {
-    std::vector<char> mark((size_t)tiles_x * tiles_y, full ? 1 : 0);
-    if (!full) {
-      const long long Rd = m->R;  // states within R of a changed cell (Chebyshev bound of the footprint)
-      for (const Rect& d : m->dirty) {
-        long long I0 = std::max(d.I0 - Rd, m->I_M), I1 = std::min(d.I1 + Rd, m->I_M + nx);
-        long long J0 = std::max(d.J0 - Rd, m->J_M), J1 = std::min(d.J1 + Rd, m->J_M + ny);
-        if (I0 >= I1 || J0 >= J1) continue;
-        for (long long tj = floor_div(J0, TY); tj <= floor_div(J1 - 1, TY); ++tj)
-          for (long long ti = floor_div(I0, TX); ti <= floor_div(I1 - 1, TX); ++ti)
-            mark[(size_t)(tj - TJ0) * tiles_x + (ti - TI0)] = 1;
-      }
+  std::vector<int4> rects;
+  if (!full) {
+    // H9: states within R (Chebyshev bound of every footprint) of a changed cell, as tile rectangles
+    const long long Rd = m->R;
+    long long bx0 = gx1, bx1 = 0, by0 = gy1, by1 = 0;
+    for (const Rect& d : m->dirty) {
+      const long long I0 = std::max(d.I0 - Rd, m->I_M), I1 = std::min(d.I1 + Rd, m->I_M + nx);
+      const long long J0 = std::max(d.J0 - Rd, m->J_M), J1 = std::min(d.J1 + Rd, m->J_M + ny);
+      if (I0 >= I1 || J0 >= J1) continue;
+      const int4 t = make_int4((int)(floor_div(I0, TX) - TI0), (int)(floor_div(I1 - 1, TX) - TI0 + 1),
+                               (int)(floor_div(J0, TY) - TJ0), (int)(floor_div(J1 - 1, TY) - TJ0 + 1));
+      rects.push_back(t);
+      bx0 = std::min<long long>(bx0, t.x); bx1 = std::max<long long>(bx1, t.y);
+      by0 = std::min<long long>(by0, t.z); by1 = std::max<long long>(by1, t.w);
     }
-    for (int t = 0; t < tiles_x * tiles_y; ++t)
-      if (mark[t] && tile_owned(m, TJ0 + t / tiles_x)) list.push_back(t);
-    if (list.size() > m->tiles_cap) {
-      if (m->d_tiles) { cudaStreamSynchronize(m->stream); cudaFree(m->d_tiles); m->d_tiles = nullptr; }
-      if (m->h_tiles) { cudaFreeHost(m->h_tiles); m->h_tiles = nullptr; }
-      m->tiles_cap = 0;
-      size_t cap = std::max<size_t>(list.size(), 1024);
-      CUDA_TRY(m, cudaMalloc(&m->d_tiles, cap * sizeof(int)), "cudaMalloc(tiles)");
-      CUDA_TRY(m, cudaMallocHost(&m->h_tiles, cap * sizeof(int)), "cudaMallocHost(tiles)");
-      m->tiles_cap = cap;
-    }
+    if (rects.empty()) { m->dirty.clear(); return SE2M_OK; }  // nothing changed
+    if ((int)rects.size() > kMaxRects) rects.assign(1, make_int4((int)bx0, (int)bx1, (int)by0, (int)by1));
+    gx0 = bx0; gx1 = bx1; gy0 = by0; gy1 = by1;
+    for (int4& t : rects) { t.x -= (int)gx0; t.y -= (int)gx0; t.z -= (int)gy0; t.w -= (int)gy0; }
   }
-  int n_tiles = tiles_x * tiles_y;
-  if (!full || sharded_rows) {
-    n_tiles = (int)list.size();
-    if (n_tiles > 0) {
-      // the pinned staging list may still be read by a previous async copy: order on the stream
-      CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(tiles)");
-      memcpy(m->h_tiles, list.data(), list.size() * sizeof(int));
-      CUDA_TRY(m, cudaMemcpyAsync(m->d_tiles, m->h_tiles, list.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream), "H2D tiles");
-    }
-    p.tile_list = m->d_tiles;
+  p.TI0 = TI0 + gx0; p.TJ0 = TJ0 + gy0;
+  p.tiles_x = (int)(gx1 - gx0);
+  const int tiles_y = (int)(gy1 - gy0);
+  p.n_rects = (int)rects.size();
+  for (int q = 0; q < p.n_rects; ++q) p.rects[q] = rects[q];
+  p.row_mod = 1; p.row_first = 0;
+  if (m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1) {
+    p.row_mod = m->prm.world_size;                       // rank owns world tile rows TJ = rank (mod G)
+    p.row_first = pmod((long long)m->prm.rank - p.TJ0, p.row_mod);
   }
+  const int grid_rows = tiles_y > p.row_first ? (tiles_y - p.row_first + p.row_mod - 1) / p.row_mod : 0;
+  const int n_tiles = p.tiles_x * grid_rows;
   // yaw chunking: enough CTAs for >= 4 waves of 148 SMs, otherwise all bins per CTA (tile reuse)
   const int nk = m->k_hi - m->k_lo;
   int chunk = nk;
   if (n_tiles > 0) {
     const long long want = 4LL * 148;
-    if ((long long)n_tiles * 1 < want) chunk = 1;
-    else chunk = (int)std::max<long long>(1, std::min<long long>(nk, (long long)n_tiles * nk / want));
-    if ((long long)n_tiles * ((nk + chunk - 1) / chunk) < want) chunk = std::max(1, (int)((long long)n_tiles * nk / want));
+    chunk = (int)std::max<long long>(1, std::min<long long>(nk, (long long)n_tiles * nk / want));
   }
   p.k_chunk = std::max(1, chunk);
   if (n_tiles > 0 && nk > 0) {
@@ -453,6 +440,13 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   }
   m->dirty.clear();
   m->all_dirty = false;
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_t* tile_y) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (tile_x) *tile_x = TX;
+  if (tile_y) *tile_y = tile_rows(m->R_T);
   return SE2M_OK;
 }
 
@@ -478,9 +472,12 @@ extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, flo
       long long k = (long long)floor((th + M_PI) / dth + 0.5);  // nearest bin (reading R3)
       k %= ny_aw;
       if (k < 0) k += ny_aw;
-      const long long TJ = floor_div(lj + m->J_M, TY);
-      if (li >= 0 && li < nx && lj >= 0 && lj < ny && owned_bin(m, (int)k) && tile_owned(m, TJ))
-        e = make_int4(pmod(m->I_M + li, nx), pmod(m->J_M + lj, ny), (int)k, 1);
+      const long long TJ = floor_div(lj + m->J_M, tile_rows(m->R_T));
+      if (li >= 0 && li < nx && lj >= 0 && lj < ny && owned_bin(m, (int)k) && tile_owned(m, TJ)) {
+        const long long I = m->I_M + li;
+        const int word = pmod(floor_div(I, 32), m->trav_words), bit = pmod(I, 32);
+        e = make_int4(pmod(I, nx), pmod(m->J_M + lj, ny), (int)k, 1 + 32 * word + bit);
+      }
     }
     if (!e.w) any_out = true;
     idx[q] = e;
@@ -550,7 +547,7 @@ extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, flo
         AssessParams q2 = p;
         const size_t plane = (size_t)m->prm.nx * m->prm.ny;
         q2.n_yaw = m->H;
-        q2.risk += plane * m->H; q2.pitch += plane * m->H; q2.roll += plane * m->H; q2.z += plane * m->H;
+        q2.out += plane * m->H;
         q2.trav += (size_t)m->H * m->prm.ny * m->trav_words;
         float* g[4];
         for (int i = 0; i < 4; ++i) g[i] = f[i] ? f[i] + plane * m->H : nullptr;

@@ -28,7 +28,7 @@ SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
 
 EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elevation", "se2m_shift_window",
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
-           "se2m_synchronize", "se2m_launch_count", "se2m_last_error"]
+           "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info"]
 
 
 class Params(ctypes.Structure):
@@ -57,12 +57,13 @@ _lib.se2m_download.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32]
 _lib.se2m_get_origin.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
 _lib.se2m_stencil_info.argtypes = [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_synchronize.argtypes = [_vp]
+_lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
 _lib.se2m_last_error.argtypes = [_vp]
 _lib.se2m_last_error.restype = ctypes.c_char_p
 for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
-              "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize"):
+              "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -94,6 +95,14 @@ def _ptr(a):
     if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
         return a.data_ptr(), (SE2M_MEM_DEVICE if a.is_cuda else SE2M_MEM_HOST), a
     a = np.ascontiguousarray(a)
+    return a.ctypes.data, SE2M_MEM_HOST, a
+
+
+def _ptr_nocopy(a):
+    if a is None:
+        return None, SE2M_MEM_HOST, None
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
+        return a.data_ptr(), (SE2M_MEM_DEVICE if a.is_cuda else SE2M_MEM_HOST), a
     return a.ctypes.data, SE2M_MEM_HOST, a
 
 
@@ -139,15 +148,26 @@ class Se2Map:
     def update_elevation(self, heights, known=None, i0: int = 0, j0: int = 0):
         """heights: (h, w) float32 NumPy array or CUDA tensor; known: same shape uint8 or None."""
         hh, w = heights.shape
-        if not hasattr(heights, "is_cuda"):
-            heights = np.ascontiguousarray(heights, dtype=np.float32)
+        if hasattr(heights, "is_cuda"):                      # torch tensor (host or device)
+            if heights.dtype.__repr__() != "torch.float32" or heights.stride(1) != 1:
+                raise ValueError("heights tensor must be float32 with unit column stride")
+            ld = heights.stride(0)
+            if known is not None and (known.shape != heights.shape or known.stride(0) != ld or known.stride(1) != 1):
+                raise ValueError("known must have the layout of heights")
+        else:                                                # NumPy: row views are passed without a copy
+            if heights.dtype != np.float32 or heights.strides[1] != 4 or heights.strides[0] % 4:
+                heights = np.ascontiguousarray(heights, dtype=np.float32)
+            ld = heights.strides[0] // 4
             if known is not None:
-                known = np.ascontiguousarray(known, dtype=np.uint8)
-        hp, mem, keep = _ptr(heights)
-        kp, mem2, keep2 = _ptr(known)
+                known = np.asarray(known, dtype=np.uint8)
+                if known.shape != heights.shape or known.strides != (ld, 1):
+                    kk = np.zeros((hh, ld), np.uint8)
+                    kk[:, :w] = known
+                    known = kk[:, :w]
+        hp, mem, keep = _ptr_nocopy(heights)
+        kp, mem2, keep2 = _ptr_nocopy(known)
         if known is not None and mem2 != mem:
             raise ValueError("heights and known must both be host or both be device memory")
-        ld = heights.stride(0) if hasattr(heights, "stride") and callable(heights.stride) else heights.strides[0] // 4
         return self._check(_lib.se2m_update_elevation(self.h, i0, j0, w, hh, hp, ld, kp, mem))
 
     def shift_window(self, x: float, y: float):
@@ -200,6 +220,11 @@ class Se2Map:
         n, r = _i32(), _i32()
         self._check(_lib.se2m_stencil_info(self.h, k, ctypes.byref(n), ctypes.byref(r)))
         return n.value, r.value
+
+    def tile_info(self):
+        tx, ty = _i32(), _i32()
+        self._check(_lib.se2m_tile_info(self.h, ctypes.byref(tx), ctypes.byref(ty)))
+        return tx.value, ty.value
 
     def synchronize(self):
         return self._check(_lib.se2m_synchronize(self.h))

@@ -85,11 +85,13 @@ class Plane:
 class Hills:
     seed: int = 1
     K: int = 24
-    slope_rms: float = 0.35
+    slope_rms: float = 0.5
     h0: float = 100.0
     sigma: float = 0.01
     lam_min: float = 1.5
     lam_max: float = 12.0
+    rock_density: float = 0.2    # probability of one rock per 1 m x 1 m world block
+    rock_block: float = 1.0
 
     def components(self):
         rng = np.random.Generator(np.random.PCG64(self.seed))
@@ -106,7 +108,32 @@ class Hills:
             h += amp[k] * np.sin(2.0 * math.pi / lam[k] * (x * math.cos(psi[k]) + y * math.sin(psi[k])) + phi[k])
         if self.sigma:
             h += self.sigma * cell_normal_noise(self.seed, I, J)
+        if self.rock_density > 0:
+            h += self.rocks(x, y)
         return h
+
+    def rocks(self, x, y):
+        """Sparse Gaussian bumps ('rocks'): at most one per rock_block-sized world block, placed and
+        sized by a hash of (seed, block) so that they are a pure function of world position.
+        Height U[0.2, 0.6] m, radius U[0.1, 0.3] m; they make the curvature term kappa matter."""
+        B = self.rock_block
+        x = np.broadcast_to(x, np.broadcast(x, y).shape)
+        y = np.broadcast_to(y, x.shape)
+        bi0 = np.floor(x / B).astype(np.int64)
+        bj0 = np.floor(y / B).astype(np.int64)
+        out = np.zeros(x.shape, dtype=np.float64)
+        to_u = lambda v: (v >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        for oj in (-1, 0, 1):
+            for oi in (-1, 0, 1):
+                bi, bj = bi0 + oi, bj0 + oj
+                present = to_u(_cell_hash(self.seed + 7919, bi, bj, 3)) < self.rock_density
+                cx = (bi + to_u(_cell_hash(self.seed + 7919, bi, bj, 4))) * B
+                cy = (bj + to_u(_cell_hash(self.seed + 7919, bi, bj, 5))) * B
+                ht = 0.2 + 0.4 * to_u(_cell_hash(self.seed + 7919, bi, bj, 6))
+                rad = 0.1 + 0.2 * to_u(_cell_hash(self.seed + 7919, bi, bj, 7))
+                d2 = (x - cx) ** 2 + (y - cy) ** 2
+                out += np.where(present, ht * np.exp(-d2 / (2.0 * rad * rad)), 0.0)
+        return out
 
 
 def world_heights(terrain, I0: int, J0: int, nx: int, ny: int, r: float) -> np.ndarray:

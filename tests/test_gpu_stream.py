@@ -101,7 +101,8 @@ def test_sharded_equals_single(mode, G):
             mask = np.broadcast_to(own[:, None, None], ref["risk"].shape)
         else:
             J = np.arange(J_M, J_M + ny)
-            own_rows = (np.floor_divide(J, 16) % G) == rank
+            TY = m.tile_info()[1]
+            own_rows = (np.floor_divide(J, TY) % G) == rank
             mask = np.broadcast_to(own_rows[None, :, None], ref["risk"].shape)
         for f in merged:
             merged[f][mask] = g[f][mask]
