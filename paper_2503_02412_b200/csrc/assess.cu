@@ -207,6 +207,163 @@ __device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float 
 }
 
 // ------------------------------------------------------------------------------------------
+// Packed two-state epilogue for interior tiles (all footprint cells known and inside the window).
+// Every FP32 add/mul/fma runs as one sm_100a FADD2/FMUL2/FFMA2 on (state a, state b); MUFU, compares
+// and selects run per lane.  The footprint geometry is the per-bin constant gc = (C00, C01, C11, 1/N),
+// gd = (r/N, C00 + C11, C01^2, -) (metres, computed in FP64 on the host), so Sx = Sy = 0, mx = my = 0.
+// ------------------------------------------------------------------------------------------
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 pk(float a, float b) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ F2 bc(float a) { return pk(a, a); }
+__device__ __forceinline__ float lo(F2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v)); return a; }
+__device__ __forceinline__ float hi(F2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v)); return b; }
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { F2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { F2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) { F2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return d;
+}
+template <class Fn>
+__device__ __forceinline__ F2 map2(F2 x, Fn f) { return pk(f(lo(x)), f(hi(x))); }
+
+__device__ __forceinline__ F2 acos2(F2 x) {  // A&S 4.4.46, packed polynomial
+  const float xl = lo(x), xh = hi(x);
+  const F2 a = pk(fabsf(xl), fabsf(xh));
+  F2 pz = fma2(bc(-0.0012624911f), a, bc(0.0066700901f));
+  pz = fma2(pz, a, bc(-0.0170881256f));
+  pz = fma2(pz, a, bc(0.0308918810f));
+  pz = fma2(pz, a, bc(-0.0501743046f));
+  pz = fma2(pz, a, bc(0.0889789874f));
+  pz = fma2(pz, a, bc(-0.2145988016f));
+  pz = fma2(pz, a, bc(1.5707963050f));
+  const F2 om = bc(1.f) - a;
+  const F2 r = pk(fsqrt(lo(om)), fsqrt(hi(om))) * pz;
+  const float rl = lo(r), rh = hi(r);
+  return pk(xl < 0.f ? 3.14159265358979f - rl : rl, xh < 0.f ? 3.14159265358979f - rh : rh);
+}
+__device__ __forceinline__ F2 asin2(F2 x) {  // Cephes asinf, packed polynomial; odd, asin(0) = 0
+  const float xl = lo(x), xh = hi(x);
+  const float al = fabsf(xl), ah = fabsf(xh);
+  const bool bl = al > 0.5f, bh = ah > 0.5f;
+  const F2 a = pk(al, ah);
+  const F2 sq = a * a;
+  const F2 half = fma2(bc(-0.5f), a, bc(0.5f));  // (1 - a) / 2
+  const F2 z = pk(bl ? lo(half) : lo(sq), bh ? hi(half) : hi(sq));
+  const F2 sv = pk(bl ? fsqrt(lo(z)) : al, bh ? fsqrt(hi(z)) : ah);
+  F2 pz = fma2(bc(4.2163199048e-2f), z, bc(2.4181311049e-2f));
+  pz = fma2(pz, z, bc(4.5470025998e-2f));
+  pz = fma2(pz, z, bc(7.4953002686e-2f));
+  pz = fma2(pz, z, bc(1.6666752422e-1f));
+  const F2 r = fma2(sv * z, pz, sv);
+  const F2 big = fma2(bc(-2.f), r, bc(1.57079632679489662f));
+  return pk(copysignf(bl ? lo(big) : lo(r), xl), copysignf(bh ? hi(big) : hi(r), xh));
+}
+
+struct StateOut2 {
+  F2 risk, pitch, roll, z;
+  unsigned trav_a, trav_b;
+};
+
+__device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, float href, float4 gc, float4 gd,
+                                               float2 csk, const AssessParams& p) {
+  const F2 mh = S0 * bc(gc.w);
+  const F2 C02 = SXH * bc(gd.x), C12 = SYH * bc(gd.x);
+  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * bc(gc.w));
+  const F2 tr = C22 + bc(gd.y);
+  const F2 q = tr * bc(1.f / 3.f);
+  const F2 b00 = bc(gc.x) - q, b11 = bc(gc.z) - q, b22 = C22 - q;
+  F2 p2 = fma2(C02, C02, fma2(C12, C12, bc(gd.z)));
+  p2 = p2 + p2;
+  p2 = fma2(b00, b00, fma2(b11, b11, fma2(b22, b22, p2)));
+  p2 = p2 * bc(1.f / 6.f);
+  const float p2l = lo(p2), p2h = hi(p2);
+  const bool okl = p2l > 0.f, okh = p2h > 0.f;  // isotropic covariance: no unique normal
+  const F2 ip = pk(rsqrtf(okl ? p2l : 1.f), rsqrtf(okh ? p2h : 1.f));
+  const F2 pp = p2 * ip;
+  const F2 d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = bc(gc.y) * ip, e02 = C02 * ip, e12 = C12 * ip;
+  // det(B/p) = d00 (d11 d22 - e12^2) - e01 (e01 d22 - e12 e02) + e02 (e01 e12 - d11 e02)
+  const F2 m1 = fma2(d11, d22, (e12 * e12) * bc(-1.f));
+  const F2 m2 = fma2(e01, d22, (e12 * e02) * bc(-1.f));
+  const F2 m3 = fma2(e01, e12, (d11 * e02) * bc(-1.f));
+  const F2 detB = fma2(e02, m3, fma2(d00, m1, (e01 * m2) * bc(-1.f)));
+  const F2 hr = pk(fminf(1.f, fmaxf(-1.f, 0.5f * lo(detB))), fminf(1.f, fmaxf(-1.f, 0.5f * hi(detB))));
+  const F2 phi = acos2(hr) * bc(1.f / 3.f);
+  float sl, cl, sh, ch;
+  __sincosf(lo(phi), &sl, &cl);
+  __sincosf(hi(phi), &sh, &ch);
+  const F2 lam0 = fma2(pp * bc(-1.f), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), q);
+  // eigenvector: largest cross product of two rows of M = C - lam0 I; one inverse-iteration step
+  const F2 C00 = bc(gc.x), C01 = bc(gc.y), C11 = bc(gc.z);
+  const F2 m00 = C00 - lam0, m11 = C11 - lam0, m22 = C22 - lam0;
+  const F2 a0 = fma2(C01, C12, (C02 * m11) * bc(-1.f)), a1 = fma2(C02, C01, (m00 * C12) * bc(-1.f)),
+           a2 = fma2(m00, m11, (C01 * C01) * bc(-1.f));
+  const F2 b0 = fma2(C01, m22, (C02 * C12) * bc(-1.f)), b1 = fma2(C02, C02, (m00 * m22) * bc(-1.f)),
+           b2 = fma2(m00, C12, (C01 * C02) * bc(-1.f));
+  const F2 c0 = fma2(m11, m22, (C12 * C12) * bc(-1.f)), c1 = fma2(C12, C02, (C01 * m22) * bc(-1.f)),
+           c2 = fma2(C01, C12, (m11 * C02) * bc(-1.f));
+  const F2 na = fma2(a0, a0, fma2(a1, a1, a2 * a2)), nb = fma2(b0, b0, fma2(b1, b1, b2 * b2)),
+           nc = fma2(c0, c0, fma2(c1, c1, c2 * c2));
+  const bool pal = lo(na) >= lo(nb) && lo(na) >= lo(nc), pbl = !pal && lo(nb) >= lo(nc);
+  const bool pah = hi(na) >= hi(nb) && hi(na) >= hi(nc), pbh = !pah && hi(nb) >= hi(nc);
+  const F2 v0 = pk(pal ? lo(a0) : (pbl ? lo(b0) : lo(c0)), pah ? hi(a0) : (pbh ? hi(b0) : hi(c0)));
+  const F2 v1 = pk(pal ? lo(a1) : (pbl ? lo(b1) : lo(c1)), pah ? hi(a1) : (pbh ? hi(b1) : hi(c1)));
+  const F2 v2 = pk(pal ? lo(a2) : (pbl ? lo(b2) : lo(c2)), pah ? hi(a2) : (pbh ? hi(b2) : hi(c2)));
+  const F2 x0 = fma2(v0, c0, fma2(v1 * bc(-1.f), b0, v2 * a0));
+  const F2 x1 = fma2(v0, c1, fma2(v1 * bc(-1.f), b1, v2 * a1));
+  const F2 x2 = fma2(v0, c2, fma2(v1 * bc(-1.f), b2, v2 * a2));
+  const F2 nx2 = fma2(x0, x0, fma2(x1, x1, x2 * x2));
+  const F2 nv2 = fma2(v0, v0, fma2(v1, v1, v2 * v2));
+  // fall back to the unrefined vector if the refinement under/overflowed
+  const bool rl = lo(nx2) > 0.f && lo(nx2) < 3.0e38f, rh = hi(nx2) > 0.f && hi(nx2) < 3.0e38f;
+  const F2 y0 = pk(rl ? lo(x0) : lo(v0), rh ? hi(x0) : hi(v0));
+  const F2 y1 = pk(rl ? lo(x1) : lo(v1), rh ? hi(x1) : hi(v1));
+  const F2 y2 = pk(rl ? lo(x2) : lo(v2), rh ? hi(x2) : hi(v2));
+  const float ql = rl ? lo(nx2) : lo(nv2), qh = rh ? hi(nx2) : hi(nv2);
+  const float il = rsqrtf(ql), ih = rsqrtf(qh);
+  const F2 inv = pk(lo(y2) < 0.f ? -il : il, hi(y2) < 0.f ? -ih : ih);  // z_b in S^2_+ 
+  const F2 n0 = y0 * inv, n1 = y1 * inv, n2 = y2 * inv;
+  // kappa = lambda_min / trace (reading R1), lambda_min = Rayleigh quotient of n
+  const F2 t0 = fma2(C00, n0, fma2(C01, n1, C02 * n2));
+  const F2 t1 = fma2(C01, n0, fma2(C11, n1, C12 * n2));
+  const F2 t2 = fma2(C02, n0, fma2(C12, n1, C22 * n2));
+  const F2 rq = fma2(n0, t0, fma2(n1, t1, n2 * t2));
+  const F2 kap = pk(fmaxf(0.f, lo(rq)) * frcp(lo(tr)), fmaxf(0.f, hi(rq)) * frcp(hi(tr)));
+  // Eqs. 2-3 reduced: b3.x_b = -n_z u / |n x x_yaw|, b3.y_b = (n_x sin - n_y cos) / |n x x_yaw|
+  const F2 u = fma2(n0, bc(csk.x), n1 * bc(csk.y));
+  const F2 t = fma2(n0, bc(csk.y), n1 * bc(-csk.x));
+  const F2 w = fma2(n2, n2, t * t);
+  const F2 rs = pk(rsqrtf(lo(w)), rsqrtf(hi(w)));
+  const F2 spv = (n2 * u) * (rs * bc(-1.f));
+  const F2 srv = t * rs;
+  const F2 sp = pk(fminf(1.f, fmaxf(-1.f, lo(spv))), fminf(1.f, fmaxf(-1.f, hi(spv))));
+  const F2 sr = pk(fminf(1.f, fmaxf(-1.f, lo(srv))), fminf(1.f, fmaxf(-1.f, hi(srv))));
+  const F2 pitch = asin2(sp), roll = asin2(sr);
+  const F2 ax = pk(fabsf(lo(pitch)), fabsf(hi(pitch))), ay = pk(fabsf(lo(roll)), fabsf(hi(roll)));
+  const F2 rk = fma2(bc(p.wk), kap, fma2(bc(p.wx), ax, ay * bc(p.wy)));
+  const bool el = lo(kap) > p.kappa_max || lo(ax) > p.phi_x_max || lo(ay) > p.phi_y_max;
+  const bool eh = hi(kap) > p.kappa_max || hi(ax) > p.phi_x_max || hi(ay) > p.phi_y_max;
+  const bool vl = okl && lo(n2) > 0.f, vh = okh && hi(n2) > 0.f;  // valid normal (reading R11)
+  const float qn = __int_as_float(0x7fc00000);
+  StateOut2 o;
+  o.risk = pk((vl && !el) ? lo(rk) : 1.f, (vh && !eh) ? hi(rk) : 1.f);
+  o.pitch = pk(vl ? lo(pitch) : qn, vh ? hi(pitch) : qn);
+  o.roll = pk(vl ? lo(roll) : qn, vh ? hi(roll) : qn);
+  const F2 zz = bc(href) + mh;  // unclipped: the fitted plane passes through the footprint mean (R14)
+  o.z = pk(vl ? lo(zz) : qn, vh ? hi(zz) : qn);
+  o.trav_a = (vl && !el) ? 1u : 0u;
+  o.trav_b = (vh && !eh) ? 1u : 0u;
+  return o;
+}
+
+// ------------------------------------------------------------------------------------------
 // The assess kernel.
 // ------------------------------------------------------------------------------------------
 template <int R_T>
@@ -287,12 +444,12 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       raw[idx] = v;
     }
   }
-  // stencil rows of this CTA's bins as byte offsets into the prefix arrays (halo row d, column R_T + a)
+  // non-empty stencil rows of this CTA's bins (compacted on the host) as byte offsets into the prefix
+  // arrays: (8*ea, 8*eb, 4*ea, dj) with ea = halo index of (row d, column R_T + a), eb = (d, R_T + b + 1)
   for (int idx = tid; idx < (ke - kb) * NR; idx += NTHREADS) {
-    const int d = idx % NR;
-    const int2 ab = p.runs[(size_t)kb * NR + idx];
-    const int ea = d * PW + R_T + ab.x, eb = d * PW + R_T + ab.y + 1;
-    runs_s[idx] = make_int4(ea * 8, eb * 8, ea * 4, eb * 4);
+    const int4 ab = p.runs[(size_t)kb * NR + idx];  // (a, b, d, -)
+    const int ea = ab.z * PW + R_T + ab.x, eb = ab.z * PW + R_T + ab.y + 1;
+    runs_s[idx] = make_int4(ea * 8, eb * 8, ea * 4, __float_as_int((float)(ab.z - R_T)));
   }
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
@@ -317,7 +474,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   float allvf = red[16];
 #pragma unroll
   for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); allvf = fminf(allvf, red[16 + w]); }
-  const bool fast = allvf > 0.5f;
+  const bool fast = allvf > 0.5f && !p.force_general;
   const float href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
@@ -397,6 +554,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 
   for (int k = kb; k < ke; ++k) {
     const int4* rk = runs_s + (k - kb) * NR;
+    const int nr = __ldg(p.nrows + k);
     const float4 g = __ldg(p.geo + k);
     const float2 csk = __ldg(p.cs + k);
     float2 S02[RPW];
@@ -409,14 +567,14 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       N[s] = g.x; Sx[s] = 0.f; Sy[s] = 0.f; Sxx[s] = g.y; Sxy[s] = g.z; Syy[s] = g.w;
     }
     if (fast) {
-#pragma unroll
-      for (int d = 0; d < NR; ++d) {
+#pragma unroll 2
+      for (int d = 0; d < nr; ++d) {
         const int4 o = rk[d];
-        const float dj = (float)(d - R_T);
+        const float dj = __int_as_float(o.w);
         const char* pa8 = b8 + o.x;
         const char* pb8 = b8 + o.y;
         const char* pa4 = b4 + o.z;
-        const char* pb4 = b4 + o.w;
+        const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
 #pragma unroll
         for (int s = 0; s < RPW; ++s) {
           const float2 A = *reinterpret_cast<const float2*>(pa8 + s * RS8);
@@ -432,20 +590,21 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     } else {
 #pragma unroll
       for (int s = 0; s < RPW; ++s) { N[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f; }
-#pragma unroll
-      for (int d = 0; d < NR; ++d) {
+#pragma unroll 1
+      for (int d = 0; d < nr; ++d) {
         const int4 o = rk[d];
-        const float dj = (float)(d - R_T);
+        const float dj = __int_as_float(o.w);
+        const int ob4 = o.z + ((o.y - o.x) >> 1);
 #pragma unroll
         for (int s = 0; s < RPW; ++s) {
           const float2 A = *reinterpret_cast<const float2*>(b8 + o.x + s * RS8);
           const float2 B = *reinterpret_cast<const float2*>(b8 + o.y + s * RS8);
           const float ax = *reinterpret_cast<const float*>(b4 + o.z + s * RS4);
-          const float bxv = *reinterpret_cast<const float*>(b4 + o.w + s * RS4);
+          const float bxv = *reinterpret_cast<const float*>(b4 + ob4 + s * RS4);
           const float2 VA = *reinterpret_cast<const float2*>(bv8 + o.x + s * RS8);
           const float2 VB = *reinterpret_cast<const float2*>(bv8 + o.y + s * RS8);
           const float wa = *reinterpret_cast<const float*>(bv4 + o.z + s * RS4);
-          const float wb = *reinterpret_cast<const float*>(bv4 + o.w + s * RS4);
+          const float wb = *reinterpret_cast<const float*>(bv4 + ob4 + s * RS4);
           const float2 dd = sub2(B, A);
           const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
           const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
@@ -465,19 +624,33 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     float4* outk2 = p.out + (size_t)(k + p.H) * plane;
     uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words + gword;
     uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words + gword;
-#pragma unroll
-    for (int s = 0; s < RPW; ++s) {
-      const StateOut o = epilogue(N[s], Sx[s], Sy[s], Sxx[s], Sxy[s], Syy[s], S02[s].x, S02[s].y, SXH[s], SYH[s],
-                                  href, csk, p, !fast);
+    auto store = [&](int s, float risk, float pitch, float roll, float z, unsigned trav) {
       if (in[s]) {
-        outk[off[s]] = make_float4(o.risk, o.pitch, o.roll, o.z);
-        if (p.paired) outk2[off[s]] = make_float4(o.risk, -o.pitch, -o.roll, o.z);
+        outk[off[s]] = make_float4(risk, pitch, roll, z);
+        if (p.paired) outk2[off[s]] = make_float4(risk, -pitch, -roll, z);
       }
       // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-      const unsigned tmask = __ballot_sync(0xffffffffu, in[s] && o.trav);
+      const unsigned tmask = __ballot_sync(0xffffffffu, in[s] && trav);
       if (lane == 0 && col_any && pys[s] >= 0) {
         travk[(size_t)pys[s] * p.trav_words] = tmask;
         if (p.paired) travk2[(size_t)pys[s] * p.trav_words] = tmask;
+      }
+    };
+    if (fast) {
+      const float4 gc = __ldg(p.geoc + 2 * k), gd = __ldg(p.geoc + 2 * k + 1);
+#pragma unroll
+      for (int s = 0; s < RPW; s += 2) {
+        const StateOut2 o = epilogue2(pk(S02[s].x, S02[s + 1].x), pk(S02[s].y, S02[s + 1].y), pk(SXH[s], SXH[s + 1]),
+                                      pk(SYH[s], SYH[s + 1]), href, gc, gd, csk, p);
+        store(s, lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
+        store(s + 1, hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < RPW; ++s) {
+        const StateOut o = epilogue(N[s], Sx[s], Sy[s], Sxx[s], Sxy[s], Syy[s], S02[s].x, S02[s].y, SXH[s], SYH[s],
+                                    href, csk, p, true);
+        store(s, o.risk, o.pitch, o.roll, o.z, (unsigned)o.trav);
       }
     }
   }

@@ -33,8 +33,10 @@ struct AssessParams {
   // yaw: rep bins k in [0, H); bin k + H (if paired) is the same footprint, x_yaw negated
   int n_yaw, H, paired;
   int R;                 // true footprint radius (cells); kernel template R_T >= R
-  const int2* runs;      // [H][2*R_T+1] per stencil row dj = -R_T..R_T: di run [a, b]; empty = (0, -1)
+  const int4* runs;      // [H][2*R_T+1] non-empty stencil rows, compacted: (a, b, d = dj + R_T, 0); di in [a, b]
+  const int* nrows;      // [H] number of non-empty rows of bin k
   const float4* geo;     // [H] full-stencil (N, Sxx, Sxy, Syy) in cell units (Sx = Sy = 0)
+  const float4* geoc;    // [H][2] full-stencil covariance: (C00, C01, C11, 1/N), (r/N, C00+C11, C01^2, 0), metres
   const float2* cs;      // [H] (cos, sin) of theta_k, k < H (reading R3)
   float r;               // resolution (m)
   // risk (Alg. 1 lines 10-18), all float
@@ -52,6 +54,7 @@ struct AssessParams {
   int k_begin, k_end;    // representative-bin range this launch covers
   int k_chunk;           // rep bins per CTA (grid.y = ceil((k_end-k_begin)/k_chunk))
   int use_tma;           // tensor map valid
+  int force_general;     // some full stencil is degenerate (< 3 cells or collinear): no interior fast path
 };
 
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.

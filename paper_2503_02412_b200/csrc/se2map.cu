@@ -47,8 +47,10 @@ struct se2m_map {
   float* d_h = nullptr;
   float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
-  int2* d_runs = nullptr;
+  int4* d_runs = nullptr;
+  int* d_nrows = nullptr;
   float4* d_geo = nullptr;
+  float4* d_geoc = nullptr;
   float2* d_cs = nullptr;
   std::vector<int> ncells;  // |P_k| per rep bin
   float* d_stage = nullptr;  // update / download staging
@@ -58,6 +60,7 @@ struct se2m_map {
   size_t q_cap = 0;
   CUtensorMap tmap;
   bool tma_ok = false;
+  bool force_general = false;  // a full stencil is degenerate (R22): every tile takes the general path
   bool have_data = false;
   bool all_dirty = true;
   std::vector<Rect> dirty;
@@ -88,7 +91,8 @@ static int pick_radius(int R) {
 
 // Footprint stencil, reading R5 (rule C5 of SURVEY.md §8(c)): cell centres, q in cell units with the
 // representative angle theta_k (k < H), include iff q <= 1 + 1e-9.  FP64 on the host, once.
-static bool build_stencils(se2m_map* m, std::vector<int2>& runs, std::vector<float4>& geo, std::vector<float2>& cs) {
+static bool build_stencils(se2m_map* m, std::vector<int4>& runs, std::vector<int>& nrows, std::vector<float4>& geo, std::vector<float4>& geoc,
+                           std::vector<float2>& cs) {
   const se2m_params& P = m->prm;
   const double a = P.ellipse_ex / P.resolution, b = P.ellipse_ey / P.resolution;
   const int Rs = (int)ceil(std::max(a, b)) + 1;
@@ -124,14 +128,23 @@ static bool build_stencils(se2m_map* m, std::vector<int2>& runs, std::vector<flo
   m->R_T = pick_radius(std::max(R, 1));
   if (m->R_T < 0) return false;
   const int NR = 2 * m->R_T + 1;
-  runs.assign((size_t)m->H * NR, make_int2(0, -1));
+  runs.assign((size_t)m->H * NR, make_int4(0, -1, 0, 0));
+  nrows.assign(m->H, 0);
   geo.resize(m->H);
+  geoc.resize(2 * (size_t)m->H);
   for (int k = 0; k < m->H; ++k) {
+    // full-stencil covariance of the cell-centre offsets, metres^2, FP64 then rounded (Sx = Sy = 0)
+    const double N = m->ncells[k], r = P.resolution;
+    const double c00 = r * r * Sxx[k] / N, c01 = r * r * Sxy[k] / N, c11 = r * r * Syy[k] / N;
+    geoc[2 * k] = make_float4((float)c00, (float)c01, (float)c11, (float)(1.0 / N));
+    geoc[2 * k + 1] = make_float4((float)(r / N), (float)(c00 + c11), (float)(c01 * c01), 0.f);
     for (int dj = -std::min(Rs, m->R_T); dj <= std::min(Rs, m->R_T); ++dj) {
       const Run& q = rr[k][dj + Rs];
-      if (q.hi >= q.lo) runs[(size_t)k * NR + dj + m->R_T] = make_int2(q.lo, q.hi);
+      if (q.hi >= q.lo) runs[(size_t)k * NR + nrows[k]++] = make_int4(q.lo, q.hi, dj + m->R_T, 0);
     }
     geo[k] = make_float4((float)m->ncells[k], (float)Sxx[k], (float)Sxy[k], (float)Syy[k]);
+    const double det2 = (double)Sxx[k] * Syy[k] - (double)Sxy[k] * Sxy[k];  // Sx = Sy = 0 (point symmetry)
+    if (m->ncells[k] < 3 || !(det2 > 0)) m->force_general = true;
   }
   return true;
 }
@@ -167,7 +180,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.out = m->d_out; p.trav = m->d_trav;
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
-  p.runs = m->d_runs; p.geo = m->d_geo; p.cs = m->d_cs;
+  p.runs = m->d_runs; p.nrows = m->d_nrows; p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
   p.kappa_max = (float)m->prm.kappa_max; p.phi_x_max = (float)m->prm.phi_x_max; p.phi_y_max = (float)m->prm.phi_y_max;
   p.wk = (float)(m->prm.w_r[0] / m->prm.kappa_max);
@@ -175,6 +188,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.wy = (float)(m->prm.w_r[2] / m->prm.phi_y_max);
   p.k_begin = m->k_lo; p.k_end = m->k_hi; p.k_chunk = 1;
   p.use_tma = m->tma_ok ? 1 : 0;
+  p.force_general = m->force_general ? 1 : 0;
   return p;
 }
 
@@ -243,10 +257,11 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     m->k_lo = (int)((long long)m->H * p->rank / p->world_size);
     m->k_hi = (int)((long long)m->H * (p->rank + 1) / p->world_size);
   }
-  std::vector<int2> runs;
-  std::vector<float4> geo;
+  std::vector<int4> runs;
+  std::vector<int> nrows;
+  std::vector<float4> geo, geoc;
   std::vector<float2> cs;
-  if (!build_stencils(m, runs, geo, cs)) {
+  if (!build_stencils(m, runs, nrows, geo, geoc, cs)) {
     fail(m, SE2M_ERR_UNSUPPORTED, "footprint stencil could not be built (radius or shape)");
     return bail(SE2M_ERR_UNSUPPORTED);
   }
@@ -261,8 +276,10 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       {(void**)&m->d_h, (size_t)m->ldh * p->ny * 4, "heights"},
       {(void**)&m->d_out, nst * sizeof(float4), "state records"},
       {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
-      {(void**)&m->d_runs, runs.size() * sizeof(int2), "runs"},
+      {(void**)&m->d_runs, runs.size() * sizeof(int4), "runs"},
+      {(void**)&m->d_nrows, nrows.size() * sizeof(int), "nrows"},
       {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
+      {(void**)&m->d_geoc, geoc.size() * sizeof(float4), "geoc"},
       {(void**)&m->d_cs, cs.size() * sizeof(float2), "cs"},
   };
   for (auto& a : allocs) {
@@ -272,8 +289,10 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       return bail(e == cudaErrorMemoryAllocation ? SE2M_ERR_OOM : SE2M_ERR_CUDA);
     }
   }
-  if ((e = cudaMemcpyAsync(m->d_runs, runs.data(), runs.size() * sizeof(int2), cudaMemcpyHostToDevice, m->stream)) ||
+  if ((e = cudaMemcpyAsync(m->d_runs, runs.data(), runs.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_nrows, nrows.data(), nrows.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_geo, geo.data(), geo.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_geoc, geoc.data(), geoc.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemsetAsync(m->d_h, 0xff, (size_t)m->ldh * p->ny * 4, m->stream)) ||  // 0xffffffff = NaN: unknown
       (e = cudaMemsetAsync(m->d_trav, 0, (size_t)n * p->ny * m->trav_words * 4, m->stream)) ||
@@ -289,7 +308,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_runs, m->d_geo,
+  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_runs, m->d_nrows, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qidx, m->d_qout};
   for (void* q : ptrs)
     if (q) cudaFree(q);
