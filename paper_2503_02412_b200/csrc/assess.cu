@@ -83,129 +83,6 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) {
 // MUFU approximations (relative error ~1 ulp); the eigenvector refinement absorbs them.
 __device__ __forceinline__ float frcp(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
 __device__ __forceinline__ float fsqrt(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
-// acos on [-1, 1]: Abramowitz & Stegun 4.4.46, acos(a) = sqrt(1 - a) * P7(a) for a in [0, 1].
-__device__ __forceinline__ float acos_fast(float x) {
-  const float a = fabsf(x);
-  float pz = fmaf(-0.0012624911f, a, 0.0066700901f);
-  pz = fmaf(pz, a, -0.0170881256f);
-  pz = fmaf(pz, a, 0.0308918810f);
-  pz = fmaf(pz, a, -0.0501743046f);
-  pz = fmaf(pz, a, 0.0889789874f);
-  pz = fmaf(pz, a, -0.2145988016f);
-  pz = fmaf(pz, a, 1.5707963050f);
-  const float r = fsqrt(1.f - a) * pz;
-  return x < 0.f ? 3.14159265358979f - r : r;
-}
-// asin on [-1, 1], branch-free Cephes asinf (odd: asin(-x) = -asin(x), asin(0) = 0 exactly).
-__device__ __forceinline__ float asin_fast(float x) {
-  const float a = fabsf(x);
-  const bool big = a > 0.5f;
-  const float z = big ? 0.5f * (1.f - a) : a * a;
-  const float s = big ? fsqrt(z) : a;
-  float pz = fmaf(4.2163199048e-2f, z, 2.4181311049e-2f);
-  pz = fmaf(pz, z, 4.5470025998e-2f);
-  pz = fmaf(pz, z, 7.4953002686e-2f);
-  pz = fmaf(pz, z, 1.6666752422e-1f);
-  float r = fmaf(s * z, pz, s);
-  r = big ? fmaf(-2.f, r, 1.57079632679489662f) : r;
-  return copysignf(r, x);
-}
-
-struct StateOut {
-  float risk, pitch, roll, z;
-  int trav;
-};
-
-// ------------------------------------------------------------------------------------------
-// Register epilogue: moments -> covariance -> smallest eigenpair -> kappa, z, pitch, roll, risk.
-// Moments are in cell units for x, y (dx = di*r) and metres for h^ = h - href.
-// ------------------------------------------------------------------------------------------
-__device__ __forceinline__ StateOut epilogue(float N, float Sx, float Sy, float Sxx, float Sxy, float Syy,
-                                             float S0, float S2, float SXH, float SYH, float href,
-                                             float2 csk, const AssessParams& p, bool general) {
-  StateOut o;
-  o.risk = 1.f;
-  o.pitch = o.roll = o.z = __int_as_float(0x7fc00000);
-  o.trav = 0;
-  if (N < 2.5f) return o;  // |P| < 3: unknown (reading R8)
-  const float invN = frcp(N);
-  const float mx = Sx * invN, my = Sy * invN, mh = S0 * invN;
-  if (general) {
-    // collinear footprint cells (exact integer moments): degenerate covariance (reading R11)
-    const double dN = N;
-    const double a = dN * Sxx - (double)Sx * Sx, b = dN * Syy - (double)Sy * Sy, c = dN * Sxy - (double)Sx * Sy;
-    if (!(a * b - c * c > 1e-9 * a * b)) return o;
-  }
-  const float r = p.r, r2 = r * r;
-  // Cov of Alg. 1 line 8 (divisor N), metres
-  const float C00 = r2 * fmaf(-mx, mx, Sxx * invN);
-  const float C01 = r2 * fmaf(-mx, my, Sxy * invN);
-  const float C11 = r2 * fmaf(-my, my, Syy * invN);
-  const float C02 = r * fmaf(-mx, mh, SXH * invN);
-  const float C12 = r * fmaf(-my, mh, SYH * invN);
-  const float C22 = fmaf(-mh, mh, S2 * invN);
-  // smallest eigenvalue: trigonometric closed form on B = (C - q I)/p
-  const float tr = C00 + C11 + C22;
-  const float q = tr * (1.f / 3.f);
-  const float b00 = C00 - q, b11 = C11 - q, b22 = C22 - q;
-  const float p2 = (b00 * b00 + b11 * b11 + b22 * b22 + 2.f * (C01 * C01 + C02 * C02 + C12 * C12)) * (1.f / 6.f);
-  if (!(p2 > 0.f)) return o;  // isotropic: no unique normal
-  const float ip = rsqrtf(p2);
-  const float pp = p2 * ip;
-  const float d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = C01 * ip, e02 = C02 * ip, e12 = C12 * ip;
-  const float detB = d00 * (d11 * d22 - e12 * e12) - e01 * (e01 * d22 - e12 * e02) + e02 * (e01 * e12 - d11 * e02);
-  const float hr = fminf(1.f, fmaxf(-1.f, 0.5f * detB));
-  const float phi = acos_fast(hr) * (1.f / 3.f);
-  float sphi, cphi;
-  __sincosf(phi, &sphi, &cphi);
-  const float lam0 = fmaf(-pp, fmaf(1.73205080756887729f, sphi, cphi), q);  // q + 2p cos(phi + 2pi/3)
-  // eigenvector: largest cross product of two rows of M = C - lam0 I (columns of adj(M))
-  const float m00 = C00 - lam0, m11 = C11 - lam0, m22 = C22 - lam0;
-  const float a0 = C01 * C12 - C02 * m11, a1 = C02 * C01 - m00 * C12, a2 = m00 * m11 - C01 * C01;  // r0 x r1
-  const float b0 = C01 * m22 - C02 * C12, b1 = C02 * C02 - m00 * m22, b2 = m00 * C12 - C01 * C02;  // r0 x r2
-  const float c0 = m11 * m22 - C12 * C12, c1 = C12 * C02 - C01 * m22, c2 = C01 * C12 - m11 * C02;  // r1 x r2
-  const float na = a0 * a0 + a1 * a1 + a2 * a2, nb = b0 * b0 + b1 * b1 + b2 * b2, nc = c0 * c0 + c1 * c1 + c2 * c2;
-  const bool pa = na >= nb && na >= nc, pb = !pa && nb >= nc;
-  const float v0 = pa ? a0 : (pb ? b0 : c0), v1 = pa ? a1 : (pb ? b1 : c1), v2 = pa ? a2 : (pb ? b2 : c2);
-  // one inverse-iteration step with the same shift: x = adj(M) v = v0 (r1 x r2) + v1 (r2 x r0) + v2 (r0 x r1)
-  float x0 = v0 * c0 - v1 * b0 + v2 * a0;
-  float x1 = v0 * c1 - v1 * b1 + v2 * a1;
-  float x2 = v0 * c2 - v1 * b2 + v2 * a2;
-  float nx2 = x0 * x0 + x1 * x1 + x2 * x2;
-  if (!(nx2 > 0.f) || !(nx2 < 3.0e38f)) {
-    x0 = v0; x1 = v1; x2 = v2;
-    nx2 = x0 * x0 + x1 * x1 + x2 * x2;
-    if (!(nx2 > 0.f)) return o;
-  }
-  float inv = rsqrtf(nx2);
-  if (x2 < 0.f) inv = -inv;  // z_b in S^2_+ 
-  const float n0 = x0 * inv, n1 = x1 * inv, n2 = x2 * inv;
-  if (!(n2 > 0.f)) return o;  // vertical plane: no S^2_+ normal (reading R11)
-  // kappa_ter = lambda_min / trace (reading R1), lambda_min by the Rayleigh quotient of n
-  const float t0 = C00 * n0 + C01 * n1 + C02 * n2;
-  const float t1 = C01 * n0 + C11 * n1 + C12 * n2;
-  const float t2 = C02 * n0 + C12 * n1 + C22 * n2;
-  const float lmin = fmaxf(0.f, n0 * t0 + n1 * t1 + n2 * t2);
-  const float kappa = lmin * frcp(tr);
-  // z = f_1: fitted plane at the state centre (reading R14)
-  o.z = href + fmaf(r * (n0 * mx + n1 * my), frcp(n2), mh);
-  // Eqs. 2-3 reduced by the vector triple product: b3.x_b = -n_z u / |n x x_yaw|,
-  // b3.y_b = (n_x sin - n_y cos) / |n x x_yaw|, |n x x_yaw|^2 = n_z^2 + (n_x sin - n_y cos)^2
-  const float u = n0 * csk.x + n1 * csk.y;
-  const float t = n0 * csk.y - n1 * csk.x;
-  const float rs = rsqrtf(fmaf(n2, n2, t * t));
-  const float sp = fminf(1.f, fmaxf(-1.f, -n2 * u * rs));
-  const float sr = fminf(1.f, fmaxf(-1.f, t * rs));
-  o.pitch = asin_fast(sp);
-  o.roll = asin_fast(sr);
-  const float ax = fabsf(o.pitch), ay = fabsf(o.roll);
-  // Alg. 1 lines 10-18 (strict >, reading R15); risk = w . [k/kmax, phx/phxmax, phy/phymax]
-  const bool early = (kappa > p.kappa_max) || (ax > p.phi_x_max) || (ay > p.phi_y_max);
-  o.risk = early ? 1.f : fmaf(p.wk, kappa, fmaf(p.wx, ax, p.wy * ay));
-  o.trav = early ? 0 : 1;
-  return o;
-}
-
 // ------------------------------------------------------------------------------------------
 // Packed two-state epilogue for interior tiles (all footprint cells known and inside the window).
 // Every FP32 add/mul/fma runs as one sm_100a FADD2/FMUL2/FFMA2 on (state a, state b); MUFU, compares
@@ -231,12 +108,19 @@ __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
   return d;
 }
-template <class Fn>
-__device__ __forceinline__ F2 map2(F2 x, Fn f) { return pk(f(lo(x)), f(hi(x))); }
+__device__ __forceinline__ F2 abs2(F2 x) { return pk(fabsf(lo(x)), fabsf(hi(x))); }
+__device__ __forceinline__ F2 rsqrt2(F2 x) { return pk(rsqrtf(lo(x)), rsqrtf(hi(x))); }
+__device__ __forceinline__ F2 rcp2(F2 x) { return pk(frcp(lo(x)), frcp(hi(x))); }
+__device__ __forceinline__ F2 sqrt2abs(F2 x) { return pk(fsqrt(fabsf(lo(x))), fsqrt(fabsf(hi(x)))); }
+__device__ __forceinline__ F2 copysign2(F2 m, F2 sg) { return pk(copysignf(lo(m), lo(sg)), copysignf(hi(m), hi(sg))); }
+__device__ __forceinline__ F2 sel2(bool cl, bool ch, F2 a, F2 b) { return pk(cl ? lo(a) : lo(b), ch ? hi(a) : hi(b)); }
 
-__device__ __forceinline__ F2 acos2(F2 x) {  // A&S 4.4.46, packed polynomial
-  const float xl = lo(x), xh = hi(x);
-  const F2 a = pk(fabsf(xl), fabsf(xh));
+constexpr float kPi2 = 1.57079632679489662f;
+
+// acos on [-1, 1] (Abramowitz & Stegun 4.4.46: acos(a) = sqrt(1 - a) P7(a), a in [0, 1]),
+// branch-free: acos(x) = pi/2 - sign(x) (pi/2 - acos(|x|)).  |1 - a| absorbs a 1-ulp overshoot.
+__device__ __forceinline__ F2 acos2(F2 x) {
+  const F2 a = abs2(x);
   F2 pz = fma2(bc(-0.0012624911f), a, bc(0.0066700901f));
   pz = fma2(pz, a, bc(-0.0170881256f));
   pz = fma2(pz, a, bc(0.0308918810f));
@@ -244,27 +128,22 @@ __device__ __forceinline__ F2 acos2(F2 x) {  // A&S 4.4.46, packed polynomial
   pz = fma2(pz, a, bc(0.0889789874f));
   pz = fma2(pz, a, bc(-0.2145988016f));
   pz = fma2(pz, a, bc(1.5707963050f));
-  const F2 om = bc(1.f) - a;
-  const F2 r = pk(fsqrt(lo(om)), fsqrt(hi(om))) * pz;
-  const float rl = lo(r), rh = hi(r);
-  return pk(xl < 0.f ? 3.14159265358979f - rl : rl, xh < 0.f ? 3.14159265358979f - rh : rh);
+  const F2 r = sqrt2abs(bc(1.f) - a) * pz;  // acos(|x|)
+  return bc(kPi2) - copysign2(bc(kPi2) - r, x);
 }
-__device__ __forceinline__ F2 asin2(F2 x) {  // Cephes asinf, packed polynomial; odd, asin(0) = 0
-  const float xl = lo(x), xh = hi(x);
-  const float al = fabsf(xl), ah = fabsf(xh);
-  const bool bl = al > 0.5f, bh = ah > 0.5f;
-  const F2 a = pk(al, ah);
-  const F2 sq = a * a;
-  const F2 half = fma2(bc(-0.5f), a, bc(0.5f));  // (1 - a) / 2
-  const F2 z = pk(bl ? lo(half) : lo(sq), bh ? hi(half) : hi(sq));
-  const F2 sv = pk(bl ? fsqrt(lo(z)) : al, bh ? fsqrt(hi(z)) : ah);
+// asin on [-1, 1] (Cephes asinf), branch-free, odd: asin(0) = 0 exactly, asin(-x) = -asin(x).
+__device__ __forceinline__ F2 asin2(F2 x) {
+  const F2 a = abs2(x);
+  const bool bl = lo(a) > 0.5f, bh = hi(a) > 0.5f;
+  const F2 zb = fma2(bc(-0.5f), a, bc(0.5f));  // (1 - a)/2
+  const F2 z = sel2(bl, bh, zb, a * a);
+  const F2 sv = sel2(bl, bh, sqrt2abs(zb), a);
   F2 pz = fma2(bc(4.2163199048e-2f), z, bc(2.4181311049e-2f));
   pz = fma2(pz, z, bc(4.5470025998e-2f));
   pz = fma2(pz, z, bc(7.4953002686e-2f));
   pz = fma2(pz, z, bc(1.6666752422e-1f));
   const F2 r = fma2(sv * z, pz, sv);
-  const F2 big = fma2(bc(-2.f), r, bc(1.57079632679489662f));
-  return pk(copysignf(bl ? lo(big) : lo(r), xl), copysignf(bh ? hi(big) : hi(r), xh));
+  return copysign2(sel2(bl, bh, fma2(bc(-2.f), r, bc(kPi2)), r), x);
 }
 
 struct StateOut2 {
@@ -272,95 +151,120 @@ struct StateOut2 {
   unsigned trav_a, trav_b;
 };
 
-__device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, float href, float4 gc, float4 gd,
-                                               float2 csk, const AssessParams& p) {
-  const F2 mh = S0 * bc(gc.w);
-  const F2 C02 = SXH * bc(gd.x), C12 = SYH * bc(gd.x);
-  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * bc(gc.w));
-  const F2 tr = C22 + bc(gd.y);
-  const F2 q = tr * bc(1.f / 3.f);
-  const F2 b00 = bc(gc.x) - q, b11 = bc(gc.z) - q, b22 = C22 - q;
-  F2 p2 = fma2(C02, C02, fma2(C12, C12, bc(gd.z)));
-  p2 = p2 + p2;
-  p2 = fma2(b00, b00, fma2(b11, b11, fma2(b22, b22, p2)));
-  p2 = p2 * bc(1.f / 6.f);
-  const float p2l = lo(p2), p2h = hi(p2);
-  const bool okl = p2l > 0.f, okh = p2h > 0.f;  // isotropic covariance: no unique normal
-  const F2 ip = pk(rsqrtf(okl ? p2l : 1.f), rsqrtf(okh ? p2h : 1.f));
+// Covariance (metres; Alg. 1 lines 2-8) -> GetMinEigenVecWithCurv (line 9) -> frame, angles, risk
+// (lines 10-18) for two states at once.  The covariance is first normalised by its trace
+// (eigenvectors unchanged, eigenvalues / trace), so kappa (reading R1) is the smallest eigenvalue
+// directly and no product can under/overflow.  Smallest eigenvalue: trigonometric closed form;
+// eigenvector: v = r0 x r1, the adj(M) column along b3 (M = C - lam0 I), refined once by x = adj(M) v
+// (one inverse-iteration step with the same shift).  ok_*: the footprint is assessable (|P| >= 3,
+// not collinear); a NaN anywhere (degenerate covariance) also ends as "unknown" (reading R11).
+template <bool GENERAL>
+__device__ __forceinline__ StateOut2 solve2(F2 C00, F2 C01, F2 C11, F2 Cp02, F2 Cp12, F2 Cp22, F2 mx, F2 my, F2 zz,
+                                            bool okl, bool okh, float Gx, float Gy, float2 csk,
+                                            const AssessParams& p) {
+  // covariance of (x, y, h) from that of (x, y, h^), h = h^ + Gx x + Gy y + const (tile plane)
+  const F2 C02 = fma2(bc(Gx), C00, fma2(bc(Gy), C01, Cp02));
+  const F2 C12 = fma2(bc(Gx), C01, fma2(bc(Gy), C11, Cp12));
+  const F2 C22 = fma2(bc(Gx), Cp02 + C02, fma2(bc(Gy), Cp12 + C12, Cp22));
+  const F2 it = rcp2(C00 + C11 + C22);
+  const F2 c00 = C00 * it, c01 = C01 * it, c11 = C11 * it, c02 = C02 * it, c12 = C12 * it, c22 = C22 * it;
+  const F2 third = bc(1.f / 3.f);
+  const F2 b00 = c00 - third, b11 = c11 - third, b22 = c22 - third;
+  F2 p2 = fma2(c02, c02, fma2(c12, c12, c01 * c01));
+  p2 = fma2(b00, b00, fma2(b11, b11, fma2(b22, b22, p2 + p2))) * bc(1.f / 6.f);
+  const F2 ip = rsqrt2(p2);
   const F2 pp = p2 * ip;
-  const F2 d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = bc(gc.y) * ip, e02 = C02 * ip, e12 = C12 * ip;
-  // det(B/p) = d00 (d11 d22 - e12^2) - e01 (e01 d22 - e12 e02) + e02 (e01 e12 - d11 e02)
+  const F2 d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = c01 * ip, e02 = c02 * ip, e12 = c12 * ip;
+  // det(B) / 2, B = (C' - I/3)/p:  d00 (d11 d22 - e12^2) - e01 (e01 d22 - e12 e02) + e02 (e01 e12 - d11 e02)
   const F2 m1 = fma2(d11, d22, (e12 * e12) * bc(-1.f));
   const F2 m2 = fma2(e01, d22, (e12 * e02) * bc(-1.f));
   const F2 m3 = fma2(e01, e12, (d11 * e02) * bc(-1.f));
-  const F2 detB = fma2(e02, m3, fma2(d00, m1, (e01 * m2) * bc(-1.f)));
-  const F2 hr = pk(fminf(1.f, fmaxf(-1.f, 0.5f * lo(detB))), fminf(1.f, fmaxf(-1.f, 0.5f * hi(detB))));
-  const F2 phi = acos2(hr) * bc(1.f / 3.f);
+  const F2 hr = fma2(e02, m3, fma2(d00, m1, (e01 * m2) * bc(-1.f))) * bc(0.5f);
+  const F2 phi = acos2(hr) * third;
   float sl, cl, sh, ch;
   __sincosf(lo(phi), &sl, &cl);
   __sincosf(hi(phi), &sh, &ch);
-  const F2 lam0 = fma2(pp * bc(-1.f), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), q);
-  // eigenvector: largest cross product of two rows of M = C - lam0 I; one inverse-iteration step
-  const F2 C00 = bc(gc.x), C01 = bc(gc.y), C11 = bc(gc.z);
-  const F2 m00 = C00 - lam0, m11 = C11 - lam0, m22 = C22 - lam0;
-  const F2 a0 = fma2(C01, C12, (C02 * m11) * bc(-1.f)), a1 = fma2(C02, C01, (m00 * C12) * bc(-1.f)),
-           a2 = fma2(m00, m11, (C01 * C01) * bc(-1.f));
-  const F2 b0 = fma2(C01, m22, (C02 * C12) * bc(-1.f)), b1 = fma2(C02, C02, (m00 * m22) * bc(-1.f)),
-           b2 = fma2(m00, C12, (C01 * C02) * bc(-1.f));
-  const F2 c0 = fma2(m11, m22, (C12 * C12) * bc(-1.f)), c1 = fma2(C12, C02, (C01 * m22) * bc(-1.f)),
-           c2 = fma2(C01, C12, (m11 * C02) * bc(-1.f));
-  const F2 na = fma2(a0, a0, fma2(a1, a1, a2 * a2)), nb = fma2(b0, b0, fma2(b1, b1, b2 * b2)),
-           nc = fma2(c0, c0, fma2(c1, c1, c2 * c2));
-  const bool pal = lo(na) >= lo(nb) && lo(na) >= lo(nc), pbl = !pal && lo(nb) >= lo(nc);
-  const bool pah = hi(na) >= hi(nb) && hi(na) >= hi(nc), pbh = !pah && hi(nb) >= hi(nc);
-  const F2 v0 = pk(pal ? lo(a0) : (pbl ? lo(b0) : lo(c0)), pah ? hi(a0) : (pbh ? hi(b0) : hi(c0)));
-  const F2 v1 = pk(pal ? lo(a1) : (pbl ? lo(b1) : lo(c1)), pah ? hi(a1) : (pbh ? hi(b1) : hi(c1)));
-  const F2 v2 = pk(pal ? lo(a2) : (pbl ? lo(b2) : lo(c2)), pah ? hi(a2) : (pbh ? hi(b2) : hi(c2)));
-  const F2 x0 = fma2(v0, c0, fma2(v1 * bc(-1.f), b0, v2 * a0));
-  const F2 x1 = fma2(v0, c1, fma2(v1 * bc(-1.f), b1, v2 * a1));
-  const F2 x2 = fma2(v0, c2, fma2(v1 * bc(-1.f), b2, v2 * a2));
-  const F2 nx2 = fma2(x0, x0, fma2(x1, x1, x2 * x2));
-  const F2 nv2 = fma2(v0, v0, fma2(v1, v1, v2 * v2));
-  // fall back to the unrefined vector if the refinement under/overflowed
-  const bool rl = lo(nx2) > 0.f && lo(nx2) < 3.0e38f, rh = hi(nx2) > 0.f && hi(nx2) < 3.0e38f;
-  const F2 y0 = pk(rl ? lo(x0) : lo(v0), rh ? hi(x0) : hi(v0));
-  const F2 y1 = pk(rl ? lo(x1) : lo(v1), rh ? hi(x1) : hi(v1));
-  const F2 y2 = pk(rl ? lo(x2) : lo(v2), rh ? hi(x2) : hi(v2));
-  const float ql = rl ? lo(nx2) : lo(nv2), qh = rh ? hi(nx2) : hi(nv2);
-  const float il = rsqrtf(ql), ih = rsqrtf(qh);
-  const F2 inv = pk(lo(y2) < 0.f ? -il : il, hi(y2) < 0.f ? -ih : ih);  // z_b in S^2_+ 
-  const F2 n0 = y0 * inv, n1 = y1 * inv, n2 = y2 * inv;
-  // kappa = lambda_min / trace (reading R1), lambda_min = Rayleigh quotient of n
-  const F2 t0 = fma2(C00, n0, fma2(C01, n1, C02 * n2));
-  const F2 t1 = fma2(C01, n0, fma2(C11, n1, C12 * n2));
-  const F2 t2 = fma2(C02, n0, fma2(C12, n1, C22 * n2));
+  const F2 lam0 = fma2(pp * bc(-1.f), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), third);
+  const F2 m00 = c00 - lam0, m11 = c11 - lam0, m22 = c22 - lam0;
+  // rows r0 = (m00, c01, c02), r1 = (c01, m11, c12), r2 = (c02, c12, m22); adj(M) = [r1xr2, r2xr0, r0xr1]
+  const F2 a0 = fma2(c01, c12, (c02 * m11) * bc(-1.f)), a1 = fma2(c02, c01, (m00 * c12) * bc(-1.f)),
+           a2 = fma2(m00, m11, (c01 * c01) * bc(-1.f));                       // r0 x r1
+  const F2 b0 = fma2(c01, m22, (c02 * c12) * bc(-1.f)), b1 = fma2(c02, c02, (m00 * m22) * bc(-1.f)),
+           b2 = fma2(m00, c12, (c01 * c02) * bc(-1.f));                       // r0 x r2 = -(r2 x r0)
+  const F2 g0 = fma2(m11, m22, (c12 * c12) * bc(-1.f)), g1 = fma2(c12, c02, (c01 * m22) * bc(-1.f)),
+           g2 = fma2(c01, c12, (m11 * c02) * bc(-1.f));                       // r1 x r2
+  // seed v = a = r0 x r1, the adj(M) column along b3 (|a| ~ n_z: well conditioned for the tilts that
+  // are assessed, |angle| < 1.3 rad, reading R12); x = adj(M) v
+  const F2 x0 = fma2(a0, g0, fma2(a1 * bc(-1.f), b0, a2 * a0));
+  const F2 x1 = fma2(a0, g1, fma2(a1 * bc(-1.f), b1, a2 * a1));
+  const F2 x2 = fma2(a0, g2, fma2(a1 * bc(-1.f), b2, a2 * a2));
+  const F2 inv = copysign2(rsqrt2(fma2(x0, x0, fma2(x1, x1, x2 * x2))), x2);  // z_b in S^2_+ 
+  const F2 n0 = x0 * inv, n1 = x1 * inv, n2 = x2 * inv;
+  // kappa = lambda_min / trace = Rayleigh quotient of n on C' (reading R1)
+  const F2 t0 = fma2(c00, n0, fma2(c01, n1, c02 * n2));
+  const F2 t1 = fma2(c01, n0, fma2(c11, n1, c12 * n2));
+  const F2 t2 = fma2(c02, n0, fma2(c12, n1, c22 * n2));
   const F2 rq = fma2(n0, t0, fma2(n1, t1, n2 * t2));
-  const F2 kap = pk(fmaxf(0.f, lo(rq)) * frcp(lo(tr)), fmaxf(0.f, hi(rq)) * frcp(hi(tr)));
+  const F2 kap = pk(fmaxf(0.f, lo(rq)), fmaxf(0.f, hi(rq)));
   // Eqs. 2-3 reduced: b3.x_b = -n_z u / |n x x_yaw|, b3.y_b = (n_x sin - n_y cos) / |n x x_yaw|
   const F2 u = fma2(n0, bc(csk.x), n1 * bc(csk.y));
   const F2 t = fma2(n0, bc(csk.y), n1 * bc(-csk.x));
-  const F2 w = fma2(n2, n2, t * t);
-  const F2 rs = pk(rsqrtf(lo(w)), rsqrtf(hi(w)));
-  const F2 spv = (n2 * u) * (rs * bc(-1.f));
-  const F2 srv = t * rs;
-  const F2 sp = pk(fminf(1.f, fmaxf(-1.f, lo(spv))), fminf(1.f, fmaxf(-1.f, hi(spv))));
-  const F2 sr = pk(fminf(1.f, fmaxf(-1.f, lo(srv))), fminf(1.f, fmaxf(-1.f, hi(srv))));
-  const F2 pitch = asin2(sp), roll = asin2(sr);
-  const F2 ax = pk(fabsf(lo(pitch)), fabsf(hi(pitch))), ay = pk(fabsf(lo(roll)), fabsf(hi(roll)));
+  const F2 rs = rsqrt2(fma2(n2, n2, t * t));
+  const F2 pitch = asin2((n2 * u) * (rs * bc(-1.f)));
+  const F2 roll = asin2(t * rs);
+  const F2 ax = abs2(pitch), ay = abs2(roll);
   const F2 rk = fma2(bc(p.wk), kap, fma2(bc(p.wx), ax, ay * bc(p.wy)));
   const bool el = lo(kap) > p.kappa_max || lo(ax) > p.phi_x_max || lo(ay) > p.phi_y_max;
   const bool eh = hi(kap) > p.kappa_max || hi(ax) > p.phi_x_max || hi(ay) > p.phi_y_max;
-  const bool vl = okl && lo(n2) > 0.f, vh = okh && hi(n2) > 0.f;  // valid normal (reading R11)
-  const float qn = __int_as_float(0x7fc00000);
+  const bool vl = okl && lo(n2) > 0.f, vh = okh && hi(n2) > 0.f;  // NaN fails: unknown (reading R11)
+  // z = f_1: the fitted plane at the state centre (reading R14); zz = mean footprint height
+  if (GENERAL) zz = fma2(fma2(n0, mx, n1 * my), rcp2(n2), zz);
+  const F2 qn = bc(__int_as_float(0x7fc00000));
   StateOut2 o;
-  o.risk = pk((vl && !el) ? lo(rk) : 1.f, (vh && !eh) ? hi(rk) : 1.f);
-  o.pitch = pk(vl ? lo(pitch) : qn, vh ? hi(pitch) : qn);
-  o.roll = pk(vl ? lo(roll) : qn, vh ? hi(roll) : qn);
-  const F2 zz = bc(href) + mh;  // unclipped: the fitted plane passes through the footprint mean (R14)
-  o.z = pk(vl ? lo(zz) : qn, vh ? hi(zz) : qn);
+  o.risk = sel2(vl && !el, vh && !eh, rk, bc(1.f));
+  o.pitch = sel2(vl, vh, pitch, qn);
+  o.roll = sel2(vl, vh, roll, qn);
+  o.z = sel2(vl, vh, zz, qn);
   o.trav_a = (vl && !el) ? 1u : 0u;
   o.trav_b = (vh && !eh) ? 1u : 0u;
   return o;
+}
+
+// interior tiles: geometry constants per bin gc = (C00, C01, C11, 1/N), gd = (r/N, -, -, -);
+// zref = tile-plane height at each state (the footprint is centred, so the mean height is zref + mean h^)
+__device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zref, float Gx, float Gy, float4 gc,
+                                               float4 gd, float2 csk, const AssessParams& p) {
+  const F2 mh = S0 * bc(gc.w);
+  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * bc(gc.w));
+  const F2 z0 = bc(0.f);
+  return solve2<false>(bc(gc.x), bc(gc.y), bc(gc.z), SXH * bc(gd.x), SYH * bc(gd.x), C22, z0, z0, zref + mh, true,
+                       true, Gx, Gy, csk, p);
+}
+
+// border / unknown tiles: per-state moments (cell units for x, y; metres for h^)
+__device__ __forceinline__ bool assessable(float N, float Sx, float Sy, float Sxx, float Sxy, float Syy) {
+  if (N < 2.5f) return false;  // |P| < 3 (reading R8)
+  const double dN = N;         // collinear footprint cells: exact integer test (reading R22)
+  const double a = dN * Sxx - (double)Sx * Sx, b = dN * Syy - (double)Sy * Sy, c = dN * Sxy - (double)Sx * Sy;
+  return a * b - c * c > 1e-9 * a * b;
+}
+__device__ __forceinline__ StateOut2 epilogue2_general(F2 N, F2 Sx, F2 Sy, F2 Sxx, F2 Sxy, F2 Syy, F2 S0, F2 S2, F2 SXH,
+                                                       F2 SYH, F2 zref, float gx, float gy, float2 csk,
+                                                       const AssessParams& p) {
+  const bool okl = assessable(lo(N), lo(Sx), lo(Sy), lo(Sxx), lo(Sxy), lo(Syy));
+  const bool okh = assessable(hi(N), hi(Sx), hi(Sy), hi(Sxx), hi(Sxy), hi(Syy));
+  const F2 iN = rcp2(sel2(okl, okh, N, bc(3.f)));
+  const F2 mxc = Sx * iN, myc = Sy * iN, mh = S0 * iN;
+  const F2 r = bc(p.r), r2 = bc(p.r * p.r);
+  const F2 C00 = r2 * fma2(mxc * bc(-1.f), mxc, Sxx * iN);
+  const F2 C01 = r2 * fma2(mxc * bc(-1.f), myc, Sxy * iN);
+  const F2 C11 = r2 * fma2(myc * bc(-1.f), myc, Syy * iN);
+  const F2 C02 = r * fma2(mxc * bc(-1.f), mh, SXH * iN);
+  const F2 C12 = r * fma2(myc * bc(-1.f), mh, SYH * iN);
+  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * iN);
+  // mean footprint height: tile plane at the footprint centroid + mean h^
+  const F2 zz = fma2(bc(gx), mxc, fma2(bc(gy), myc, zref + mh));
+  return solve2<true>(C00, C01, C11, C02, C12, C22, mxc * r, myc * r, zz, okl, okh, gx / p.r, gy / p.r, csk, p);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -381,12 +285,12 @@ struct Geom {
   static constexpr size_t pv_off = px_off + (size_t)HY * PW * 4;            // float2 {PV, PVX}
   static constexpr size_t pvxx_off = pv_off + (size_t)HY * PW * 8;          // float  PVXX
   static constexpr size_t misc_off = (pvxx_off + (size_t)HY * PW * 4 + 15) / 16 * 16;
-  static constexpr size_t runs_off = misc_off + 128;  // int4 byte offsets per (bin, stencil row)
+  static constexpr size_t runs_off = misc_off + 512;  // int4 byte offsets per (bin, stencil row)
   static size_t bytes(int k_chunk) { return runs_off + (size_t)k_chunk * NR * 16; }
 };
 
 template <int R_T>
-__global__ void __launch_bounds__(NTHREADS, 2)
+__global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
   constexpr int HX = G::HX, HY = G::HY, PW = G::PW, NR = G::NR, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
@@ -397,7 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   float2* pv = reinterpret_cast<float2*>(smem + G::pv_off);
   float* pvxx = reinterpret_cast<float*>(smem + G::pvxx_off);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
-  float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8]
+  float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -477,8 +381,67 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   const bool fast = allvf > 0.5f && !p.force_general;
   const float href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
 
-  // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
+  // ---- 2b. tile plane: least squares over the valid halo cells (fixed reduction order) ----------
+  // The prefix sums below hold h^ = h - href - (c + gx x' + gy y'), so their magnitudes are the
+  // terrain's deviation from the tile plane; the covariance is mapped back exactly in the epilogue
+  // (Cov(x, h) = Cov(x, h^) + G Cov(x, x), G = g / r).  Any plane is correct; this one is accurate.
   constexpr float XC = (float)(R_T + TX / 2);  // x' = col - XC; the state at lane l has x' = l - TX/2
+  constexpr float YC = (float)(R_T + TY / 2);  // y' = row - YC; tile row t has y' = t - TY/2
+  float* tplane = red + 8 * 9;
+  {
+    float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f, q6 = 0.f, q7 = 0.f, q8 = 0.f;
+    for (int idx = tid; idx < HX * HY; idx += NTHREADS) {
+      const float v = raw[idx];
+      if (!isnan(v)) {
+        const int row = idx / HX;
+        const float xq = (float)(idx - row * HX) - XC, yq = (float)row - YC, hq = v - href;
+        q0 += 1.f; q1 += xq; q2 += yq; q3 += hq;
+        q4 = fmaf(xq, xq, q4); q5 = fmaf(xq, yq, q5); q6 = fmaf(yq, yq, q6);
+        q7 = fmaf(xq, hq, q7); q8 = fmaf(yq, hq, q8);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      q0 += __shfl_xor_sync(0xffffffffu, q0, o); q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+      q2 += __shfl_xor_sync(0xffffffffu, q2, o); q3 += __shfl_xor_sync(0xffffffffu, q3, o);
+      q4 += __shfl_xor_sync(0xffffffffu, q4, o); q5 += __shfl_xor_sync(0xffffffffu, q5, o);
+      q6 += __shfl_xor_sync(0xffffffffu, q6, o); q7 += __shfl_xor_sync(0xffffffffu, q7, o);
+      q8 += __shfl_xor_sync(0xffffffffu, q8, o);
+    }
+    __syncthreads();  // red[] (min/max) consumed by every thread above
+    if (lane == 0) {
+      red[0 * 8 + warp] = q0; red[1 * 8 + warp] = q1; red[2 * 8 + warp] = q2; red[3 * 8 + warp] = q3;
+      red[4 * 8 + warp] = q4; red[5 * 8 + warp] = q5; red[6 * 8 + warp] = q6; red[7 * 8 + warp] = q7;
+      red[8 * 8 + warp] = q8;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      float t[9];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        t[i] = red[i * 8];
+        for (int w = 1; w < NWARPS; ++w) t[i] += red[i * 8 + w];
+      }
+      float c = 0.f, gx = 0.f, gy = 0.f;
+      if (t[0] >= 3.f) {
+        const float in = 1.f / t[0];
+        const float mxq = t[1] * in, myq = t[2] * in, mhq = t[3] * in;
+        const float cxx = t[4] * in - mxq * mxq, cxy = t[5] * in - mxq * myq, cyy = t[6] * in - myq * myq;
+        const float cxh = t[7] * in - mxq * mhq, cyh = t[8] * in - myq * mhq;
+        const float det = cxx * cyy - cxy * cxy;
+        if (det > 1e-6f * cxx * cyy && det > 0.f) {
+          gx = (cxh * cyy - cyh * cxy) / det;
+          gy = (cyh * cxx - cxh * cxy) / det;
+        }
+        c = mhq - gx * mxq - gy * myq;
+      }
+      tplane[0] = c; tplane[1] = gx; tplane[2] = gy;
+    }
+    __syncthreads();
+  }
+  const float pc = tplane[0], pgx = tplane[1], pgy = tplane[2];
+
+  // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
     float e[CPL], e2[CPL], ex[CPL], vv[CPL], vx[CPL], vxx[CPL];
     float s0 = 0.f, s2 = 0.f, sx = 0.f, sv = 0.f, svx = 0.f, svxx = 0.f;
@@ -487,8 +450,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       const int col = lane * CPL + c;
       float hv = (col < HX) ? raw[row * HX + col] : __int_as_float(0x7fc00000);
       const bool ok = !isnan(hv);
-      const float hh = ok ? hv - href : 0.f;
       const float xp = (float)col - XC;
+      const float hh = ok ? (hv - href) - fmaf(pgx, xp, fmaf(pgy, (float)row - YC, pc)) : 0.f;
       s0 += hh; s2 = fmaf(hh, hh, s2); sx = fmaf(xp, hh, sx);
       e[c] = s0; e2[c] = s2; ex[c] = sx;
       if (!fast) {
@@ -532,19 +495,11 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   int pxs = 0;
   if (col_in) { pxs = p.pxM + (int)li; if (pxs >= p.nx) pxs -= p.nx; }
   const bool col_any = __any_sync(0xffffffffu, col_in);
-  int off[RPW], pys[RPW];
-  bool in[RPW];
-#pragma unroll
-  for (int s = 0; s < RPW; ++s) {
-    const long long lj = TJ * TY + warp + s * NWARPS - p.J_M;
-    const bool row_in = lj >= 0 && lj < p.ny;
-    in[s] = col_in && row_in;
-    int py = 0;
-    if (row_in) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
-    pys[s] = row_in ? py : -1;
-    off[s] = py * p.nx + pxs;
-  }
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
+  const float Gx = pgx / p.r, Gy = pgy / p.r;
+  // tile-plane height at state s: zref0 + s * zstep (absolute, metres)
+  const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)warp - (float)(TY / 2), pc));
+  const float zstep = pgy * (float)NWARPS;
   // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, column lane)
   const char* b8 = reinterpret_cast<const char*>(p02) + (size_t)(warp * PW + lane) * 8;
   const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(warp * PW + lane) * 4;
@@ -552,21 +507,43 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(warp * PW + lane) * 4;
   constexpr int RS8 = NWARPS * PW * 8, RS4 = NWARPS * PW * 4;  // state s -> s * NWARPS halo rows lower
 
+  auto state_py = [&](int srow) {  // physical row of tile row srow, -1 outside the window
+    const long long lj = TJ * TY + srow - p.J_M;
+    int py = -1;
+    if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
+    return py;
+  };
+
   for (int k = kb; k < ke; ++k) {
     const int4* rk = runs_s + (k - kb) * NR;
     const int nr = __ldg(p.nrows + k);
-    const float4 g = __ldg(p.geo + k);
     const float2 csk = __ldg(p.cs + k);
-    float2 S02[RPW];
-    float SXH[RPW], SYH[RPW];
-    float N[RPW], Sx[RPW], Sy[RPW], Sxx[RPW], Sxy[RPW], Syy[RPW];
-#pragma unroll
-    for (int s = 0; s < RPW; ++s) {
-      S02[s] = make_float2(0.f, 0.f);
-      SXH[s] = SYH[s] = 0.f;
-      N[s] = g.x; Sx[s] = 0.f; Sy[s] = 0.f; Sxx[s] = g.y; Sxy[s] = g.z; Syy[s] = g.w;
-    }
+    float4* outk = p.out + (size_t)k * plane;
+    float4* outk2 = p.out + (size_t)(k + p.H) * plane;
+    uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words;
+    uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words;
+    auto store = [&](int py, float risk, float pitch, float roll, float z, unsigned trav) {
+      const bool row_in = py >= 0;
+      const bool in = col_in && row_in;
+      if (in) {  // write-once stream: evict-first stores
+        const int off = py * p.nx + pxs;
+        __stcs(outk + off, make_float4(risk, pitch, roll, z));
+        if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
+      }
+      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
+      const unsigned tmask = __ballot_sync(0xffffffffu, in && trav);
+      if (lane == 0 && col_any && row_in) {
+        const int toff = py * p.trav_words + gword;
+        travk[toff] = tmask;
+        if (p.paired) travk2[toff] = tmask;
+      }
+    };
     if (fast) {
+      // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant
+      float2 S02[RPW];
+      float SXH[RPW], SYH[RPW];
+#pragma unroll
+      for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
 #pragma unroll 2
       for (int d = 0; d < nr; ++d) {
         const int4 o = rk[d];
@@ -587,70 +564,60 @@ __global__ void __launch_bounds__(NTHREADS, 2)
           SYH[s] = fmaf(dj, dd.x, SYH[s]);
         }
       }
-    } else {
-#pragma unroll
-      for (int s = 0; s < RPW; ++s) { N[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f; }
-#pragma unroll 1
-      for (int d = 0; d < nr; ++d) {
-        const int4 o = rk[d];
-        const float dj = __int_as_float(o.w);
-        const int ob4 = o.z + ((o.y - o.x) >> 1);
-#pragma unroll
-        for (int s = 0; s < RPW; ++s) {
-          const float2 A = *reinterpret_cast<const float2*>(b8 + o.x + s * RS8);
-          const float2 B = *reinterpret_cast<const float2*>(b8 + o.y + s * RS8);
-          const float ax = *reinterpret_cast<const float*>(b4 + o.z + s * RS4);
-          const float bxv = *reinterpret_cast<const float*>(b4 + ob4 + s * RS4);
-          const float2 VA = *reinterpret_cast<const float2*>(bv8 + o.x + s * RS8);
-          const float2 VB = *reinterpret_cast<const float2*>(bv8 + o.y + s * RS8);
-          const float wa = *reinterpret_cast<const float*>(bv4 + o.z + s * RS4);
-          const float wb = *reinterpret_cast<const float*>(bv4 + ob4 + s * RS4);
-          const float2 dd = sub2(B, A);
-          const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
-          const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
-          S02[s] = add2(S02[s], dd);
-          SXH[s] += fmaf(-xs, dd.x, bxv - ax);
-          SYH[s] = fmaf(dj, dd.x, SYH[s]);
-          N[s] += cnt;
-          Sx[s] += sdi;
-          Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
-          Sy[s] = fmaf(dj, cnt, Sy[s]);
-          Syy[s] = fmaf(dj * dj, cnt, Syy[s]);
-          Sxy[s] = fmaf(dj, sdi, Sxy[s]);
-        }
-      }
-    }
-    float4* outk = p.out + (size_t)k * plane;
-    float4* outk2 = p.out + (size_t)(k + p.H) * plane;
-    uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words + gword;
-    uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words + gword;
-    auto store = [&](int s, float risk, float pitch, float roll, float z, unsigned trav) {
-      if (in[s]) {
-        outk[off[s]] = make_float4(risk, pitch, roll, z);
-        if (p.paired) outk2[off[s]] = make_float4(risk, -pitch, -roll, z);
-      }
-      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-      const unsigned tmask = __ballot_sync(0xffffffffu, in[s] && trav);
-      if (lane == 0 && col_any && pys[s] >= 0) {
-        travk[(size_t)pys[s] * p.trav_words] = tmask;
-        if (p.paired) travk2[(size_t)pys[s] * p.trav_words] = tmask;
-      }
-    };
-    if (fast) {
       const float4 gc = __ldg(p.geoc + 2 * k), gd = __ldg(p.geoc + 2 * k + 1);
 #pragma unroll
       for (int s = 0; s < RPW; s += 2) {
         const StateOut2 o = epilogue2(pk(S02[s].x, S02[s + 1].x), pk(S02[s].y, S02[s + 1].y), pk(SXH[s], SXH[s + 1]),
-                                      pk(SYH[s], SYH[s + 1]), href, gc, gd, csk, p);
-        store(s, lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
-        store(s + 1, hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+                                      pk(SYH[s], SYH[s + 1]),
+                                      pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gx, Gy,
+                                      gc, gd, csk, p);
+        store(state_py(warp + s * NWARPS), lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
+        store(state_py(warp + (s + 1) * NWARPS), hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
       }
     } else {
+      // ---- border / unknown tile: also the validity moments (N, sum di, sum di^2, ...), two states at a time
+#pragma unroll 1
+      for (int sp = 0; sp < RPW; sp += 2) {
+        float2 S02[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float SXH[2] = {0.f, 0.f}, SYH[2] = {0.f, 0.f}, N[2] = {0.f, 0.f}, Sx[2] = {0.f, 0.f}, Sy[2] = {0.f, 0.f};
+        float Sxx[2] = {0.f, 0.f}, Sxy[2] = {0.f, 0.f}, Syy[2] = {0.f, 0.f};
+        const int so8 = sp * RS8, so4 = sp * RS4;
+#pragma unroll 1
+        for (int d = 0; d < nr; ++d) {
+          const int4 o = rk[d];
+          const float dj = __int_as_float(o.w);
+          const int ob4 = o.z + ((o.y - o.x) >> 1);
 #pragma unroll
-      for (int s = 0; s < RPW; ++s) {
-        const StateOut o = epilogue(N[s], Sx[s], Sy[s], Sxx[s], Sxy[s], Syy[s], S02[s].x, S02[s].y, SXH[s], SYH[s],
-                                    href, csk, p, true);
-        store(s, o.risk, o.pitch, o.roll, o.z, (unsigned)o.trav);
+          for (int s = 0; s < 2; ++s) {
+            const float2 A = *reinterpret_cast<const float2*>(b8 + so8 + o.x + s * RS8);
+            const float2 B = *reinterpret_cast<const float2*>(b8 + so8 + o.y + s * RS8);
+            const float ax = *reinterpret_cast<const float*>(b4 + so4 + o.z + s * RS4);
+            const float bxv = *reinterpret_cast<const float*>(b4 + so4 + ob4 + s * RS4);
+            const float2 VA = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + s * RS8);
+            const float2 VB = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + s * RS8);
+            const float wa = *reinterpret_cast<const float*>(bv4 + so4 + o.z + s * RS4);
+            const float wb = *reinterpret_cast<const float*>(bv4 + so4 + ob4 + s * RS4);
+            const float2 dd = sub2(B, A);
+            const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
+            const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
+            S02[s] = add2(S02[s], dd);
+            SXH[s] += fmaf(-xs, dd.x, bxv - ax);
+            SYH[s] = fmaf(dj, dd.x, SYH[s]);
+            N[s] += cnt;
+            Sx[s] += sdi;
+            Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
+            Sy[s] = fmaf(dj, cnt, Sy[s]);
+            Syy[s] = fmaf(dj * dj, cnt, Syy[s]);
+            Sxy[s] = fmaf(dj, sdi, Sxy[s]);
+          }
+        }
+        const StateOut2 o = epilogue2_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), pk(Sxx[0], Sxx[1]),
+                                              pk(Sxy[0], Sxy[1]), pk(Syy[0], Syy[1]), pk(S02[0].x, S02[1].x),
+                                              pk(S02[0].y, S02[1].y), pk(SXH[0], SXH[1]), pk(SYH[0], SYH[1]),
+                                              pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)),
+                                              pgx, pgy, csk, p);
+        store(state_py(warp + sp * NWARPS), lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
+        store(state_py(warp + (sp + 1) * NWARPS), hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
       }
     }
   }
