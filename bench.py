@@ -128,6 +128,22 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def max_over_ranks(vals, world, device=None):
+    """Element-wise max over ranks (NCCL on the GPU path, gloo in the CPU tests); identity at N = 1."""
+    if world <= 1:
+        return list(vals)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(vals), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def rank_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -200,9 +216,7 @@ def main():
 
     from paper_2503_02412_b200 import se2map as S
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = rank_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -280,10 +294,7 @@ def main():
         kern_ms = [a.elapsed_time(b) for a, b in evk]
     tot_s = sum(step_ms) / 1e3
     kern_s = sum(kern_ms) / 1e3
-    if world > 1:
-        tt_ = torch.tensor([tot_s, kern_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-        tot_s, kern_s = tt_.tolist()
+    tot_s, kern_s = max_over_ranks([tot_s, kern_s], world, dev)
     value = n_states * K / tot_s
 
     # ---- e2e: public API with host buffers (H2D of the step's map from pinned memory, D2H of the
@@ -312,10 +323,7 @@ def main():
             e1.record(stream)
             stream.synchronize()
             e2e_s = e0.elapsed_time(e1) / 1e3
-        if world > 1:
-            tt_ = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
-            e2e_s = tt_.item()
+        e2e_s = max_over_ranks([e2e_s], world, dev)[0]
         e2e = {"value": n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
                "d2h_bytes_per_step": n_states * 4, "ms_per_step": e2e_s / ke * 1e3, "steps": ke,
                "note": "H2D of the full window from pinned host memory + assess FULL + D2H of the risk map "

@@ -78,6 +78,12 @@ void se2m_default_params(se2m_params* p);
  * *out is set only on SE2M_OK. */
 se2m_status se2m_init(const se2m_params* p, se2m_map** out);
 
+/* Host-only (no device is touched): the share of the states the rank described by p computes.
+ * Representative yaw bins [k_lo, k_hi) of n_rep (bin k + n_rep shares bin k's footprint when n_yaw is
+ * even); world tile rows TJ (of tile_y cells) with TJ mod row_mod == row_rank.  Any pointer may be NULL. */
+se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int32_t* k_lo, int32_t* k_hi,
+                            int32_t* tile_y, int32_t* row_mod, int32_t* row_rank);
+
 /* Free everything (synchronises the stream).  NULL-safe. */
 void se2m_destroy(se2m_map* m);
 

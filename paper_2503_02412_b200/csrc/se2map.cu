@@ -229,6 +229,30 @@ static se2m_status validate(const se2m_params* p) {
   return SE2M_OK;
 }
 
+extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int32_t* k_lo, int32_t* k_hi,
+                                       int32_t* tile_y, int32_t* row_mod, int32_t* row_rank) {
+  se2m_status st = validate(p);
+  if (st != SE2M_OK) return st;
+  se2m_map m;  // host-only: no device memory, no CUDA calls
+  m.prm = *p;
+  m.paired = (p->n_yaw % 2 == 0) ? 1 : 0;
+  m.H = m.paired ? p->n_yaw / 2 : p->n_yaw;
+  std::vector<int4> runs;
+  std::vector<int> nrows;
+  std::vector<float4> geo, geoc;
+  std::vector<float2> cs;
+  if (!build_stencils(&m, runs, nrows, geo, geoc, cs)) return fail(nullptr, SE2M_ERR_UNSUPPORTED, "stencil");
+  const bool yaw = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
+  const bool rows = p->shard_mode == SE2M_SHARD_ROWS && p->world_size > 1;
+  if (n_rep) *n_rep = m.H;
+  if (k_lo) *k_lo = yaw ? (int32_t)((long long)m.H * p->rank / p->world_size) : 0;
+  if (k_hi) *k_hi = yaw ? (int32_t)((long long)m.H * (p->rank + 1) / p->world_size) : m.H;
+  if (tile_y) *tile_y = tile_rows(m.R_T);
+  if (row_mod) *row_mod = rows ? p->world_size : 1;
+  if (row_rank) *row_rank = rows ? p->rank : 0;
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   if (!out) return fail(nullptr, SE2M_ERR_INVALID_ARG, "out is NULL");
   se2m_status st = validate(p);

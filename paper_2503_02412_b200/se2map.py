@@ -28,7 +28,7 @@ SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
 
 EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elevation", "se2m_shift_window",
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
-           "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info"]
+           "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan"]
 
 
 class Params(ctypes.Structure):
@@ -58,12 +58,14 @@ _lib.se2m_get_origin.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)
 _lib.se2m_stencil_info.argtypes = [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_synchronize.argtypes = [_vp]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
+_lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
 _lib.se2m_last_error.argtypes = [_vp]
 _lib.se2m_last_error.restype = ctypes.c_char_p
 for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
-              "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info"):
+              "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info",
+              "se2m_shard_plan"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -104,6 +106,16 @@ def _ptr_nocopy(a):
     if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
         return a.data_ptr(), (SE2M_MEM_DEVICE if a.is_cuda else SE2M_MEM_HOST), a
     return a.ctypes.data, SE2M_MEM_HOST, a
+
+
+def shard_plan(params: Params) -> dict:
+    """Host-only share of this rank (no GPU needed): representative bins and tile-row ownership."""
+    v = [_i32() for _ in range(6)]
+    st = _lib.se2m_shard_plan(ctypes.byref(params), *[ctypes.byref(x) for x in v])
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    keys = ("n_rep", "k_lo", "k_hi", "tile_y", "row_mod", "row_rank")
+    return {k: x.value for k, x in zip(keys, v)}
 
 
 def init(params: Params):

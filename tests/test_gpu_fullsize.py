@@ -1,0 +1,56 @@
+"""Parity at BASELINE.json's full sizes (high-res 800x800x72 @ 0.05 m, large 2000x2000x72 @ 0.1 m), in
+the launch configuration bench.py times (one FULL assess of the whole window), on sampled states the
+oracle computes one by one: uniform random states plus a band along the window edges (clipped
+footprints) and every yaw bin of a few fixed cells.  Outputs are read through se2m_query, so the
+world -> (cell, bin) indexing of the C ABI is exercised at full size too.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from synth.terrain import CONFIGS, world_heights
+from tests.gpu_common import make_map, oracle_params
+from tests.parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _samples(nx, ny, n_yaw, R, rng, n_uniform=60000, n_edge=20000):
+    u = np.stack([rng.integers(0, nx, n_uniform), rng.integers(0, ny, n_uniform),
+                  rng.integers(0, n_yaw, n_uniform)], axis=1)
+    band = R + 2
+    side = rng.integers(0, 4, n_edge)
+    a = rng.integers(0, band, n_edge)
+    i = np.where(side == 0, a, np.where(side == 1, nx - 1 - a, rng.integers(0, nx, n_edge)))
+    j = np.where(side == 2, a, np.where(side == 3, ny - 1 - a, rng.integers(0, ny, n_edge)))
+    e = np.stack([i, j, rng.integers(0, n_yaw, n_edge)], axis=1)
+    cells = [(0, 0), (nx - 1, ny - 1), (nx // 2, ny // 2), (nx // 3, 2 * ny // 3)]
+    f = np.array([(ci, cj, k) for ci, cj in cells for k in range(n_yaw)])
+    return np.concatenate([u, e, f]).astype(np.int32)
+
+
+@pytest.mark.parametrize("name", ["highres", "large"])
+def test_fullsize_sampled_parity(name):
+    cfg = CONFIGS[name]
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    m = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    I_M, J_M = m.origin()
+    assert (I_M, J_M) == oracle.window_origin(*cfg["robot"], r, nx, ny)
+    h = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+    m.update_elevation(h)
+    m.assess_se2(0)
+    R = m.stencil_info(0)[1]
+    ijk = _samples(nx, ny, n_yaw, R, np.random.default_rng(17))
+    # query at cell centres and exact bin angles (reading R3/R6)
+    x = (I_M + ijk[:, 0] + 0.5) * r
+    y = (J_M + ijk[:, 1] + 0.5) * r
+    th = -math.pi + 2 * math.pi * ijk[:, 2] / n_yaw
+    q = m.query(np.stack([x, y, th], axis=1))
+    assert q["status"] == 0
+    orc = oracle.assess_states(oracle_params(nx, ny, r, n_yaw), h, ijk)
+    rep = compare({k: q[k] for k in ("risk", "pitch", "roll", "z", "trav")}, orc)
+    print(name, rep)
+    assert rep["ok"], rep
+    assert rep["normal"] > 0.95 * rep["n"]

@@ -1,0 +1,75 @@
+"""CPU, world_size 2 with gloo: the host side of the multi-GPU path (no GPU needed).
+
+* se2m_shard_plan (host-only C ABI call): the ranks' shares partition the representative yaw bins
+  (SE2M_SHARD_YAW) and the world tile rows (SE2M_SHARD_ROWS) exactly — disjoint and covering;
+* bench.max_over_ranks: the max-over-ranks timing reduction bench.py uses, over gloo.
+"""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2503_02412_b200 import se2map as S
+        import bench
+        out = {}
+        for name, kw in (("large", dict(nx=2000, ny=2000, n_yaw=72, resolution=0.1)),
+                         ("highres", dict(nx=800, ny=800, n_yaw=72, resolution=0.05)),
+                         ("odd", dict(nx=37, ny=23, n_yaw=5, resolution=0.1))):
+            for mode in (S.SE2M_SHARD_YAW, S.SE2M_SHARD_ROWS):
+                p = S.default_params(shard_mode=mode, rank=rank, world_size=world, **kw)
+                out[(name, mode)] = S.shard_plan(p)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, out)
+        assert bench.rank_env()[:2] == (world, rank)
+        t = bench.max_over_ranks([1.0 + rank, 10.0 - rank], world)
+        q.put((rank, gathered, t))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_shard_plan_partitions_and_max_reduce(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    for rank, gathered, t in res:
+        assert t == [float(world), 10.0]                     # element-wise max over ranks
+        plans = gathered
+        for key in plans[0]:
+            name, mode = key
+            ps = [plans[r][key] for r in range(world)]
+            n_rep = ps[0]["n_rep"]
+            if mode == 1:                                     # yaw: contiguous, disjoint, covering
+                owned = sorted(k for pl in ps for k in range(pl["k_lo"], pl["k_hi"]))
+                assert owned == list(range(n_rep)), (key, ps)
+                assert all(pl["row_mod"] == 1 for pl in ps)
+            else:                                             # rows: TJ mod G == rank, all bins
+                assert sorted(pl["row_rank"] for pl in ps) == list(range(world))
+                assert all(pl["row_mod"] == world and (pl["k_lo"], pl["k_hi"]) == (0, n_rep) for pl in ps)
+                for TJ in range(-7, 40):
+                    owners = [r for r, pl in enumerate(ps) if TJ % pl["row_mod"] == pl["row_rank"]]
+                    assert len(owners) == 1
