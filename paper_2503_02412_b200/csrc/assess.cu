@@ -285,8 +285,8 @@ struct Geom {
   static constexpr size_t pv_off = px_off + (size_t)HY * PW * 4;            // float2 {PV, PVX}
   static constexpr size_t pvxx_off = pv_off + (size_t)HY * PW * 8;          // float  PVXX
   static constexpr size_t misc_off = (pvxx_off + (size_t)HY * PW * 4 + 15) / 16 * 16;
-  static constexpr size_t runs_off = misc_off + 512;  // int4 byte offsets per (bin, stencil row)
-  static size_t bytes(int k_chunk) { return runs_off + (size_t)k_chunk * NR * 16; }
+  static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
+  static size_t bytes(int tab_cap) { return runs_off + (size_t)tab_cap * 16; }
 };
 
 template <int R_T>
@@ -347,13 +347,6 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
       }
       raw[idx] = v;
     }
-  }
-  // non-empty stencil rows of this CTA's bins (compacted on the host) as byte offsets into the prefix
-  // arrays: (8*ea, 8*eb, 4*ea, dj) with ea = halo index of (row d, column R_T + a), eb = (d, R_T + b + 1)
-  for (int idx = tid; idx < (ke - kb) * NR; idx += NTHREADS) {
-    const int4 ab = p.runs[(size_t)kb * NR + idx];  // (a, b, d, -)
-    const int ea = ab.z * PW + R_T + ab.x, eb = ab.z * PW + R_T + ab.y + 1;
-    runs_s[idx] = make_int4(ea * 8, eb * 8, ea * 4, __float_as_int((float)(ab.z - R_T)));
   }
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
@@ -441,6 +434,16 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
   }
   const float pc = tplane[0], pgx = tplane[1], pgy = tplane[2];
 
+  // run entries of this CTA's bins as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj)
+  // (interior tiles: the yaw chain table; border tiles: full rows)
+  const int4* tab = fast ? p.chain : p.full;
+  const int* tab_off = fast ? p.chain_off : p.full_off;
+  const int tab_base = __ldg(tab_off + kb);
+  for (int idx = tid; idx < __ldg(tab_off + ke) - tab_base; idx += NTHREADS) {
+    const int4 e = __ldg(tab + tab_base + idx);
+    runs_s[idx] = make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
+  }
+
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
     float e[CPL], e2[CPL], ex[CPL], vv[CPL], vx[CPL], vxx[CPL];
@@ -514,9 +517,12 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
     return py;
   };
 
+  float2 S02[RPW];            // interior tiles: moments carried along the yaw chain
+  float SXH[RPW], SYH[RPW];
   for (int k = kb; k < ke; ++k) {
-    const int4* rk = runs_s + (k - kb) * NR;
-    const int nr = __ldg(p.nrows + k);
+    const int e0 = __ldg(tab_off + k);
+    const int4* rk = runs_s + (e0 - tab_base);
+    const int nr = __ldg(tab_off + k + 1) - e0;
     const float2 csk = __ldg(p.cs + k);
     float4* outk = p.out + (size_t)k * plane;
     float4* outk2 = p.out + (size_t)(k + p.H) * plane;
@@ -539,11 +545,12 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
       }
     };
     if (fast) {
-      // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant
-      float2 S02[RPW];
-      float SXH[RPW], SYH[RPW];
+      // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.
+      // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
+      if (k == kb || k % p.period == 0) {
 #pragma unroll
-      for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
+        for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
+      }
 #pragma unroll 2
       for (int d = 0; d < nr; ++d) {
         const int4 o = rk[d];
@@ -626,7 +633,7 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
 template <int R_T>
 static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {
   using G = Geom<R_T>;
-  const size_t smem = G::bytes(p.k_chunk);
+  const size_t smem = G::bytes(p.tab_cap);
   static int configured_bytes = 0;
   if ((int)smem > configured_bytes) {
     cudaError_t e = cudaFuncSetAttribute(assess_kernel<R_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

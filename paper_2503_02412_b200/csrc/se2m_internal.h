@@ -33,8 +33,16 @@ struct AssessParams {
   // yaw: rep bins k in [0, H); bin k + H (if paired) is the same footprint, x_yaw negated
   int n_yaw, H, paired;
   int R;                 // true footprint radius (cells); kernel template R_T >= R
-  const int4* runs;      // [H][2*R_T+1] non-empty stencil rows, compacted: (a, b, d = dj + R_T, 0); di in [a, b]
-  const int* nrows;      // [H] number of non-empty rows of bin k
+  // Stencil tables as "run entries" (e_minus, e_plus, d, 0): a run sum is P[e_plus] - P[e_minus] of halo
+  // row d (= dj + R_T), element offsets relative to the state's own prefix column.  full: the non-empty
+  // rows of bin k; chain: the full rows when k % period == 0, else the endpoint corrections from bin
+  // k-1 to bin k (moments carried along the yaw chain).  Entries of bin k: [off[k], off[k+1]).
+  const int4* full;
+  const int* full_off;   // [H+1]
+  const int4* chain;
+  const int* chain_off;  // [H+1]
+  int period;            // yaw-chain restart period (1 = no chain); chunks start at multiples of it
+  int tab_cap;           // max entries of one CTA's chunk (shared-memory table size)
   const float4* geo;     // [H] full-stencil (N, Sxx, Sxy, Syy) in cell units (Sx = Sy = 0)
   const float4* geoc;    // [H][2] full-stencil covariance: (C00, C01, C11, 1/N), (r/N, C00+C11, C01^2, 0), metres
   const float2* cs;      // [H] (cos, sin) of theta_k, k < H (reading R3)

@@ -47,8 +47,12 @@ struct se2m_map {
   float* d_h = nullptr;
   float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
-  int4* d_runs = nullptr;
-  int* d_nrows = nullptr;
+  int4* d_full = nullptr;   // run-entry tables (see AssessParams)
+  int* d_full_off = nullptr;
+  int4* d_chain = nullptr;
+  int* d_chain_off = nullptr;
+  std::vector<int> full_off, chain_off;
+  int period = 1;
   float4* d_geo = nullptr;
   float4* d_geoc = nullptr;
   float2* d_cs = nullptr;
@@ -149,6 +153,52 @@ static bool build_stencils(se2m_map* m, std::vector<int4>& runs, std::vector<int
   return true;
 }
 
+// Run-entry tables (AssessParams::full / chain) from the per-bin row runs: element offsets into a
+// halo prefix row of pitch PW = TX + 2 R_T + 1, relative to the state's own column.
+static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows,
+                         std::vector<int4>& full, std::vector<int4>& chain) {
+  const int RT = m->R_T, NR = 2 * RT + 1, PW = TX + 2 * RT + 1;
+  auto row_runs = [&](int k) {  // d -> (a, b) or (0, -1)
+    std::vector<int2> r(NR, make_int2(0, -1));
+    for (int i = 0; i < nrows[k]; ++i) {
+      const int4 q = runs[(size_t)k * NR + i];
+      r[q.z] = make_int2(q.x, q.y);
+    }
+    return r;
+  };
+  auto ea = [&](int d, int a) { return d * PW + RT + a; };
+  auto eb = [&](int d, int b) { return d * PW + RT + b + 1; };
+  m->full_off.assign(m->H + 1, 0);
+  m->chain_off.assign(m->H + 1, 0);
+  full.clear();
+  chain.clear();
+  std::vector<int2> prev;
+  for (int k = 0; k < m->H; ++k) {
+    const std::vector<int2> cur = row_runs(k);
+    m->full_off[k] = (int)full.size();
+    for (int d = 0; d < NR; ++d)
+      if (cur[d].y >= cur[d].x) full.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
+    m->chain_off[k] = (int)chain.size();
+    if (k % m->period == 0) {
+      for (int d = 0; d < NR; ++d)
+        if (cur[d].y >= cur[d].x) chain.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
+    } else {
+      // run(k) - run(k-1) = (P[eb2] - P[eb1]) + (P[ea1] - P[ea2]) per row (empty run: P[x] - P[x] = 0)
+      for (int d = 0; d < NR; ++d) {
+        const bool e1 = prev[d].y < prev[d].x, e2 = cur[d].y < cur[d].x;
+        if (e1 && e2) continue;
+        if (e1) { chain.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0)); continue; }
+        if (e2) { chain.push_back(make_int4(eb(d, prev[d].y), ea(d, prev[d].x), d, 0)); continue; }
+        if (cur[d].x != prev[d].x) chain.push_back(make_int4(ea(d, cur[d].x), ea(d, prev[d].x), d, 0));
+        if (cur[d].y != prev[d].y) chain.push_back(make_int4(eb(d, prev[d].y), eb(d, cur[d].y), d, 0));
+      }
+    }
+    prev = cur;
+  }
+  m->full_off[m->H] = (int)full.size();
+  m->chain_off[m->H] = (int)chain.size();
+}
+
 static bool make_tensor_map(se2m_map* m) {
   typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -180,7 +230,9 @@ static AssessParams make_params(const se2m_map* m) {
   p.out = m->d_out; p.trav = m->d_trav;
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
-  p.runs = m->d_runs; p.nrows = m->d_nrows; p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
+  p.full = m->d_full; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off;
+  p.period = m->period;
+  p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
   p.kappa_max = (float)m->prm.kappa_max; p.phi_x_max = (float)m->prm.phi_x_max; p.phi_y_max = (float)m->prm.phi_y_max;
   p.wk = (float)(m->prm.w_r[0] / m->prm.kappa_max);
@@ -245,8 +297,10 @@ extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int
   const bool yaw = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
   const bool rows = p->shard_mode == SE2M_SHARD_ROWS && p->world_size > 1;
   if (n_rep) *n_rep = m.H;
-  if (k_lo) *k_lo = yaw ? (int32_t)((long long)m.H * p->rank / p->world_size) : 0;
-  if (k_hi) *k_hi = yaw ? (int32_t)((long long)m.H * (p->rank + 1) / p->world_size) : m.H;
+  const int period = (m.H >= 18 && (long long)p->nx * p->ny >= 512LL * 512LL) ? 9 : 1;
+  const int nper = (m.H + period - 1) / period;
+  if (k_lo) *k_lo = yaw ? std::min(m.H, period * (int32_t)((long long)nper * p->rank / p->world_size)) : 0;
+  if (k_hi) *k_hi = yaw ? std::min(m.H, period * (int32_t)((long long)nper * (p->rank + 1) / p->world_size)) : m.H;
   if (tile_y) *tile_y = tile_rows(m.R_T);
   if (row_mod) *row_mod = rows ? p->world_size : 1;
   if (row_rank) *row_rank = rows ? p->rank : 0;
@@ -277,10 +331,6 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   m->paired = (n % 2 == 0) ? 1 : 0;
   m->H = m->paired ? n / 2 : n;
   m->k_lo = 0; m->k_hi = m->H;
-  if (p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1) {
-    m->k_lo = (int)((long long)m->H * p->rank / p->world_size);
-    m->k_hi = (int)((long long)m->H * (p->rank + 1) / p->world_size);
-  }
   std::vector<int4> runs;
   std::vector<int> nrows;
   std::vector<float4> geo, geoc;
@@ -289,6 +339,16 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     fail(m, SE2M_ERR_UNSUPPORTED, "footprint stencil could not be built (radius or shape)");
     return bail(SE2M_ERR_UNSUPPORTED);
   }
+  // yaw chain: on maps big enough that every CTA takes all its bins, carry moments along
+  // the bins and restart every 9; small maps split the bins across CTAs instead (period 1)
+  m->period = (m->H >= 18 && (long long)p->nx * p->ny >= 512LL * 512LL) ? 9 : 1;
+  if (p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1) {  // shard whole chain periods
+    const int nper = (m->H + m->period - 1) / m->period;
+    m->k_lo = std::min(m->H, m->period * (int)((long long)nper * p->rank / p->world_size));
+    m->k_hi = std::min(m->H, m->period * (int)((long long)nper * (p->rank + 1) / p->world_size));
+  }
+  std::vector<int4> full, chain;
+  build_tables(m, runs, nrows, full, chain);
   // Eq. 4 (reading R6/R7): window origin = floor(x/r) - nx/2 in IEEE double
   m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
   m->J_M = (long long)floor(p->robot_y / p->resolution) - p->ny / 2;
@@ -300,8 +360,10 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       {(void**)&m->d_h, (size_t)m->ldh * p->ny * 4, "heights"},
       {(void**)&m->d_out, nst * sizeof(float4), "state records"},
       {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
-      {(void**)&m->d_runs, runs.size() * sizeof(int4), "runs"},
-      {(void**)&m->d_nrows, nrows.size() * sizeof(int), "nrows"},
+      {(void**)&m->d_full, std::max<size_t>(1, full.size()) * sizeof(int4), "full table"},
+      {(void**)&m->d_full_off, m->full_off.size() * sizeof(int), "full offsets"},
+      {(void**)&m->d_chain, std::max<size_t>(1, chain.size()) * sizeof(int4), "chain table"},
+      {(void**)&m->d_chain_off, m->chain_off.size() * sizeof(int), "chain offsets"},
       {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
       {(void**)&m->d_geoc, geoc.size() * sizeof(float4), "geoc"},
       {(void**)&m->d_cs, cs.size() * sizeof(float2), "cs"},
@@ -313,8 +375,10 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       return bail(e == cudaErrorMemoryAllocation ? SE2M_ERR_OOM : SE2M_ERR_CUDA);
     }
   }
-  if ((e = cudaMemcpyAsync(m->d_runs, runs.data(), runs.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
-      (e = cudaMemcpyAsync(m->d_nrows, nrows.data(), nrows.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+  if ((e = cudaMemcpyAsync(m->d_full, full.data(), full.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_full_off, m->full_off.data(), m->full_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_chain, chain.data(), chain.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_chain_off, m->chain_off.data(), m->chain_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_geo, geo.data(), geo.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_geoc, geoc.data(), geoc.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, m->stream)) ||
@@ -332,7 +396,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_runs, m->d_nrows, m->d_geo, m->d_geoc,
+  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qidx, m->d_qout};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -475,7 +539,15 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
     const long long want = 4LL * 148;
     chunk = (int)std::max<long long>(1, std::min<long long>(nk, (long long)n_tiles * nk / want));
   }
-  p.k_chunk = std::max(1, chunk);
+  chunk = std::max(1, chunk);
+  if (m->period > 1) chunk = std::min(nk, (chunk + m->period - 1) / m->period * m->period);  // chain-aligned
+  p.k_chunk = chunk;
+  int cap = 1;
+  for (int kb = m->k_lo; kb < m->k_hi; kb += chunk) {
+    const int ke = std::min(kb + chunk, m->k_hi);
+    cap = std::max(cap, std::max(m->full_off[ke] - m->full_off[kb], m->chain_off[ke] - m->chain_off[kb]));
+  }
+  p.tab_cap = cap;
   if (n_tiles > 0 && nk > 0) {
     cudaError_t e = launch_assess(p, m->R_T, n_tiles, &m->tmap, m->stream);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");

@@ -93,8 +93,9 @@ def test_sharded_equals_single(mode, G):
         m.assess_se2(0)
         g = m.download()
         if mode == 1:
-            H = n_yaw // 2
-            lo, hi = H * rank // G, H * (rank + 1) // G
+            from paper_2503_02412_b200 import se2map as S
+            plan = S.shard_plan(m.params)
+            H, lo, hi = plan["n_rep"], plan["k_lo"], plan["k_hi"]
             own = np.zeros(n_yaw, bool)
             own[lo:hi] = True
             own[lo + H:hi + H] = True
