@@ -22,6 +22,10 @@
 
 #include "se2m_internal.h"
 
+#ifndef SE2M_MINB
+#define SE2M_MINB(R_T) 2
+#endif
+
 namespace se2m {
 
 // ------------------------------------------------------------------------------------------
@@ -68,18 +72,8 @@ __device__ __forceinline__ float warp_incl_scan(float v, int lane) {
 }
 
 // Packed FP32x2 (sm_100a FADD2): two lanes of arithmetic per issue slot.
-__device__ __forceinline__ unsigned long long f2_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
-__device__ __forceinline__ float2 bits_f2(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return bits_f2(d);
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return bits_f2(d);
-}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 // MUFU approximations (relative error ~1 ulp); the eigenvector refinement absorbs them.
 __device__ __forceinline__ float frcp(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
 __device__ __forceinline__ float fsqrt(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
@@ -89,25 +83,19 @@ __device__ __forceinline__ float fsqrt(float x) { float r; asm("sqrt.approx.ftz.
 // and selects run per lane.  The footprint geometry is the per-bin constant gc = (C00, C01, C11, 1/N),
 // gd = (r/N, C00 + C11, C01^2, -) (metres, computed in FP64 on the host), so Sx = Sy = 0, mx = my = 0.
 // ------------------------------------------------------------------------------------------
-struct F2 {
-  unsigned long long v;
-};
-__device__ __forceinline__ F2 pk(float a, float b) {
-  F2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ F2 bc(float a) { return pk(a, a); }
-__device__ __forceinline__ float lo(F2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v)); return a; }
-__device__ __forceinline__ float hi(F2 x) { float a, b; asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.v)); return b; }
-__device__ __forceinline__ F2 operator+(F2 a, F2 b) { F2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
-__device__ __forceinline__ F2 operator-(F2 a, F2 b) { F2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
-__device__ __forceinline__ F2 operator*(F2 a, F2 b) { F2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v)); return d; }
-__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) {
-  F2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
-  return d;
-}
+// F2 = (state a, state b) in one 64-bit register pair; the CUDA 12.9 sm_100 builtins __fadd2_rn /
+// __fmul2_rn / __ffma2_rn keep the operations visible to the compiler (negations and constants fold
+// into the FADD2 / FMUL2 / FFMA2 operand modifiers).
+typedef float2 F2;
+__device__ __forceinline__ F2 pk(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ F2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float lo(F2 x) { return x.x; }
+__device__ __forceinline__ float hi(F2 x) { return x.y; }
+__device__ __forceinline__ F2 neg2(F2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ F2 operator-(F2 a, F2 b) { return __fadd2_rn(a, neg2(b)); }
+__device__ __forceinline__ F2 operator*(F2 a, F2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ F2 abs2(F2 x) { return pk(fabsf(lo(x)), fabsf(hi(x))); }
 __device__ __forceinline__ F2 rsqrt2(F2 x) { return pk(rsqrtf(lo(x)), rsqrtf(hi(x))); }
 __device__ __forceinline__ F2 rcp2(F2 x) { return pk(frcp(lo(x)), frcp(hi(x))); }
@@ -176,28 +164,28 @@ __device__ __forceinline__ StateOut2 solve2(F2 C00, F2 C01, F2 C11, F2 Cp02, F2 
   const F2 pp = p2 * ip;
   const F2 d00 = b00 * ip, d11 = b11 * ip, d22 = b22 * ip, e01 = c01 * ip, e02 = c02 * ip, e12 = c12 * ip;
   // det(B) / 2, B = (C' - I/3)/p:  d00 (d11 d22 - e12^2) - e01 (e01 d22 - e12 e02) + e02 (e01 e12 - d11 e02)
-  const F2 m1 = fma2(d11, d22, (e12 * e12) * bc(-1.f));
-  const F2 m2 = fma2(e01, d22, (e12 * e02) * bc(-1.f));
-  const F2 m3 = fma2(e01, e12, (d11 * e02) * bc(-1.f));
-  const F2 hr = fma2(e02, m3, fma2(d00, m1, (e01 * m2) * bc(-1.f))) * bc(0.5f);
+  const F2 m1 = fma2(d11, d22, neg2(e12 * e12));
+  const F2 m2 = fma2(e01, d22, neg2(e12 * e02));
+  const F2 m3 = fma2(e01, e12, neg2(d11 * e02));
+  const F2 hr = fma2(e02, m3, fma2(d00, m1, neg2(e01 * m2))) * bc(0.5f);
   const F2 phi = acos2(hr) * third;
   float sl, cl, sh, ch;
   __sincosf(lo(phi), &sl, &cl);
   __sincosf(hi(phi), &sh, &ch);
-  const F2 lam0 = fma2(pp * bc(-1.f), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), third);
+  const F2 lam0 = fma2(neg2(pp), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), third);
   const F2 m00 = c00 - lam0, m11 = c11 - lam0, m22 = c22 - lam0;
   // rows r0 = (m00, c01, c02), r1 = (c01, m11, c12), r2 = (c02, c12, m22); adj(M) = [r1xr2, r2xr0, r0xr1]
-  const F2 a0 = fma2(c01, c12, (c02 * m11) * bc(-1.f)), a1 = fma2(c02, c01, (m00 * c12) * bc(-1.f)),
-           a2 = fma2(m00, m11, (c01 * c01) * bc(-1.f));                       // r0 x r1
-  const F2 b0 = fma2(c01, m22, (c02 * c12) * bc(-1.f)), b1 = fma2(c02, c02, (m00 * m22) * bc(-1.f)),
-           b2 = fma2(m00, c12, (c01 * c02) * bc(-1.f));                       // r0 x r2 = -(r2 x r0)
-  const F2 g0 = fma2(m11, m22, (c12 * c12) * bc(-1.f)), g1 = fma2(c12, c02, (c01 * m22) * bc(-1.f)),
-           g2 = fma2(c01, c12, (m11 * c02) * bc(-1.f));                       // r1 x r2
+  const F2 a0 = fma2(c01, c12, neg2(c02 * m11)), a1 = fma2(c02, c01, neg2(m00 * c12)),
+           a2 = fma2(m00, m11, neg2(c01 * c01));                       // r0 x r1
+  const F2 b0 = fma2(c01, m22, neg2(c02 * c12)), b1 = fma2(c02, c02, neg2(m00 * m22)),
+           b2 = fma2(m00, c12, neg2(c01 * c02));                       // r0 x r2 = -(r2 x r0)
+  const F2 g0 = fma2(m11, m22, neg2(c12 * c12)), g1 = fma2(c12, c02, neg2(c01 * m22)),
+           g2 = fma2(c01, c12, neg2(m11 * c02));                       // r1 x r2
   // seed v = a = r0 x r1, the adj(M) column along b3 (|a| ~ n_z: well conditioned for the tilts that
   // are assessed, |angle| < 1.3 rad, reading R12); x = adj(M) v
-  const F2 x0 = fma2(a0, g0, fma2(a1 * bc(-1.f), b0, a2 * a0));
-  const F2 x1 = fma2(a0, g1, fma2(a1 * bc(-1.f), b1, a2 * a1));
-  const F2 x2 = fma2(a0, g2, fma2(a1 * bc(-1.f), b2, a2 * a2));
+  const F2 x0 = fma2(a0, g0, fma2(neg2(a1), b0, a2 * a0));
+  const F2 x1 = fma2(a0, g1, fma2(neg2(a1), b1, a2 * a1));
+  const F2 x2 = fma2(a0, g2, fma2(neg2(a1), b2, a2 * a2));
   const F2 inv = copysign2(rsqrt2(fma2(x0, x0, fma2(x1, x1, x2 * x2))), x2);  // z_b in S^2_+ 
   const F2 n0 = x0 * inv, n1 = x1 * inv, n2 = x2 * inv;
   // kappa = lambda_min / trace = Rayleigh quotient of n on C' (reading R1)
@@ -210,7 +198,7 @@ __device__ __forceinline__ StateOut2 solve2(F2 C00, F2 C01, F2 C11, F2 Cp02, F2 
   const F2 u = fma2(n0, bc(csk.x), n1 * bc(csk.y));
   const F2 t = fma2(n0, bc(csk.y), n1 * bc(-csk.x));
   const F2 rs = rsqrt2(fma2(n2, n2, t * t));
-  const F2 pitch = asin2((n2 * u) * (rs * bc(-1.f)));
+  const F2 pitch = asin2((n2 * u) * (neg2(rs)));
   const F2 roll = asin2(t * rs);
   const F2 ax = abs2(pitch), ay = abs2(roll);
   const F2 rk = fma2(bc(p.wk), kap, fma2(bc(p.wx), ax, ay * bc(p.wy)));
@@ -235,7 +223,7 @@ __device__ __forceinline__ StateOut2 solve2(F2 C00, F2 C01, F2 C11, F2 Cp02, F2 
 __device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zref, float Gx, float Gy, float4 gc,
                                                float4 gd, float2 csk, const AssessParams& p) {
   const F2 mh = S0 * bc(gc.w);
-  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * bc(gc.w));
+  const F2 C22 = fma2(neg2(mh), mh, S2 * bc(gc.w));
   const F2 z0 = bc(0.f);
   return solve2<false>(bc(gc.x), bc(gc.y), bc(gc.z), SXH * bc(gd.x), SYH * bc(gd.x), C22, z0, z0, zref + mh, true,
                        true, Gx, Gy, csk, p);
@@ -256,12 +244,12 @@ __device__ __forceinline__ StateOut2 epilogue2_general(F2 N, F2 Sx, F2 Sy, F2 Sx
   const F2 iN = rcp2(sel2(okl, okh, N, bc(3.f)));
   const F2 mxc = Sx * iN, myc = Sy * iN, mh = S0 * iN;
   const F2 r = bc(p.r), r2 = bc(p.r * p.r);
-  const F2 C00 = r2 * fma2(mxc * bc(-1.f), mxc, Sxx * iN);
-  const F2 C01 = r2 * fma2(mxc * bc(-1.f), myc, Sxy * iN);
-  const F2 C11 = r2 * fma2(myc * bc(-1.f), myc, Syy * iN);
-  const F2 C02 = r * fma2(mxc * bc(-1.f), mh, SXH * iN);
-  const F2 C12 = r * fma2(myc * bc(-1.f), mh, SYH * iN);
-  const F2 C22 = fma2(mh * bc(-1.f), mh, S2 * iN);
+  const F2 C00 = r2 * fma2(neg2(mxc), mxc, Sxx * iN);
+  const F2 C01 = r2 * fma2(neg2(mxc), myc, Sxy * iN);
+  const F2 C11 = r2 * fma2(neg2(myc), myc, Syy * iN);
+  const F2 C02 = r * fma2(neg2(mxc), mh, SXH * iN);
+  const F2 C12 = r * fma2(neg2(myc), mh, SYH * iN);
+  const F2 C22 = fma2(neg2(mh), mh, S2 * iN);
   // mean footprint height: tile plane at the footprint centroid + mean h^
   const F2 zz = fma2(bc(gx), mxc, fma2(bc(gy), myc, zref + mh));
   return solve2<true>(C00, C01, C11, C02, C12, C22, mxc * r, myc * r, zz, okl, okh, gx / p.r, gy / p.r, csk, p);
@@ -290,7 +278,7 @@ struct Geom {
 };
 
 template <int R_T>
-__global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
+__global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
   constexpr int HX = G::HX, HY = G::HY, PW = G::PW, NR = G::NR, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
@@ -510,12 +498,17 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
   const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(warp * PW + lane) * 4;
   constexpr int RS8 = NWARPS * PW * 8, RS4 = NWARPS * PW * 4;  // state s -> s * NWARPS halo rows lower
 
-  auto state_py = [&](int srow) {  // physical row of tile row srow, -1 outside the window
-    const long long lj = TJ * TY + srow - p.J_M;
+  // per state s (tile row warp + s NWARPS): record index in a bin plane, traversable-word index (-1: the
+  // state's row is outside the window)
+  int soff[RPW], stoff[RPW];
+#pragma unroll
+  for (int s = 0; s < RPW; ++s) {
+    const long long lj = TJ * TY + warp + s * NWARPS - p.J_M;
     int py = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
-    return py;
-  };
+    soff[s] = (py >= 0 && col_in) ? py * p.nx + pxs : -1;
+    stoff[s] = (py >= 0 && col_any && lane == 0) ? py * p.trav_words + gword : -1;
+  }
 
   float2 S02[RPW];            // interior tiles: moments carried along the yaw chain
   float SXH[RPW], SYH[RPW];
@@ -528,18 +521,14 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
     float4* outk2 = p.out + (size_t)(k + p.H) * plane;
     uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words;
     uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words;
-    auto store = [&](int py, float risk, float pitch, float roll, float z, unsigned trav) {
-      const bool row_in = py >= 0;
-      const bool in = col_in && row_in;
-      if (in) {  // write-once stream: evict-first stores
-        const int off = py * p.nx + pxs;
+    auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
+      if (off >= 0) {  // write-once stream: evict-first stores
         __stcs(outk + off, make_float4(risk, pitch, roll, z));
         if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
       }
       // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-      const unsigned tmask = __ballot_sync(0xffffffffu, in && trav);
-      if (lane == 0 && col_any && row_in) {
-        const int toff = py * p.trav_words + gword;
+      const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
+      if (toff >= 0) {
         travk[toff] = tmask;
         if (p.paired) travk2[toff] = tmask;
       }
@@ -578,8 +567,8 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
                                       pk(SYH[s], SYH[s + 1]),
                                       pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gx, Gy,
                                       gc, gd, csk, p);
-        store(state_py(warp + s * NWARPS), lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
-        store(state_py(warp + (s + 1) * NWARPS), hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+        store(soff[s], stoff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
+        store(soff[s + 1], stoff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
       }
     } else {
       // ---- border / unknown tile: also the validity moments (N, sum di, sum di^2, ...), two states at a time
@@ -623,8 +612,12 @@ __global__ void __launch_bounds__(NTHREADS, (R_T <= 12 ? 3 : 2))
                                               pk(S02[0].y, S02[1].y), pk(SXH[0], SXH[1]), pk(SYH[0], SYH[1]),
                                               pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)),
                                               pgx, pgy, csk, p);
-        store(state_py(warp + sp * NWARPS), lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
-        store(state_py(warp + (sp + 1) * NWARPS), hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+        int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
+#pragma unroll
+        for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
+          if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
+        store(so0, st0, lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
+        store(so1, st1, hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
       }
     }
   }

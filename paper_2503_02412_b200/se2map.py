@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _build
 
-_LIB_PATH = _build.LIB
+_LIB_PATH = os.environ.get("SE2M_LIB") or _build.LIB  # SE2M_LIB: A/B-test an alternative build
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         "libse2map.so is not built (%s); run __graft_entry__.build() — there is no CPU fallback" % _LIB_PATH)
