@@ -367,7 +367,9 @@ def main():
                 "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
                         "bytes_per_state": bytes_state}}
     if prof:
-        roofline["ncu"] = {k: v for k, v in prof.items() if k != "dram_bytes_per_launch"}
+        roofline["ncu"] = {k: v for k, v in prof.items()
+                           if k not in ("dram_bytes_per_launch", "hot_lines", "launch_shares")}
+        roofline["ncu"]["source"] = "profiles/latest_ncu_summary.json (ncu --set full of this kernel)"
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
