@@ -108,3 +108,61 @@ def test_sharded_equals_single(mode, G):
         for f in merged:
             merged[f][mask] = g[f][mask]
     assert _equal(merged, ref)
+
+
+@pytest.mark.parametrize("n_yaw", [72, 36])
+def test_chain_map_incremental_and_sharded(n_yaw):
+    """A map big enough for the yaw chain (period 9): INCREMENTAL after shifts == FULL bit-exact, and
+    yaw / row sharding == single, with the chain restarts aligned to the shards."""
+    from paper_2503_02412_b200 import se2map as S
+    nx, ny, r = 544, 520, 0.1
+    terrain = CONFIGS["large"]["terrain"]
+    robot = (3.37, -2.61)
+    single = make_map(nx, ny, r, n_yaw, robot=robot)
+    full = make_map(nx, ny, r, n_yaw, robot=robot)
+    I_M, J_M = single.origin()
+    h = world_heights(terrain, I_M, J_M, nx, ny, r)
+    for m in (single, full):
+        m.update_elevation(h)
+        m.assess_se2(0)
+    for (x, y) in [(3.61, -2.47), (4.02, -2.55), (3.1, -3.3), (3.1, -3.3), (2.2, -1.05)]:
+        d = single.shift_window(x, y)
+        assert full.shift_window(x, y) == d
+        I_M, J_M = single.origin()
+        for (i0, j0, w, hh) in _exposed_strips(*d, nx, ny):
+            strip = world_heights(terrain, I_M + i0, J_M + j0, w, hh, r)
+            single.update_elevation(strip, i0=i0, j0=j0)
+            full.update_elevation(strip, i0=i0, j0=j0)
+        single.assess_se2(1)
+        full.assess_se2(0)
+        assert _equal(single.download(), full.download())
+    ref = full.download()
+    h = world_heights(terrain, I_M, J_M, nx, ny, r)
+    for mode in (1, 2):
+        for G in (2, 3):
+            merged = {f: np.full_like(v, np.nan if v.dtype != np.uint8 else 0) for f, v in ref.items()}
+            for rank in range(G):
+                m = make_map(nx, ny, r, n_yaw, robot=(2.2, -1.05), shard_mode=mode, rank=rank, world_size=G)
+                m.update_elevation(h)
+                m.assess_se2(0)
+                g = m.download()
+                plan = S.shard_plan(m.params)
+                if mode == 1:
+                    H, lo, hi = plan["n_rep"], plan["k_lo"], plan["k_hi"]
+                    own = np.zeros(n_yaw, bool)
+                    own[lo:hi] = True
+                    own[lo + H:hi + H] = True
+                    mask = np.broadcast_to(own[:, None, None], ref["risk"].shape)
+                else:
+                    J = np.arange(J_M, J_M + ny)
+                    mask = np.broadcast_to(((np.floor_divide(J, plan["tile_y"]) % G) == rank)[None, :, None],
+                                           ref["risk"].shape)
+                for f in merged:
+                    merged[f][mask] = g[f][mask]
+            assert _equal(merged, ref), (mode, G)
+    # and parity with the oracle on a sample
+    rng = np.random.default_rng(4)
+    ijk = np.stack([rng.integers(0, nx, 20000), rng.integers(0, ny, 20000), rng.integers(0, n_yaw, 20000)], 1)
+    orc = oracle.assess_states(oracle_params(nx, ny, r, n_yaw), h, ijk.astype(np.int32))
+    rep = compare({f: ref[f][ijk[:, 2], ijk[:, 1], ijk[:, 0]] for f in ref}, orc)
+    assert rep["ok"], rep
