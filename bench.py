@@ -301,7 +301,9 @@ def main():
     #      risk map to pinned memory: the paper sends the risk map back to the CPU) -----
     e2e = None
     if not args.no_e2e:
-        risk_host = torch.empty((n_yaw, ny, nx), dtype=torch.float32).pin_memory()
+        wpr = (nx + 31) // 32
+        comp = {"risk_q": torch.empty((n_yaw, ny, nx), dtype=torch.int16).pin_memory(),
+                "trav_bits": torch.empty((n_yaw, ny, wpr), dtype=torch.int32).pin_memory()}
         ke = max(2, min(K, 5))
         with torch.cuda.stream(stream):
             for t in range(2):                      # warm the staging buffers
@@ -309,7 +311,7 @@ def main():
                 I_M, J_M = m.origin()
                 m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
                 m.assess_se2(S.SE2M_FULL)
-                m.download(planes=("risk",), out={"risk": risk_host})
+                m.download_compact(out=comp)
             if world > 1:
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -319,15 +321,17 @@ def main():
                 I_M, J_M = m.origin()
                 m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
                 m.assess_se2(S.SE2M_FULL)
-                m.download(planes=("risk",), out={"risk": risk_host})
+                m.download_compact(out=comp)
             e1.record(stream)
             stream.synchronize()
             e2e_s = e0.elapsed_time(e1) / 1e3
         e2e_s = max_over_ranks([e2e_s], world, dev)[0]
         e2e = {"value": n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
-               "d2h_bytes_per_step": n_states * 4, "ms_per_step": e2e_s / ke * 1e3, "steps": ke,
-               "note": "H2D of the full window from pinned host memory + assess FULL + D2H of the risk map "
-                       "(logical order) to pinned host memory, per step"}
+               "d2h_bytes_per_step": n_states * 2 + n_yaw * ny * wpr * 4, "ms_per_step": e2e_s / ke * 1e3,
+               "steps": ke,
+               "note": "per step: H2D of the full window from pinned host memory, assess FULL, and D2H of the "
+                       "risk map (u16, 1.5e-5 resolution) + traversable bits in logical order to pinned host "
+                       "memory (se2m_download_compact; the paper sends the risk map to the CPU, PAPER.md:95)"}
 
     if rank != 0:
         if world > 1:

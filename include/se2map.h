@@ -124,6 +124,13 @@ se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, f
 se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z,
                           uint8_t* trav, int32_t mem);
 
+/* Compact copy of the map for planners (the paper sends the risk map to the CPU):
+ * risk_q[k][j][i] = rint(risk * 65535) (u16, resolution 1.5e-5; unknown / not owned = 65535) and the
+ * traversable bits re-packed in logical order, trav_bits[k][j][w] bit b = column 32 w + b
+ * (ceil(nx/32) words per row, bits past nx zero).  Either pointer may be NULL; mem as in se2m_download.
+ * Synchronises. */
+se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+
 /* Window origin (world cell of logical (0,0)) and the owned representative-yaw range. */
 se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
 

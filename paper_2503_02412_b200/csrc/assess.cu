@@ -728,6 +728,46 @@ cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, flo
   return cudaGetLastError();
 }
 
+// Compact download: risk quantised to u16 (q = rint(risk * 65535), unknown = 65535) and traversable bits
+// re-packed in logical order (word w of logical row j holds logical columns 32w .. 32w+31, bit = column
+// mod 32; bits beyond nx are 0).  Bins outside [k_lo, k_hi) (not owned) read as risk 65535, trav 0.
+__global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, uint16_t* __restrict__ risk_q,
+                                      uint32_t* __restrict__ bits, int wpr) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  const int k = blockIdx.z;
+  int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+  const bool owned = k >= k_lo && k < k_hi;
+  if (risk_q && i < p.nx) {
+    int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
+    const float r = owned ? p.out[((size_t)k * p.ny + py) * p.nx + px].x : 1.f;
+    risk_q[((size_t)k * p.ny + j) * p.nx + i] = (uint16_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 65535.f);
+  }
+  if (bits && i < wpr) {
+    uint32_t w = 0;
+    if (owned) {
+      const long long I0 = p.I_M + 32LL * i;            // world column of logical column 32 i
+      const long long g = I0 >= 0 ? I0 / 32 : -((-I0 + 31) / 32);
+      const int sh = (int)(I0 - g * 32);
+      const uint32_t* row = p.trav + ((size_t)k * p.ny + py) * p.trav_words;
+      const int w0 = (int)(((g % p.trav_words) + p.trav_words) % p.trav_words);
+      const int w1 = w0 + 1 == p.trav_words ? 0 : w0 + 1;
+      w = row[w0] >> sh;
+      if (sh) w |= row[w1] << (32 - sh);
+      const int valid = p.nx - 32 * i;                    // logical columns left in this word
+      if (valid < 32) w &= (1u << valid) - 1u;
+    }
+    bits[((size_t)k * p.ny + j) * wpr + i] = w;
+  }
+}
+
+cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
+                                  int words_per_row, cudaStream_t s) {
+  dim3 grid((p.nx + 255) / 256, p.ny, p.n_yaw);
+  gather_compact_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk_q, bits, words_per_row);
+  return cudaGetLastError();
+}
+
 __global__ void query_kernel(const AssessParams p, int n, const int4* __restrict__ idx, float* __restrict__ out) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;

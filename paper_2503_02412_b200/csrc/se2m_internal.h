@@ -76,6 +76,8 @@ cudaError_t launch_scatter_rect(float* h, int ldh, int nx, int ny, int px0, int 
                                 const float* src, long long ld, const uint8_t* known, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
+cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
+                                  int words_per_row, cudaStream_t s);
 cudaError_t launch_query(const AssessParams& p, int n, const int4* idx /* (px, py, k, 1 + 32*word + bit | 0) */,
                          float* out /* 5 x n: risk, pitch, roll, z, trav */, cudaStream_t s);
 

@@ -677,6 +677,48 @@ extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, flo
   return SE2M_OK;
 }
 
+extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact: bad mem");
+  const int wpr = (m->prm.nx + 31) / 32;
+  const size_t nst = (size_t)m->prm.nx * m->prm.ny * m->prm.n_yaw;
+  const size_t rb = risk_q ? nst * 2 : 0, bb = trav_bits ? (size_t)m->prm.n_yaw * m->prm.ny * wpr * 4 : 0;
+  if (!rb && !bb) return SE2M_OK;
+  uint16_t* dr = risk_q;
+  uint32_t* db = trav_bits;
+  if (mem == SE2M_MEM_HOST) {
+    se2m_status st = ensure_stage(m, rb + bb);
+    if (st != SE2M_OK) return st;
+    dr = risk_q ? reinterpret_cast<uint16_t*>(m->d_stage) : nullptr;
+    db = trav_bits ? reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(m->d_stage) + rb) : nullptr;
+  }
+  AssessParams p = make_params(m);
+  // owned full bins: [k_lo, k_hi) and, if paired, [k_lo + H, k_hi + H) -> two launches over half planes
+  if (!m->paired || (m->k_lo == 0 && m->k_hi == m->H)) {
+    CUDA_TRY(m, launch_gather_compact(p, m->paired ? 0 : m->k_lo, m->paired ? m->prm.n_yaw : m->k_hi, dr, db, wpr,
+                                      m->stream), "gather_compact");
+    m->launches++;
+  } else {
+    const size_t plane = (size_t)m->prm.nx * m->prm.ny;
+    for (int half = 0; half < 2; ++half) {
+      AssessParams q = p;
+      q.n_yaw = m->H;
+      q.out += plane * m->H * half;
+      q.trav += (size_t)m->H * m->prm.ny * m->trav_words * half;
+      CUDA_TRY(m, launch_gather_compact(q, m->k_lo, m->k_hi, dr ? dr + plane * m->H * half : nullptr,
+                                        db ? db + (size_t)m->H * m->prm.ny * wpr * half : nullptr, wpr, m->stream),
+               "gather_compact");
+      m->launches++;
+    }
+  }
+  if (mem == SE2M_MEM_HOST) {
+    if (risk_q) CUDA_TRY(m, cudaMemcpyAsync(risk_q, dr, rb, cudaMemcpyDeviceToHost, m->stream), "D2H risk_q");
+    if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->stream), "D2H bits");
+  }
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_compact)");
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M) {
   if (!m) return SE2M_ERR_INVALID_ARG;
   if (I_M) *I_M = m->I_M;

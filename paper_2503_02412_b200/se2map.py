@@ -28,7 +28,8 @@ SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
 
 EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elevation", "se2m_shift_window",
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
-           "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan"]
+           "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
+           "se2m_download_compact"]
 
 
 class Params(ctypes.Structure):
@@ -57,6 +58,7 @@ _lib.se2m_download.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _i32]
 _lib.se2m_get_origin.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
 _lib.se2m_stencil_info.argtypes = [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_synchronize.argtypes = [_vp]
+_lib.se2m_download_compact.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_launch_count.argtypes = [_vp]
@@ -65,7 +67,7 @@ _lib.se2m_last_error.argtypes = [_vp]
 _lib.se2m_last_error.restype = ctypes.c_char_p
 for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
               "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info",
-              "se2m_shard_plan"):
+              "se2m_shard_plan", "se2m_download_compact"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -222,6 +224,21 @@ class Se2Map:
             ptrs.append(p)
         self._check(_lib.se2m_download(self.h, *ptrs, mem))
         return res
+
+    def download_compact(self, out=None):
+        """(risk_q u16 [k][j][i], trav bits u32 [k][j][ceil(nx/32)]) in logical order (host NumPy by default)."""
+        P = self.params
+        wpr = (P.nx + 31) // 32
+        if out is None:
+            out = {"risk_q": np.empty((P.n_yaw, P.ny, P.nx), np.uint16),
+                   "trav_bits": np.empty((P.n_yaw, P.ny, wpr), np.uint32)}
+        rp, mem, k1 = _ptr_nocopy(out.get("risk_q"))
+        bp, mem2, k2 = _ptr_nocopy(out.get("trav_bits"))
+        if out.get("risk_q") is not None and out.get("trav_bits") is not None and mem != mem2:
+            raise ValueError("both outputs must be host or both device")
+        mem = mem if out.get("risk_q") is not None else mem2
+        self._check(_lib.se2m_download_compact(self.h, rp, bp, mem))
+        return out
 
     def origin(self):
         I, J = _i64(), _i64()

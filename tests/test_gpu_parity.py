@@ -155,3 +155,17 @@ def test_all_unknown_after_big_shift():
     m.assess_se2(1)
     g2 = m.download()
     assert np.all(np.isnan(g2["pitch"])) and np.all(g2["risk"] == 1) and np.all(g2["trav"] == 0)
+
+
+@pytest.mark.parametrize("nx,ny,robot", [(100, 100, (0.37, 0.61)), (37, 23, (-1.37, 2.21)), (64, 40, (5.55, -3.21))])
+def test_download_compact_matches_download(nx, ny, robot):
+    cfg = dict(CONFIGS["paper"], nx=nx, ny=ny, robot=robot)
+    m, h, g, orc, rep = run_config(cfg=cfg)
+    c = m.download_compact()
+    exp_q = np.rint(np.clip(g["risk"], 0, 1).astype(np.float32) * np.float32(65535)).astype(np.uint16)
+    assert np.array_equal(c["risk_q"], exp_q)
+    wpr = (nx + 31) // 32
+    t = np.zeros((g["trav"].shape[0], ny, wpr * 32), np.uint64)
+    t[:, :, :nx] = g["trav"]
+    exp_bits = (t.reshape(-1, ny, wpr, 32) << np.arange(32, dtype=np.uint64)).sum(-1).astype(np.uint32)
+    assert np.array_equal(c["trav_bits"], exp_bits)
