@@ -119,19 +119,19 @@ __device__ __forceinline__ F2 acos2(F2 x) {
   const F2 r = sqrt2abs(bc(1.f) - a) * pz;  // acos(|x|)
   return bc(kPi2) - copysign2(bc(kPi2) - r, x);
 }
-// asin on [-1, 1] (Cephes asinf), branch-free, odd: asin(0) = 0 exactly, asin(-x) = -asin(x).
+// asin on [-1, 1], branch-free and odd: asin(x) = sign(x) (pi/2 - sqrt(1 - |x|) P7(|x|)) (A&S 4.4.46,
+// |error| <= 2e-8 in exact arithmetic, ~1.2e-7 absolute in FP32 near 0).  P7(0) is set to the FP32 pi/2
+// so that asin(0) = 0 exactly (flat terrain gives exactly zero pitch and roll, pin Q1).
 __device__ __forceinline__ F2 asin2(F2 x) {
   const F2 a = abs2(x);
-  const bool bl = lo(a) > 0.5f, bh = hi(a) > 0.5f;
-  const F2 zb = fma2(bc(-0.5f), a, bc(0.5f));  // (1 - a)/2
-  const F2 z = sel2(bl, bh, zb, a * a);
-  const F2 sv = sel2(bl, bh, sqrt2abs(zb), a);
-  F2 pz = fma2(bc(4.2163199048e-2f), z, bc(2.4181311049e-2f));
-  pz = fma2(pz, z, bc(4.5470025998e-2f));
-  pz = fma2(pz, z, bc(7.4953002686e-2f));
-  pz = fma2(pz, z, bc(1.6666752422e-1f));
-  const F2 r = fma2(sv * z, pz, sv);
-  return copysign2(sel2(bl, bh, fma2(bc(-2.f), r, bc(kPi2)), r), x);
+  F2 pz = fma2(bc(-0.0012624911f), a, bc(0.0066700901f));
+  pz = fma2(pz, a, bc(-0.0170881256f));
+  pz = fma2(pz, a, bc(0.0308918810f));
+  pz = fma2(pz, a, bc(-0.0501743046f));
+  pz = fma2(pz, a, bc(0.0889789874f));
+  pz = fma2(pz, a, bc(-0.2145988016f));
+  pz = fma2(pz, a, bc(kPi2));
+  return copysign2(fma2(neg2(sqrt2abs(bc(1.f) - a)), pz, bc(kPi2)), x);
 }
 
 struct StateOut2 {

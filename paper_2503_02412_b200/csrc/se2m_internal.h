@@ -12,7 +12,10 @@ namespace se2m {
 constexpr int TX = 32;
 constexpr int NTHREADS = 256;              // 8 warps; warp w owns tile rows w, w + 8, w + 16, ...
 constexpr int NWARPS = NTHREADS / 32;
-constexpr int tile_rows(int R_T) { return R_T <= 12 ? 32 : 16; }
+#ifndef SE2M_TY_SMALL
+#define SE2M_TY_SMALL 32
+#endif
+constexpr int tile_rows(int R_T) { return R_T <= 12 ? SE2M_TY_SMALL : 16; }
 
 // Stencil radii the assess kernel is instantiated for (R_T >= the footprint radius R).
 constexpr int kRadii[] = {4, 8, 12, 16, 24, 32};
