@@ -281,7 +281,7 @@ template <int R_T>
 __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
-  constexpr int HX = G::HX, HY = G::HY, PW = G::PW, NR = G::NR, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
+  constexpr int HX = G::HX, HY = G::HY, PW = G::PW, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
   extern __shared__ __align__(128) unsigned char smem[];
   float* raw = reinterpret_cast<float*>(smem);
   float2* p02 = reinterpret_cast<float2*>(smem + G::p02_off);
