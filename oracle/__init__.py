@@ -81,6 +81,8 @@ def lib():
         _lib.orc_assess_state.argtypes = [P, F, U8, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_uint64, P]
         _lib.orc_eig3.argtypes = [P, P, P]
+        _lib.orc_sdf_layer.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double, P,
+                                       ctypes.c_int]
     return _lib
 
 
@@ -168,6 +170,25 @@ def eig3(C) -> tuple[np.ndarray, np.ndarray]:
     V = np.zeros((3, 3))
     lib().orc_eig3(A.ctypes.data, lam.ctypes.data, V.ctypes.data)
     return lam, V
+
+
+def sdf(obstacle, r: float, d_max: float, nthreads: int | None = None) -> np.ndarray:
+    """Signed distance field (metres) of obstacle masks [..., ny, nx] (reading R24): free cells
+    get the distance to the nearest obstacle cell, obstacle cells minus the distance to the nearest free
+    cell, clamped to +-d_max.  Brute force over all cell pairs, one layer at a time."""
+    ob = np.ascontiguousarray(obstacle, dtype=np.uint8)
+    shape = ob.shape
+    ny, nx = shape[-2], shape[-1]
+    layers = ob.reshape(-1, ny, nx)
+    out = np.empty(layers.shape, dtype=np.float64)
+    for L in range(len(layers)):
+        lay = np.ascontiguousarray(layers[L])
+        o = np.empty((ny, nx), dtype=np.float64)
+        rc = lib().orc_sdf_layer(lay.ctypes.data, nx, ny, r, d_max, o.ctypes.data, nthreads or default_threads())
+        if rc:
+            raise ValueError("oracle sdf: bad arguments")
+        out[L] = o
+    return out.reshape(shape)
 
 
 # ---------------------------------------------------------------------------------------

@@ -336,3 +336,58 @@ int orc_assess_states(const orc_params* P, const float* h, const uint8_t* known,
 
 int orc_result_size(void) { return (int)sizeof(orc_result); }
 int orc_params_size(void) { return (int)sizeof(orc_params); }
+
+/* ---------------------------------------------------------------------------------- */
+/* Signed distance field of one yaw layer (NEXT-2; "the corresponding signed  */
+/* distance field (SDF) will be generated", "the distance to the edge of the  */
+/* nearest region, with negative values inside obstacles").  Reading R24:    */
+/* obstacle = Risk = 1; a free cell's value is the Euclidean distance (m)   */
+/* between cell centres to the nearest obstacle cell, an obstacle cell's value is minus    */
+/* the distance to the nearest free cell; distances are clamped to [-d_max, d_max]; cells  */
+/* with no counterpart in the window get +-d_max.  Brute force over all cell pairs.        */
+/* obstacle: ny*nx bytes (1 obstacle, 0 free), row-major, x fastest.                       */
+/* ---------------------------------------------------------------------------------- */
+typedef struct {
+  const uint8_t* obstacle;
+  int nx, ny;
+  double r, d_max;
+  double* out;
+  int j_begin, j_end;
+} orc_sdf_job;
+
+static void* orc_sdf_worker(void* arg) {
+  orc_sdf_job* J = (orc_sdf_job*)arg;
+  for (int j = J->j_begin; j < J->j_end; ++j)
+    for (int i = 0; i < J->nx; ++i) {
+      const int self = J->obstacle[(size_t)j * J->nx + i] ? 1 : 0;
+      double best = INFINITY;
+      for (int jj = 0; jj < J->ny; ++jj)
+        for (int ii = 0; ii < J->nx; ++ii) {
+          const int other = J->obstacle[(size_t)jj * J->nx + ii] ? 1 : 0;
+          if (other == self) continue;  /* free cell: nearest obstacle; obstacle: nearest free */
+          const double dx = (ii - i) * J->r, dy = (jj - j) * J->r;
+          const double d = sqrt(dx * dx + dy * dy);
+          if (d < best) best = d;
+        }
+      if (best > J->d_max) best = J->d_max;
+      J->out[(size_t)j * J->nx + i] = self ? -best : best;
+    }
+  return NULL;
+}
+
+int orc_sdf_layer(const uint8_t* obstacle, int nx, int ny, double r, double d_max, double* out, int nthreads) {
+  if (!obstacle || !out || nx < 1 || ny < 1 || !(r > 0) || !(d_max > 0)) return -2;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  if (nthreads > ny) nthreads = ny;
+  pthread_t th[256];
+  orc_sdf_job jobs[256];
+  for (int t = 0; t < nthreads; ++t) {
+    jobs[t].obstacle = obstacle; jobs[t].nx = nx; jobs[t].ny = ny; jobs[t].r = r; jobs[t].d_max = d_max;
+    jobs[t].out = out; jobs[t].j_begin = ny * t / nthreads; jobs[t].j_end = ny * (t + 1) / nthreads;
+  }
+  if (nthreads == 1) { orc_sdf_worker(&jobs[0]); return 0; }
+  for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, orc_sdf_worker, &jobs[t]);
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}
