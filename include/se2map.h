@@ -131,6 +131,34 @@ se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, f
  * Synchronises. */
 se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
 
+/* NEXT-2: signed distance field of the explicit obstacles (Risk = 1) of
+ * every yaw layer, from the last assess ("the corresponding signed distance field (SDF)
+ * will be generated"; "the distance to the edge of the nearest region, with negative
+ * values inside obstacles").  Reading R24: a free state's value is the Euclidean distance in metres
+ * between cell centres to the nearest obstacle state of the same layer, an obstacle state's value is
+ * minus the distance to the nearest free state; cells outside the window are neither; values are
+ * clamped to [-d_max, d_max] (d_max / resolution <= 96).  Exact within d_max.  Asynchronous.
+ * Bins k and k + n/2 share an obstacle set and thus a layer.  SE2M_ERR_UNSUPPORTED with row sharding. */
+se2m_status se2m_compute_sdf(se2m_map* m, double d_max);
+
+/* The SDF in logical order, out[k][j][i] for all n_yaw bins (mem: host or device).  Synchronises. */
+se2m_status se2m_download_sdf(se2m_map* m, float* out, int32_t mem);
+
+/* Stand-alone SDF of obstacle masks (no map): mask[layer][j][i] bytes (1 obstacle, 0 free), logical
+ * order, out the same layout in float metres; same definition as se2m_compute_sdf.  mem: whether mask
+ * and out are host or device memory.  Runs on `device`, synchronous. */
+se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32_t ny, int32_t layers,
+                               double resolution, double d_max, float* out, int32_t mem, int32_t device);
+
+/* NEXT-3: the planner's map access: trilinear interpolation over (x, y, theta) of
+ * field 0 = Risk or 1 = SDF (after se2m_compute_sdf), theta cyclic across +-pi; value[q] and the exact
+ * gradient of the interpolant grad[3q..3q+2] = (d/dx, d/dy, d/dtheta) per metre / radian.  Lattice:
+ * node (i, j, k) at ((I_M + i + 1/2) r, (J_M + j + 1/2) r, theta_k).  Queries whose 8 corner nodes are
+ * not all inside the window (or owned) give NaN and the call returns SE2M_ERR_OUT_OF_RANGE after
+ * filling the others.  Any output pointer may be NULL (host memory).  Synchronises. */
+se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double* xyt, int32_t field, float* value,
+                                 float* grad);
+
 /* Window origin (world cell of logical (0,0)) and the owned representative-yaw range. */
 se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
 

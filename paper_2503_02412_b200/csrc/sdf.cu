@@ -1,0 +1,142 @@
+// sdf.cu — NEXT-2: signed distance field of the explicit-obstacle set (Risk = 1) per yaw
+// layer ("the corresponding signed distance field (SDF) will be generated"
+// "the distance to the edge of the nearest region, with negative values inside obstacles"); reading R24:
+// centre-to-centre Euclidean distance to the nearest cell of the other class, clamped to +-d_max.
+//
+// Exact within d_max: one CTA per 32 x 32 tile of one layer loads the class of every cell of the tile
+// plus a W = ceil(d_max / r) halo into shared memory, computes per column the distance (in rows) to the
+// nearest obstacle / free cell within W (separable first pass of an EDT), then per cell the minimum of
+// dx^2 + g(x + dx)^2 over |dx| <= W with early exit once dx^2 exceeds the best (second pass).
+#include <math.h>
+#include <stdint.h>
+
+#include "se2m_internal.h"
+
+namespace se2m {
+
+constexpr int SDF_T = 32;
+constexpr int SDF_THREADS = 256;
+
+__global__ void __launch_bounds__(SDF_THREADS) sdf_kernel(const SdfParams p) {
+  extern __shared__ unsigned char sm[];
+  const int W = p.W, RW = SDF_T + 2 * W;  // region width / height
+  unsigned char* cls = sm;                 // [RW][RW]: 0 free, 1 obstacle, 2 outside the window
+  unsigned char* gO = cls + RW * RW;       // [SDF_T][RW]: rows to the nearest obstacle in the column (255 none)
+  unsigned char* gF = gO + SDF_T * RW;     // ... to the nearest free cell
+  const int tiles_x = (p.nx + SDF_T - 1) / SDF_T;
+  const int i0 = (blockIdx.x % tiles_x) * SDF_T, j0 = (blockIdx.x / tiles_x) * SDF_T;
+  const int L = blockIdx.y;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < RW * RW; idx += SDF_THREADS) {
+    const int rj = idx / RW, ri = idx - rj * RW;
+    const int i = i0 - W + ri, j = j0 - W + rj;
+    unsigned char c = 2;
+    if (i >= 0 && i < p.nx && j >= 0 && j < p.ny) {
+      if (p.trav) {
+        int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+        const long long I = p.I_M + i;
+        const long long g = I >= 0 ? I / 32 : -((-I + 31) / 32);
+        const int w = (int)(((g % p.trav_words) + p.trav_words) % p.trav_words);
+        const uint32_t word = p.trav[((size_t)L * p.ny + py) * p.trav_words + w];
+        c = ((word >> (int)(I - g * 32)) & 1u) ? 0 : 1;  // traversable -> free, Risk = 1 -> obstacle
+      } else {
+        c = p.mask[((size_t)L * p.ny + j) * p.nx + i] ? 1 : 0;
+      }
+    }
+    cls[idx] = c;
+  }
+  __syncthreads();
+  // pass 1: per region column, per tile row: nearest obstacle / free cell in the column within W
+  for (int idx = tid; idx < SDF_T * RW; idx += SDF_THREADS) {
+    const int ty = idx / RW, c = idx - ty * RW;
+    const int rj = ty + W;
+    int dO = 255, dF = 255;
+    for (int d = 0; d <= W && (dO == 255 || dF == 255); ++d) {
+      const unsigned char a = cls[(rj - d) * RW + c], b = cls[(rj + d) * RW + c];
+      if (dO == 255 && (a == 1 || b == 1)) dO = d;
+      if (dF == 255 && (a == 0 || b == 0)) dF = d;
+    }
+    gO[ty * RW + c] = (unsigned char)dO;
+    gF[ty * RW + c] = (unsigned char)dF;
+  }
+  __syncthreads();
+  // pass 2: per tile cell, nearest cell of the other class
+  for (int idx = tid; idx < SDF_T * SDF_T; idx += SDF_THREADS) {
+    const int ty = idx / SDF_T, tx = idx - ty * SDF_T;
+    const int i = i0 + tx, j = j0 + ty;
+    if (i >= p.nx || j >= p.ny) continue;
+    const int c = tx + W;
+    const unsigned char self = cls[(ty + W) * RW + c];
+    const unsigned char* g = (self == 1 ? gF : gO) + ty * RW;
+    int best = 0x7fffffff;
+    for (int dx = 0; dx <= W && dx * dx < best; ++dx) {
+      const int a = g[c - dx], b = g[c + dx];
+      if (a != 255) best = min(best, dx * dx + a * a);
+      if (b != 255) best = min(best, dx * dx + b * b);
+    }
+    float d = best == 0x7fffffff ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
+    if (self == 1) d = -d;
+    size_t o;
+    if (p.trav) {
+      int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
+      int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+      o = ((size_t)L * p.ny + py) * p.nx + px;
+    } else {
+      o = ((size_t)L * p.ny + j) * p.nx + i;
+    }
+    p.out[o] = d;
+  }
+}
+
+cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
+  if (p.layers <= 0 || p.nx <= 0 || p.ny <= 0) return cudaSuccess;
+  const int RW = SDF_T + 2 * p.W;
+  const size_t smem = (size_t)RW * RW + 2 * (size_t)SDF_T * RW;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(sdf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int tiles = ((p.nx + SDF_T - 1) / SDF_T) * ((p.ny + SDF_T - 1) / SDF_T);
+  sdf_kernel<<<dim3(tiles, p.layers), SDF_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ---- NEXT-3: trilinear interpolation with gradient --------------------------------
+__global__ void trilinear_kernel(const float* __restrict__ f, int stride, int nx, int ny, int n,
+                                 const TriQuery* __restrict__ q, float inv_r, float inv_dth, float* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const TriQuery e = q[t];
+  const float qnan = __int_as_float(0x7fc00000);
+  float v = qnan, gx = qnan, gy = qnan, gt = qnan;
+  if (e.ok) {
+    const size_t plane = (size_t)nx * ny;
+    auto at = [&](int k, int py, int px) { return __ldg(f + ((size_t)k * plane + (size_t)py * nx + px) * stride); };
+    const float c000 = at(e.k0, e.py0, e.px0), c001 = at(e.k0, e.py0, e.px1);
+    const float c010 = at(e.k0, e.py1, e.px0), c011 = at(e.k0, e.py1, e.px1);
+    const float c100 = at(e.k1, e.py0, e.px0), c101 = at(e.k1, e.py0, e.px1);
+    const float c110 = at(e.k1, e.py1, e.px0), c111 = at(e.k1, e.py1, e.px1);
+    const float uy = 1.f - e.ty, ut = 1.f - e.tt;
+    // bilinear in (x, y) on each of the two yaw layers, then linear in theta
+    const float a0 = fmaf(e.tx, c001 - c000, c000), a1 = fmaf(e.tx, c011 - c010, c010);
+    const float b0 = fmaf(e.tx, c101 - c100, c100), b1 = fmaf(e.tx, c111 - c110, c110);
+    const float l0 = fmaf(e.ty, a1 - a0, a0), l1 = fmaf(e.ty, b1 - b0, b0);
+    v = fmaf(e.tt, l1 - l0, l0);
+    gt = (l1 - l0) * inv_dth;
+    gy = fmaf(e.tt, b1 - b0 - (a1 - a0), a1 - a0) * inv_r;
+    const float dx00 = c001 - c000, dx01 = c011 - c010, dx10 = c101 - c100, dx11 = c111 - c110;
+    gx = (ut * (uy * dx00 + e.ty * dx01) + e.tt * (uy * dx10 + e.ty * dx11)) * inv_r;
+  }
+  out[t] = v; out[n + t] = gx; out[2 * (size_t)n + t] = gy; out[3 * (size_t)n + t] = gt;
+}
+
+cudaError_t launch_trilinear(const float* field, int stride_elems, int nx, int ny, int n, const TriQuery* q, float inv_r,
+                             float inv_dth, float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  trilinear_kernel<<<(n + 255) / 256, 256, 0, s>>>(field, stride_elems, nx, ny, n, q, inv_r, inv_dth, out);
+  return cudaGetLastError();
+}
+
+}  // namespace se2m

@@ -84,4 +84,30 @@ cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uin
 cudaError_t launch_query(const AssessParams& p, int n, const int4* idx /* (px, py, k, 1 + 32*word + bit | 0) */,
                          float* out /* 5 x n: risk, pitch, roll, z, trav */, cudaStream_t s);
 
+// ---- NEXT-2: signed distance field of the Risk = 1 set per yaw layer (sdf.cu) ----------------------
+struct SdfParams {
+  int nx, ny, layers;    // logical window size, number of layers
+  float r, d_max;        // resolution, clamp (m)
+  int W;                 // search radius in cells = ceil(d_max / r)
+  // input: map mode (trav != nullptr): obstacle = traversable bit 0 of the map's state at logical (i, j)
+  const uint32_t* trav;
+  int trav_words, pxM, pyM;
+  long long I_M;
+  // input: mask mode: obstacle bytes [layer][j][i] logical (1 obstacle, 0 free)
+  const uint8_t* mask;
+  // output: map mode -> physical ring layout [layer][py][px]; mask mode -> logical [layer][j][i]
+  float* out;
+};
+cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s);
+
+// ---- NEXT-3: trilinear query (query.cu) ---------------------------------------------------------------
+struct TriQuery {        // host-resolved corners (physical) and weights of one query
+  int px0, px1, py0, py1, k0, k1, ok, pad;
+  float tx, ty, tt, pad2;
+};
+// field 0: risk from the state records (stride = plane of float4); field 1: sdf plane (float, layers)
+cudaError_t launch_trilinear(const float* field, int stride_elems, int nx, int ny, int n, const TriQuery* q,
+                             float inv_r, float inv_dth, float* out /* 4 x n: value, d/dx, d/dy, d/dtheta */,
+                             cudaStream_t s);
+
 }  // namespace se2m

@@ -47,6 +47,12 @@ struct se2m_map {
   float* d_h = nullptr;
   float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
+  float* d_sdf = nullptr;    // NEXT-2: SDF layers (representative bins), ring layout
+  bool sdf_valid = false;
+  double sdf_dmax = 0;
+  TriQuery* d_tq = nullptr;
+  float* d_tout = nullptr;
+  size_t tq_cap = 0;
   int4* d_full = nullptr;   // run-entry tables (see AssessParams)
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
@@ -396,7 +402,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
+  void* ptrs[] = {m->d_sdf, m->d_tq, m->d_tout, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qidx, m->d_qout};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -555,6 +561,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   }
   m->dirty.clear();
   m->all_dirty = false;
+  m->sdf_valid = false;  // the SDF follows the risk map: recompute with se2m_compute_sdf
   return SE2M_OK;
 }
 
@@ -716,6 +723,163 @@ extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint
     if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->stream), "D2H bits");
   }
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_compact)");
+  return SE2M_OK;
+}
+
+// ---- NEXT-2: SDF of the explicit-obstacle set --------------------------------------------------------
+static int sdf_radius(double d_max, double r) { return (int)ceil(d_max / r - 1e-9); }
+
+extern "C" se2m_status se2m_compute_sdf(se2m_map* m, double d_max) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!(d_max > 0) || !isfinite(d_max)) return fail(m, SE2M_ERR_INVALID_ARG, "compute_sdf: d_max must be > 0");
+  const int W = sdf_radius(d_max, m->prm.resolution);
+  if (W > 96) return fail(m, SE2M_ERR_UNSUPPORTED, "compute_sdf: d_max / resolution > 96 cells");
+  if (m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1)
+    return fail(m, SE2M_ERR_UNSUPPORTED, "compute_sdf: needs whole layers (not available with row sharding)");
+  if (!m->have_data) return fail(m, SE2M_ERR_STATE, "compute_sdf before any assess");
+  const size_t plane = (size_t)m->prm.nx * m->prm.ny;
+  if (!m->d_sdf) CUDA_TRY(m, cudaMalloc(&m->d_sdf, plane * m->H * sizeof(float)), "cudaMalloc(sdf)");
+  SdfParams sp;
+  memset(&sp, 0, sizeof sp);
+  sp.nx = m->prm.nx; sp.ny = m->prm.ny; sp.layers = m->k_hi - m->k_lo;
+  sp.r = (float)m->prm.resolution; sp.d_max = (float)d_max; sp.W = W;
+  sp.trav = m->d_trav + (size_t)m->k_lo * m->prm.ny * m->trav_words;
+  sp.trav_words = m->trav_words; sp.pxM = pmod(m->I_M, m->prm.nx); sp.pyM = pmod(m->J_M, m->prm.ny);
+  sp.I_M = m->I_M;
+  sp.out = m->d_sdf + plane * m->k_lo;
+  CUDA_TRY(m, launch_sdf(sp, m->stream), "sdf kernel");
+  m->launches++;
+  m->sdf_valid = true;
+  m->sdf_dmax = d_max;
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32_t ny, int32_t layers,
+                                          double resolution, double d_max, float* out, int32_t mem,
+                                          int32_t device) {
+  if (!mask || !out || nx < 1 || ny < 1 || layers < 1 || !(resolution > 0) || !(d_max > 0) ||
+      (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(nullptr, SE2M_ERR_INVALID_ARG, "sdf_from_mask: bad arguments");
+  const int W = sdf_radius(d_max, resolution);
+  if (W > 96) return fail(nullptr, SE2M_ERR_UNSUPPORTED, "sdf_from_mask: d_max / resolution > 96 cells");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, SE2M_ERR_CUDA, cudaGetErrorString(e));
+  const size_t n = (size_t)nx * ny * layers;
+  uint8_t* dm = const_cast<uint8_t*>(mask);
+  float* dout = out;
+  if (mem == SE2M_MEM_HOST) {
+    if ((e = cudaMalloc(&dm, n)) != cudaSuccess) return fail(nullptr, SE2M_ERR_OOM, "cudaMalloc(mask)");
+    if ((e = cudaMalloc(&dout, n * 4)) != cudaSuccess) { cudaFree(dm); return fail(nullptr, SE2M_ERR_OOM, "cudaMalloc(sdf)"); }
+    e = cudaMemcpy(dm, mask, n, cudaMemcpyHostToDevice);
+  }
+  SdfParams sp;
+  memset(&sp, 0, sizeof sp);
+  sp.nx = nx; sp.ny = ny; sp.layers = layers; sp.r = (float)resolution; sp.d_max = (float)d_max; sp.W = W;
+  sp.mask = dm; sp.out = dout;
+  if (e == cudaSuccess) e = launch_sdf(sp, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && mem == SE2M_MEM_HOST) e = cudaMemcpy(out, dout, n * 4, cudaMemcpyDeviceToHost);
+  if (mem == SE2M_MEM_HOST) { cudaFree(dm); cudaFree(dout); }
+  return e == cudaSuccess ? SE2M_OK : fail(nullptr, SE2M_ERR_CUDA, cudaGetErrorString(e));
+}
+
+// ---- NEXT-3: trilinear query of Risk / SDF with gradient ------------------------------
+extern "C" se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double* xyt, int32_t field,
+                                            float* value, float* grad) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (n < 0 || (n > 0 && !xyt) || n > (1ll << 30) || (field != 0 && field != 1))
+    return fail(m, SE2M_ERR_INVALID_ARG, "query_trilinear: bad n / xyt / field");
+  if (field == 1 && !m->sdf_valid) return fail(m, SE2M_ERR_STATE, "query_trilinear: no SDF (call se2m_compute_sdf)");
+  if (n == 0) return SE2M_OK;
+  const int nx = m->prm.nx, ny = m->prm.ny, nyaw = m->prm.n_yaw;
+  const double r = m->prm.resolution, dth = 2.0 * M_PI / nyaw;
+  std::vector<TriQuery> q((size_t)n);
+  bool any_out = false;
+  for (int64_t t = 0; t < n; ++t) {
+    TriQuery e;
+    memset(&e, 0, sizeof e);
+    const double x = xyt[3 * t], y = xyt[3 * t + 1], th = xyt[3 * t + 2];
+    if (isfinite(x) && isfinite(y) && isfinite(th)) {
+      const double fx = x / r - 0.5 - (double)m->I_M, fy = y / r - 0.5 - (double)m->J_M;
+      const double ft = (th + M_PI) / dth;
+      const double i0 = floor(fx), j0 = floor(fy), kf = floor(ft);
+      long long k0 = (long long)kf % nyaw;
+      if (k0 < 0) k0 += nyaw;
+      const long long k1 = (k0 + 1) % nyaw;
+      if (i0 >= 0 && i0 + 1 < nx && j0 >= 0 && j0 + 1 < ny) {
+        auto own = [&](long long k) { return owned_bin(m, (int)k); };
+        if (own(k0) && own(k1) && tile_owned(m, floor_div(m->J_M + (long long)j0, tile_rows(m->R_T))) &&
+            tile_owned(m, floor_div(m->J_M + (long long)j0 + 1, tile_rows(m->R_T)))) {
+          e.px0 = pmod(m->I_M + (long long)i0, nx); e.px1 = pmod(m->I_M + (long long)i0 + 1, nx);
+          e.py0 = pmod(m->J_M + (long long)j0, ny); e.py1 = pmod(m->J_M + (long long)j0 + 1, ny);
+          // the SDF is stored per representative bin (bins k and k + n/2 share their obstacle set)
+          e.k0 = (int)(field == 1 && m->paired ? k0 % m->H : k0);
+          e.k1 = (int)(field == 1 && m->paired ? k1 % m->H : k1);
+          e.tx = (float)(fx - i0); e.ty = (float)(fy - j0); e.tt = (float)(ft - kf);
+          e.ok = 1;
+        }
+      }
+    }
+    if (!e.ok) any_out = true;
+    q[t] = e;
+  }
+  if ((size_t)n > m->tq_cap) {
+    if (m->d_tq) cudaFree(m->d_tq);
+    if (m->d_tout) cudaFree(m->d_tout);
+    m->d_tq = nullptr; m->d_tout = nullptr; m->tq_cap = 0;
+    CUDA_TRY(m, cudaMalloc(&m->d_tq, (size_t)n * sizeof(TriQuery)), "cudaMalloc(trilinear)");
+    CUDA_TRY(m, cudaMalloc(&m->d_tout, (size_t)n * 4 * sizeof(float)), "cudaMalloc(trilinear)");
+    m->tq_cap = (size_t)n;
+  }
+  CUDA_TRY(m, cudaMemcpyAsync(m->d_tq, q.data(), (size_t)n * sizeof(TriQuery), cudaMemcpyHostToDevice, m->stream),
+           "H2D trilinear");
+  const float* f = field == 0 ? reinterpret_cast<const float*>(m->d_out) : m->d_sdf;
+  CUDA_TRY(m, launch_trilinear(f, field == 0 ? 4 : 1, nx, ny, (int)n, m->d_tq, (float)(1.0 / r), (float)(1.0 / dth),
+                               m->d_tout, m->stream), "trilinear kernel");
+  m->launches++;
+  std::vector<float> out((size_t)n * 4);
+  CUDA_TRY(m, cudaMemcpyAsync(out.data(), m->d_tout, out.size() * sizeof(float), cudaMemcpyDeviceToHost, m->stream),
+           "D2H trilinear");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(trilinear)");
+  for (int64_t t = 0; t < n; ++t) {
+    if (value) value[t] = out[t];
+    if (grad) { grad[3 * t] = out[n + t]; grad[3 * t + 1] = out[2 * n + t]; grad[3 * t + 2] = out[3 * n + t]; }
+  }
+  return any_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query_trilinear: some corners outside the window / not owned")
+                 : SE2M_OK;
+}
+
+// SDF planes in logical order: out[k][j][i] for all n_yaw bins (bins k and k + n/2 share a layer).
+extern "C" se2m_status se2m_download_sdf(se2m_map* m, float* out, int32_t mem) {
+  if (!m || !out || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE)) return SE2M_ERR_INVALID_ARG;
+  if (!m->sdf_valid) return fail(m, SE2M_ERR_STATE, "download_sdf: no SDF (call se2m_compute_sdf)");
+  const int nx = m->prm.nx, ny = m->prm.ny;
+  const size_t plane = (size_t)nx * ny, nst = plane * m->prm.n_yaw;
+  float* target = out;
+  if (mem == SE2M_MEM_HOST) {
+    se2m_status st = ensure_stage(m, nst * 4);
+    if (st != SE2M_OK) return st;
+    target = m->d_stage;
+  }
+  // one 2-D strided copy per logical quadrant of the ring (no extra kernel): rows [0, ny - pyM) come from
+  // physical rows [pyM, ny), the rest from [0, pyM); same split in x
+  const int pxM = pmod(m->I_M, nx), pyM = pmod(m->J_M, ny);
+  for (int k = 0; k < m->prm.n_yaw; ++k) {
+    const int L = m->paired ? k % m->H : k;
+    const float* src = m->d_sdf + plane * L;
+    float* dst = target + plane * k;
+    const int xs[2][3] = {{0, pxM, nx - pxM}, {nx - pxM, 0, pxM}};  // (logical x0, physical x0, width)
+    const int ys[2][3] = {{0, pyM, ny - pyM}, {ny - pyM, 0, pyM}};
+    for (auto& X : xs)
+      for (auto& Y : ys)
+        if (X[2] > 0 && Y[2] > 0)
+          CUDA_TRY(m, cudaMemcpy2DAsync(dst + (size_t)Y[0] * nx + X[0], (size_t)nx * 4, src + (size_t)Y[1] * nx + X[1],
+                                        (size_t)nx * 4, (size_t)X[2] * 4, Y[2], cudaMemcpyDeviceToDevice, m->stream),
+                   "sdf gather");
+  }
+  if (mem == SE2M_MEM_HOST)
+    CUDA_TRY(m, cudaMemcpyAsync(out, target, nst * 4, cudaMemcpyDeviceToHost, m->stream), "D2H sdf");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_sdf)");
   return SE2M_OK;
 }
 

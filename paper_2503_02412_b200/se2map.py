@@ -29,7 +29,8 @@ SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
 EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elevation", "se2m_shift_window",
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
-           "se2m_download_compact"]
+           "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
+           "se2m_query_trilinear"]
 
 
 class Params(ctypes.Structure):
@@ -59,6 +60,10 @@ _lib.se2m_get_origin.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)
 _lib.se2m_stencil_info.argtypes = [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_synchronize.argtypes = [_vp]
 _lib.se2m_download_compact.argtypes = [_vp, _vp, _vp, _i32]
+_lib.se2m_compute_sdf.argtypes = [_vp, _f64]
+_lib.se2m_download_sdf.argtypes = [_vp, _vp, _i32]
+_lib.se2m_sdf_from_mask.argtypes = [_vp, _i32, _i32, _i32, _f64, _f64, _vp, _i32, _i32]
+_lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_launch_count.argtypes = [_vp]
@@ -67,7 +72,8 @@ _lib.se2m_last_error.argtypes = [_vp]
 _lib.se2m_last_error.restype = ctypes.c_char_p
 for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
               "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info",
-              "se2m_shard_plan", "se2m_download_compact"):
+              "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
+              "se2m_sdf_from_mask", "se2m_query_trilinear"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -118,6 +124,20 @@ def shard_plan(params: Params) -> dict:
         raise Se2mError(st, _lib.se2m_last_error(None).decode())
     keys = ("n_rep", "k_lo", "k_hi", "tile_y", "row_mod", "row_rank")
     return {k: x.value for k, x in zip(keys, v)}
+
+
+def sdf_from_mask(mask, resolution: float, d_max: float, device: int = 0):
+    """NEXT-2 stand-alone: signed distance field (metres) of obstacle masks [layers][ny][nx] (host NumPy)."""
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    shp = m.shape
+    ny, nx = shp[-2], shp[-1]
+    layers = int(np.prod(shp[:-2])) if len(shp) > 2 else 1
+    out = np.empty(shp, np.float32)
+    st = _lib.se2m_sdf_from_mask(m.ctypes.data, nx, ny, layers, resolution, d_max, out.ctypes.data,
+                                 SE2M_MEM_HOST, device)
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    return out
 
 
 def init(params: Params):
@@ -239,6 +259,25 @@ class Se2Map:
         mem = mem if out.get("risk_q") is not None else mem2
         self._check(_lib.se2m_download_compact(self.h, rp, bp, mem))
         return out
+
+    def compute_sdf(self, d_max: float = 2.0):
+        return self._check(_lib.se2m_compute_sdf(self.h, d_max))
+
+    def download_sdf(self):
+        P = self.params
+        out = np.empty((P.n_yaw, P.ny, P.nx), np.float32)
+        self._check(_lib.se2m_download_sdf(self.h, out.ctypes.data, SE2M_MEM_HOST))
+        return out
+
+    def query_trilinear(self, xyt, field: int = 0):
+        """field 0 = risk, 1 = sdf: (value (n,), grad (n, 3), status)."""
+        xyt = np.ascontiguousarray(xyt, dtype=np.float64).reshape(-1, 3)
+        n = len(xyt)
+        v = np.empty(n, np.float32)
+        g = np.empty((n, 3), np.float32)
+        st = _lib.se2m_query_trilinear(self.h, n, xyt.ctypes.data, field, v.ctypes.data, g.ctypes.data)
+        self._check(st, ok=(SE2M_OK, SE2M_ERR_OUT_OF_RANGE))
+        return v, g, st
 
     def origin(self):
         I, J = _i64(), _i64()
