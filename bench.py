@@ -386,6 +386,7 @@ def main():
     extras = {}
     if not args.no_extras and world == 1:
         extras = small_configs(S, stream, torch)
+        extras.update(next_rows(m, stream, torch, cfg))
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -407,6 +408,39 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def next_rows(m, stream, torch, cfg, d_max=2.0, n_queries=1 << 20):
+    """SURVEY §8(f) rows built so far, on the bench map after its last assess: NEXT-2 SDF of the Risk = 1
+    set (all layers, d_max = 2 m) and NEXT-3 trilinear Risk queries with gradients (1 Mi random states)."""
+    out = {}
+    with torch.cuda.stream(stream):
+        m.compute_sdf(d_max)                         # warm
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            m.compute_sdf(d_max)
+        e1.record(stream)
+        stream.synchronize()
+        sdf_ms = e0.elapsed_time(e1) / 5
+    layers = cfg["n_yaw"] // 2 if cfg["n_yaw"] % 2 == 0 else cfg["n_yaw"]
+    out["sdf_ms"] = sdf_ms
+    out["sdf_cells_per_s"] = cfg["nx"] * cfg["ny"] * layers / (sdf_ms * 1e-3)
+    out["sdf_d_max_m"] = d_max
+    I_M, J_M = m.origin()
+    r, nx, ny = cfg["r"], cfg["nx"], cfg["ny"]
+    rng = np.random.default_rng(7)
+    q = np.stack([rng.uniform((I_M + 1) * r, (I_M + nx - 1) * r, n_queries),
+                  rng.uniform((J_M + 1) * r, (J_M + ny - 1) * r, n_queries),
+                  rng.uniform(-math.pi, math.pi, n_queries)], axis=1)
+    m.query_trilinear(q[:1024], 0)
+    t0 = time.perf_counter()
+    m.query_trilinear(q, 0)
+    dt = time.perf_counter() - t0
+    out["trilinear_queries_per_s"] = n_queries / dt
+    out["trilinear_note"] = "host wall clock of se2m_query_trilinear (host index math + H2D + kernel + D2H), 1 Mi queries"
+    return out
 
 
 def exposed_strips(di, dj, nx, ny):

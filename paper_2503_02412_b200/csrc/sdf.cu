@@ -6,7 +6,8 @@
 // Exact within d_max: one CTA per 32 x 32 tile of one layer loads the class of every cell of the tile
 // plus a W = ceil(d_max / r) halo into shared memory, computes per column the distance (in rows) to the
 // nearest obstacle / free cell within W (separable first pass of an EDT), then per cell the minimum of
-// dx^2 + g(x + dx)^2 over |dx| <= W with early exit once dx^2 exceeds the best (second pass).
+// dx^2 + g(x + dx)^2 over |dx| <= W with early exit once dx^2 exceeds the best (second pass).  The
+// column distances come from per-column bit masks (ffs / clz), O(1) per entry.
 #include <math.h>
 #include <stdint.h>
 
@@ -46,18 +47,46 @@ __global__ void __launch_bounds__(SDF_THREADS) sdf_kernel(const SdfParams p) {
     cls[idx] = c;
   }
   __syncthreads();
-  // pass 1: per region column, per tile row: nearest obstacle / free cell in the column within W
+  // pass 1: per region column a bit mask over the region's rows of obstacle / free cells (one thread per
+  // column), then per (tile row, column) the distance to the nearest set bit by ffs / clz (O(1))
+  uint64_t* mO = reinterpret_cast<uint64_t*>(((uintptr_t)(gF + SDF_T * RW) + 7) & ~(uintptr_t)7);
+  const int NWd = (RW + 63) >> 6;          // 64-bit words per column mask (<= 4 for W <= 96)
+  uint64_t* mF = mO + (size_t)RW * NWd;
+  for (int c = tid; c < RW; c += SDF_THREADS) {
+    for (int w = 0; w < NWd; ++w) {
+      uint64_t o = 0, f = 0;
+      for (int b = 0; b < 64; ++b) {
+        const int rr = w * 64 + b;
+        if (rr >= RW) break;
+        const unsigned char v = cls[rr * RW + c];
+        o |= (uint64_t)(v == 1) << b;
+        f |= (uint64_t)(v == 0) << b;
+      }
+      mO[c * NWd + w] = o;
+      mF[c * NWd + w] = f;
+    }
+  }
+  __syncthreads();
+  auto nearest = [&](const uint64_t* m, int r) {  // rows from row r to the nearest set bit, 255 beyond W
+    const int w = r >> 6, b = r & 63;
+    int up = 1 << 20, dn = 1 << 20;
+    const uint64_t x = m[w] >> b;
+    if (x) up = __ffsll((long long)x) - 1;
+    else
+      for (int w2 = w + 1; w2 < NWd; ++w2)
+        if (m[w2]) { up = w2 * 64 + __ffsll((long long)m[w2]) - 1 - r; break; }
+    const uint64_t y = m[w] << (63 - b);
+    if (y) dn = __clzll((long long)y);
+    else
+      for (int w2 = w - 1; w2 >= 0; --w2)
+        if (m[w2]) { dn = r - (w2 * 64 + 63 - __clzll((long long)m[w2])); break; }
+    const int d = min(up, dn);
+    return d <= W ? d : 255;
+  };
   for (int idx = tid; idx < SDF_T * RW; idx += SDF_THREADS) {
     const int ty = idx / RW, c = idx - ty * RW;
-    const int rj = ty + W;
-    int dO = 255, dF = 255;
-    for (int d = 0; d <= W && (dO == 255 || dF == 255); ++d) {
-      const unsigned char a = cls[(rj - d) * RW + c], b = cls[(rj + d) * RW + c];
-      if (dO == 255 && (a == 1 || b == 1)) dO = d;
-      if (dF == 255 && (a == 0 || b == 0)) dF = d;
-    }
-    gO[ty * RW + c] = (unsigned char)dO;
-    gF[ty * RW + c] = (unsigned char)dF;
+    gO[ty * RW + c] = (unsigned char)nearest(mO + c * NWd, ty + W);
+    gF[ty * RW + c] = (unsigned char)nearest(mF + c * NWd, ty + W);
   }
   __syncthreads();
   // pass 2: per tile cell, nearest cell of the other class
@@ -91,7 +120,7 @@ __global__ void __launch_bounds__(SDF_THREADS) sdf_kernel(const SdfParams p) {
 cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   if (p.layers <= 0 || p.nx <= 0 || p.ny <= 0) return cudaSuccess;
   const int RW = SDF_T + 2 * p.W;
-  const size_t smem = (size_t)RW * RW + 2 * (size_t)SDF_T * RW;
+  const size_t smem = (size_t)RW * RW + 2 * (size_t)SDF_T * RW + 8 + 2 * (size_t)RW * ((RW + 63) / 64) * 8;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(sdf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
