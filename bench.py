@@ -439,7 +439,7 @@ def next_rows(m, stream, torch, cfg, d_max=2.0, n_queries=1 << 20):
     m.query_trilinear(q, 0)
     dt = time.perf_counter() - t0
     out["trilinear_queries_per_s"] = n_queries / dt
-    out["trilinear_note"] = "host wall clock of se2m_query_trilinear (host index math + H2D + kernel + D2H), 1 Mi queries"
+    out["trilinear_note"] = "host wall clock of se2m_query_trilinear (H2D of the queries, device index math + interpolation, D2H), 1 Mi queries"
     return out
 
 

@@ -768,24 +768,107 @@ cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uin
   return cudaGetLastError();
 }
 
-__global__ void query_kernel(const AssessParams p, int n, const int4* __restrict__ idx, float* __restrict__ out) {
+__device__ __forceinline__ long long floor_div_ll(long long a, long long b) {
+  long long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+__device__ __forceinline__ int pmod_ll(long long a, int n) {
+  long long m = a % n;
+  return (int)(m < 0 ? m + n : m);
+}
+__device__ __forceinline__ bool owned_rep(const QueryGeo& g, long long k) {
+  const long long kr = (g.paired && k >= g.H) ? k - g.H : k;
+  return kr >= g.k_lo && kr < g.k_hi;
+}
+__device__ __forceinline__ bool owned_row(const QueryGeo& g, long long J) {
+  return g.row_mod <= 1 || pmod_ll(floor_div_ll(J, g.TY), g.row_mod) == g.row_rank;
+}
+
+__global__ void query_kernel(const AssessParams p, const QueryGeo g, int n, const double* __restrict__ xyt,
+                             float* __restrict__ out, int* n_out) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  const int4 e = idx[q];
+  const double x = xyt[3 * (size_t)q], y = xyt[3 * (size_t)q + 1], th = xyt[3 * (size_t)q + 2];
   const float qnan = __int_as_float(0x7fc00000);
   float4 v = make_float4(qnan, qnan, qnan, qnan);
   float tv = 0.f;
-  if (e.w) {
-    v = p.out[((size_t)e.z * p.ny + e.y) * p.nx + e.x];
-    const int wb = e.w - 1;
-    tv = (float)((p.trav[((size_t)e.z * p.ny + e.y) * p.trav_words + (wb >> 5)] >> (wb & 31)) & 1u);
+  bool ok = false;
+  if (isfinite(x) && isfinite(y) && isfinite(th)) {
+    const long long I = (long long)floor(x / g.r), J = (long long)floor(y / g.r);  // reading R6
+    const long long li = I - g.I_M, lj = J - g.J_M;
+    long long k = (long long)floor((th + 3.14159265358979323846) / g.dth + 0.5);   // nearest bin, R3
+    k %= g.n_yaw;
+    if (k < 0) k += g.n_yaw;
+    if (li >= 0 && li < g.nx && lj >= 0 && lj < g.ny && owned_rep(g, k) && owned_row(g, J)) {
+      const int px = pmod_ll(I, g.nx), py = pmod_ll(J, g.ny);
+      v = p.out[((size_t)k * g.ny + py) * g.nx + px];
+      const long long gw = floor_div_ll(I, 32);
+      const int w = pmod_ll(gw, g.trav_words), bit = (int)(I - gw * 32);
+      tv = (float)((p.trav[((size_t)k * g.ny + py) * g.trav_words + w] >> bit) & 1u);
+      ok = true;
+    }
   }
+  if (!ok) atomicAdd(n_out, 1);
   out[q] = v.x; out[n + q] = v.y; out[2 * (size_t)n + q] = v.z; out[3 * (size_t)n + q] = v.w; out[4 * (size_t)n + q] = tv;
 }
 
-cudaError_t launch_query(const AssessParams& p, int n, const int4* idx, float* out, cudaStream_t s) {
+cudaError_t launch_query(const AssessParams& p, const QueryGeo& g, int n, const double* xyt, float* out, int* n_out,
+                         cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  query_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, n, idx, out);
+  query_kernel<<<(n + 255) / 256, 256, 0, s>>>(p, g, n, xyt, out, n_out);
+  return cudaGetLastError();
+}
+
+// NEXT-3 trilinear query: node (i, j, k) at ((I_M + i + 1/2) r, (J_M + j + 1/2) r, theta_k),
+// theta cyclic; value and the exact gradient of the interpolant.
+__global__ void trilinear_kernel(const float* __restrict__ f, int stride, int is_sdf, const QueryGeo g, int n,
+                                 const double* __restrict__ xyt, float* __restrict__ out, int* n_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double x = xyt[3 * (size_t)t], y = xyt[3 * (size_t)t + 1], th = xyt[3 * (size_t)t + 2];
+  const float qnan = __int_as_float(0x7fc00000);
+  float v = qnan, gx = qnan, gy = qnan, gt = qnan;
+  bool ok = false;
+  if (isfinite(x) && isfinite(y) && isfinite(th)) {
+    const double fx = x / g.r - 0.5 - (double)g.I_M, fy = y / g.r - 0.5 - (double)g.J_M;
+    const double ft = (th + 3.14159265358979323846) / g.dth;
+    const double i0 = floor(fx), j0 = floor(fy), kf = floor(ft);
+    long long k0 = (long long)kf % g.n_yaw;
+    if (k0 < 0) k0 += g.n_yaw;
+    const long long k1 = (k0 + 1) % g.n_yaw;
+    const long long J0 = g.J_M + (long long)j0;
+    if (i0 >= 0 && i0 + 1 < g.nx && j0 >= 0 && j0 + 1 < g.ny && owned_rep(g, k0) && owned_rep(g, k1) &&
+        owned_row(g, J0) && owned_row(g, J0 + 1)) {
+      const int px0 = pmod_ll(g.I_M + (long long)i0, g.nx), px1 = pmod_ll(g.I_M + (long long)i0 + 1, g.nx);
+      const int py0 = pmod_ll(J0, g.ny), py1 = pmod_ll(J0 + 1, g.ny);
+      // the SDF is stored per representative bin (bins k and k + n/2 share their obstacle set)
+      const int L0 = (int)(is_sdf && g.paired ? k0 % g.H : k0), L1 = (int)(is_sdf && g.paired ? k1 % g.H : k1);
+      const float tx = (float)(fx - i0), ty = (float)(fy - j0), tt = (float)(ft - kf);
+      const size_t plane = (size_t)g.nx * g.ny;
+      auto at = [&](int L, int py, int px) { return __ldg(f + ((size_t)L * plane + (size_t)py * g.nx + px) * stride); };
+      const float c000 = at(L0, py0, px0), c001 = at(L0, py0, px1), c010 = at(L0, py1, px0), c011 = at(L0, py1, px1);
+      const float c100 = at(L1, py0, px0), c101 = at(L1, py0, px1), c110 = at(L1, py1, px0), c111 = at(L1, py1, px1);
+      const float uy = 1.f - ty, ut = 1.f - tt;
+      const float a0 = fmaf(tx, c001 - c000, c000), a1 = fmaf(tx, c011 - c010, c010);
+      const float b0 = fmaf(tx, c101 - c100, c100), b1 = fmaf(tx, c111 - c110, c110);
+      const float l0 = fmaf(ty, a1 - a0, a0), l1 = fmaf(ty, b1 - b0, b0);
+      v = fmaf(tt, l1 - l0, l0);
+      gt = (l1 - l0) * (float)(1.0 / g.dth);
+      gy = fmaf(tt, b1 - b0 - (a1 - a0), a1 - a0) * (float)(1.0 / g.r);
+      gx = (ut * (uy * (c001 - c000) + ty * (c011 - c010)) + tt * (uy * (c101 - c100) + ty * (c111 - c110))) *
+           (float)(1.0 / g.r);
+      ok = true;
+    }
+  }
+  if (!ok) atomicAdd(n_out, 1);
+  out[t] = v; out[n + t] = gx; out[2 * (size_t)n + t] = gy; out[3 * (size_t)n + t] = gt;
+}
+
+cudaError_t launch_trilinear(const float* field, int stride_elems, int is_sdf, const QueryGeo& g, int n,
+                             const double* xyt, float* out, int* n_out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  trilinear_kernel<<<(n + 255) / 256, 256, 0, s>>>(field, stride_elems, is_sdf, g, n, xyt, out, n_out);
   return cudaGetLastError();
 }
 

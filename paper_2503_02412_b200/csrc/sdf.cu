@@ -132,40 +132,4 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ---- NEXT-3: trilinear interpolation with gradient --------------------------------
-__global__ void trilinear_kernel(const float* __restrict__ f, int stride, int nx, int ny, int n,
-                                 const TriQuery* __restrict__ q, float inv_r, float inv_dth, float* __restrict__ out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const TriQuery e = q[t];
-  const float qnan = __int_as_float(0x7fc00000);
-  float v = qnan, gx = qnan, gy = qnan, gt = qnan;
-  if (e.ok) {
-    const size_t plane = (size_t)nx * ny;
-    auto at = [&](int k, int py, int px) { return __ldg(f + ((size_t)k * plane + (size_t)py * nx + px) * stride); };
-    const float c000 = at(e.k0, e.py0, e.px0), c001 = at(e.k0, e.py0, e.px1);
-    const float c010 = at(e.k0, e.py1, e.px0), c011 = at(e.k0, e.py1, e.px1);
-    const float c100 = at(e.k1, e.py0, e.px0), c101 = at(e.k1, e.py0, e.px1);
-    const float c110 = at(e.k1, e.py1, e.px0), c111 = at(e.k1, e.py1, e.px1);
-    const float uy = 1.f - e.ty, ut = 1.f - e.tt;
-    // bilinear in (x, y) on each of the two yaw layers, then linear in theta
-    const float a0 = fmaf(e.tx, c001 - c000, c000), a1 = fmaf(e.tx, c011 - c010, c010);
-    const float b0 = fmaf(e.tx, c101 - c100, c100), b1 = fmaf(e.tx, c111 - c110, c110);
-    const float l0 = fmaf(e.ty, a1 - a0, a0), l1 = fmaf(e.ty, b1 - b0, b0);
-    v = fmaf(e.tt, l1 - l0, l0);
-    gt = (l1 - l0) * inv_dth;
-    gy = fmaf(e.tt, b1 - b0 - (a1 - a0), a1 - a0) * inv_r;
-    const float dx00 = c001 - c000, dx01 = c011 - c010, dx10 = c101 - c100, dx11 = c111 - c110;
-    gx = (ut * (uy * dx00 + e.ty * dx01) + e.tt * (uy * dx10 + e.ty * dx11)) * inv_r;
-  }
-  out[t] = v; out[n + t] = gx; out[2 * (size_t)n + t] = gy; out[3 * (size_t)n + t] = gt;
-}
-
-cudaError_t launch_trilinear(const float* field, int stride_elems, int nx, int ny, int n, const TriQuery* q, float inv_r,
-                             float inv_dth, float* out, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  trilinear_kernel<<<(n + 255) / 256, 256, 0, s>>>(field, stride_elems, nx, ny, n, q, inv_r, inv_dth, out);
-  return cudaGetLastError();
-}
-
 }  // namespace se2m

@@ -81,8 +81,18 @@ cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, flo
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
 cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
                                   int words_per_row, cudaStream_t s);
-cudaError_t launch_query(const AssessParams& p, int n, const int4* idx /* (px, py, k, 1 + 32*word + bit | 0) */,
-                         float* out /* 5 x n: risk, pitch, roll, z, trav */, cudaStream_t s);
+// World (x, y, theta) -> ring indices, resolved on the device in FP64 exactly as readings R3/R6 state.
+struct QueryGeo {
+  double r, dth;
+  long long I_M, J_M;
+  int nx, ny, n_yaw, H, paired;
+  int k_lo, k_hi;          // owned representative bins
+  int row_mod, row_rank;   // owned world tile rows (TJ mod row_mod == row_rank)
+  int TY, trav_words;
+};
+// nearest state (H10): out 5 x n (risk, pitch, roll, z, trav); *n_out += queries outside / not owned
+cudaError_t launch_query(const AssessParams& p, const QueryGeo& g, int n, const double* xyt, float* out, int* n_out,
+                         cudaStream_t s);
 
 // ---- NEXT-2: signed distance field of the Risk = 1 set per yaw layer (sdf.cu) ----------------------
 struct SdfParams {
@@ -101,13 +111,9 @@ struct SdfParams {
 cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s);
 
 // ---- NEXT-3: trilinear query (query.cu) ---------------------------------------------------------------
-struct TriQuery {        // host-resolved corners (physical) and weights of one query
-  int px0, px1, py0, py1, k0, k1, ok, pad;
-  float tx, ty, tt, pad2;
-};
-// field 0: risk from the state records (stride = plane of float4); field 1: sdf plane (float, layers)
-cudaError_t launch_trilinear(const float* field, int stride_elems, int nx, int ny, int n, const TriQuery* q,
-                             float inv_r, float inv_dth, float* out /* 4 x n: value, d/dx, d/dy, d/dtheta */,
-                             cudaStream_t s);
+// field 0: risk from the state records (stride 4 floats); field 1: sdf layers (stride 1, representative
+// bins when paired); out 4 x n (value, d/dx, d/dy, d/dtheta); *n_out += queries with a corner outside
+cudaError_t launch_trilinear(const float* field, int stride_elems, int is_sdf, const QueryGeo& g, int n,
+                             const double* xyt, float* out, int* n_out, cudaStream_t s);
 
 }  // namespace se2m

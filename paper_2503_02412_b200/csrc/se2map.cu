@@ -50,9 +50,6 @@ struct se2m_map {
   float* d_sdf = nullptr;    // NEXT-2: SDF layers (representative bins), ring layout
   bool sdf_valid = false;
   double sdf_dmax = 0;
-  TriQuery* d_tq = nullptr;
-  float* d_tout = nullptr;
-  size_t tq_cap = 0;
   int4* d_full = nullptr;   // run-entry tables (see AssessParams)
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
@@ -65,8 +62,9 @@ struct se2m_map {
   std::vector<int> ncells;  // |P_k| per rep bin
   float* d_stage = nullptr;  // update / download staging
   size_t stage_bytes = 0;
-  int4* d_qidx = nullptr;
+  double* d_qxyt = nullptr;   // query staging: xyt in, 5 x n floats out, out-of-range counter
   float* d_qout = nullptr;
+  int* d_qcnt = nullptr;
   size_t q_cap = 0;
   CUtensorMap tmap;
   bool tma_ok = false;
@@ -402,8 +400,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_sdf, m->d_tq, m->d_tout, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
-                  m->d_cs, m->d_stage, m->d_qidx, m->d_qout};
+  void* ptrs[] = {m->d_sdf, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
+                  m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
@@ -489,10 +487,6 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
   return SE2M_OK;
 }
 
-static bool tile_owned(const se2m_map* m, long long TJ) {  // TJ: world tile row (tile_rows(R_T) rows)
-  if (m->prm.shard_mode != SE2M_SHARD_ROWS || m->prm.world_size <= 1) return true;
-  return pmod(TJ, m->prm.world_size) == m->prm.rank;
-}
 
 extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   if (!m) return SE2M_ERR_INVALID_ARG;
@@ -572,9 +566,35 @@ extern "C" se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_
   return SE2M_OK;
 }
 
-static bool owned_bin(const se2m_map* m, int k) {
-  const int kr = (m->paired && k >= m->H) ? k - m->H : k;
-  return kr >= m->k_lo && kr < m->k_hi;
+
+static QueryGeo query_geo(const se2m_map* m) {
+  QueryGeo g;
+  memset(&g, 0, sizeof g);
+  g.r = m->prm.resolution; g.dth = 2.0 * M_PI / m->prm.n_yaw;
+  g.I_M = m->I_M; g.J_M = m->J_M;
+  g.nx = m->prm.nx; g.ny = m->prm.ny; g.n_yaw = m->prm.n_yaw; g.H = m->H; g.paired = m->paired;
+  g.k_lo = m->k_lo; g.k_hi = m->k_hi;
+  const bool rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  g.row_mod = rows ? m->prm.world_size : 1; g.row_rank = rows ? m->prm.rank : 0;
+  g.TY = tile_rows(m->R_T); g.trav_words = m->trav_words;
+  return g;
+}
+
+// Stage n queries on the device; returns the number of output floats per query slot (cap grows).
+static se2m_status stage_queries(se2m_map* m, int64_t n, const double* xyt) {
+  if ((size_t)n > m->q_cap) {
+    if (m->d_qxyt) cudaFree(m->d_qxyt);
+    if (m->d_qout) cudaFree(m->d_qout);
+    m->d_qxyt = nullptr; m->d_qout = nullptr; m->q_cap = 0;
+    CUDA_TRY(m, cudaMalloc(&m->d_qxyt, (size_t)n * 3 * sizeof(double)), "cudaMalloc(query)");
+    CUDA_TRY(m, cudaMalloc(&m->d_qout, (size_t)n * 5 * sizeof(float)), "cudaMalloc(query)");
+    m->q_cap = (size_t)n;
+  }
+  if (!m->d_qcnt) CUDA_TRY(m, cudaMalloc(&m->d_qcnt, sizeof(int)), "cudaMalloc(query)");
+  CUDA_TRY(m, cudaMemsetAsync(m->d_qcnt, 0, sizeof(int), m->stream), "query counter");
+  CUDA_TRY(m, cudaMemcpyAsync(m->d_qxyt, xyt, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, m->stream),
+           "H2D query");
+  return SE2M_OK;
 }
 
 extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, float* pitch, float* roll,
@@ -582,51 +602,23 @@ extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, flo
   if (!m) return SE2M_ERR_INVALID_ARG;
   if (n < 0 || (n > 0 && !xyt) || n > (1ll << 30)) return fail(m, SE2M_ERR_INVALID_ARG, "query: bad n / xyt");
   if (n == 0) return SE2M_OK;
-  const int nx = m->prm.nx, ny = m->prm.ny, ny_aw = m->prm.n_yaw;
-  const double r = m->prm.resolution, dth = 2.0 * M_PI / ny_aw;
-  std::vector<int4> idx((size_t)n);
-  bool any_out = false;
-  for (int64_t q = 0; q < n; ++q) {
-    const double x = xyt[3 * q], y = xyt[3 * q + 1], th = xyt[3 * q + 2];
-    int4 e = make_int4(0, 0, 0, 0);
-    if (isfinite(x) && isfinite(y) && isfinite(th)) {
-      const long long li = (long long)floor(x / r) - m->I_M, lj = (long long)floor(y / r) - m->J_M;
-      long long k = (long long)floor((th + M_PI) / dth + 0.5);  // nearest bin (reading R3)
-      k %= ny_aw;
-      if (k < 0) k += ny_aw;
-      const long long TJ = floor_div(lj + m->J_M, tile_rows(m->R_T));
-      if (li >= 0 && li < nx && lj >= 0 && lj < ny && owned_bin(m, (int)k) && tile_owned(m, TJ)) {
-        const long long I = m->I_M + li;
-        const int word = pmod(floor_div(I, 32), m->trav_words), bit = pmod(I, 32);
-        e = make_int4(pmod(I, nx), pmod(m->J_M + lj, ny), (int)k, 1 + 32 * word + bit);
-      }
-    }
-    if (!e.w) any_out = true;
-    idx[q] = e;
-  }
-  if ((size_t)n > m->q_cap) {
-    if (m->d_qidx) cudaFree(m->d_qidx);
-    if (m->d_qout) cudaFree(m->d_qout);
-    m->d_qidx = nullptr; m->d_qout = nullptr; m->q_cap = 0;
-    CUDA_TRY(m, cudaMalloc(&m->d_qidx, (size_t)n * sizeof(int4)), "cudaMalloc(query)");
-    CUDA_TRY(m, cudaMalloc(&m->d_qout, (size_t)n * 5 * sizeof(float)), "cudaMalloc(query)");
-    m->q_cap = (size_t)n;
-  }
-  CUDA_TRY(m, cudaMemcpyAsync(m->d_qidx, idx.data(), (size_t)n * sizeof(int4), cudaMemcpyHostToDevice, m->stream), "H2D query");
+  se2m_status st = stage_queries(m, n, xyt);
+  if (st != SE2M_OK) return st;
   AssessParams p = make_params(m);
-  CUDA_TRY(m, launch_query(p, (int)n, m->d_qidx, m->d_qout, m->stream), "query kernel");
+  CUDA_TRY(m, launch_query(p, query_geo(m), (int)n, m->d_qxyt, m->d_qout, m->d_qcnt, m->stream), "query kernel");
   m->launches++;
   std::vector<float> out((size_t)n * 5);
+  int n_out = 0;
   CUDA_TRY(m, cudaMemcpyAsync(out.data(), m->d_qout, out.size() * sizeof(float), cudaMemcpyDeviceToHost, m->stream), "D2H query");
+  CUDA_TRY(m, cudaMemcpyAsync(&n_out, m->d_qcnt, sizeof(int), cudaMemcpyDeviceToHost, m->stream), "D2H query");
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(query)");
-  for (int64_t q = 0; q < n; ++q) {
-    if (risk) risk[q] = out[q];
-    if (pitch) pitch[q] = out[n + q];
-    if (roll) roll[q] = out[2 * n + q];
-    if (z) z[q] = out[3 * n + q];
-    if (trav) trav[q] = out[4 * n + q] > 0.5f ? 1 : 0;
-  }
-  return any_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query: some states outside the window / not owned") : SE2M_OK;
+  if (risk) memcpy(risk, out.data(), n * sizeof(float));
+  if (pitch) memcpy(pitch, out.data() + n, n * sizeof(float));
+  if (roll) memcpy(roll, out.data() + 2 * n, n * sizeof(float));
+  if (z) memcpy(z, out.data() + 3 * n, n * sizeof(float));
+  if (trav)
+    for (int64_t q = 0; q < n; ++q) trav[q] = out[4 * n + q] > 0.5f ? 1 : 0;
+  return n_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query: some states outside the window / not owned") : SE2M_OK;
 }
 
 extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z, uint8_t* trav,
@@ -791,62 +783,25 @@ extern "C" se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double
     return fail(m, SE2M_ERR_INVALID_ARG, "query_trilinear: bad n / xyt / field");
   if (field == 1 && !m->sdf_valid) return fail(m, SE2M_ERR_STATE, "query_trilinear: no SDF (call se2m_compute_sdf)");
   if (n == 0) return SE2M_OK;
-  const int nx = m->prm.nx, ny = m->prm.ny, nyaw = m->prm.n_yaw;
-  const double r = m->prm.resolution, dth = 2.0 * M_PI / nyaw;
-  std::vector<TriQuery> q((size_t)n);
-  bool any_out = false;
-  for (int64_t t = 0; t < n; ++t) {
-    TriQuery e;
-    memset(&e, 0, sizeof e);
-    const double x = xyt[3 * t], y = xyt[3 * t + 1], th = xyt[3 * t + 2];
-    if (isfinite(x) && isfinite(y) && isfinite(th)) {
-      const double fx = x / r - 0.5 - (double)m->I_M, fy = y / r - 0.5 - (double)m->J_M;
-      const double ft = (th + M_PI) / dth;
-      const double i0 = floor(fx), j0 = floor(fy), kf = floor(ft);
-      long long k0 = (long long)kf % nyaw;
-      if (k0 < 0) k0 += nyaw;
-      const long long k1 = (k0 + 1) % nyaw;
-      if (i0 >= 0 && i0 + 1 < nx && j0 >= 0 && j0 + 1 < ny) {
-        auto own = [&](long long k) { return owned_bin(m, (int)k); };
-        if (own(k0) && own(k1) && tile_owned(m, floor_div(m->J_M + (long long)j0, tile_rows(m->R_T))) &&
-            tile_owned(m, floor_div(m->J_M + (long long)j0 + 1, tile_rows(m->R_T)))) {
-          e.px0 = pmod(m->I_M + (long long)i0, nx); e.px1 = pmod(m->I_M + (long long)i0 + 1, nx);
-          e.py0 = pmod(m->J_M + (long long)j0, ny); e.py1 = pmod(m->J_M + (long long)j0 + 1, ny);
-          // the SDF is stored per representative bin (bins k and k + n/2 share their obstacle set)
-          e.k0 = (int)(field == 1 && m->paired ? k0 % m->H : k0);
-          e.k1 = (int)(field == 1 && m->paired ? k1 % m->H : k1);
-          e.tx = (float)(fx - i0); e.ty = (float)(fy - j0); e.tt = (float)(ft - kf);
-          e.ok = 1;
-        }
-      }
-    }
-    if (!e.ok) any_out = true;
-    q[t] = e;
-  }
-  if ((size_t)n > m->tq_cap) {
-    if (m->d_tq) cudaFree(m->d_tq);
-    if (m->d_tout) cudaFree(m->d_tout);
-    m->d_tq = nullptr; m->d_tout = nullptr; m->tq_cap = 0;
-    CUDA_TRY(m, cudaMalloc(&m->d_tq, (size_t)n * sizeof(TriQuery)), "cudaMalloc(trilinear)");
-    CUDA_TRY(m, cudaMalloc(&m->d_tout, (size_t)n * 4 * sizeof(float)), "cudaMalloc(trilinear)");
-    m->tq_cap = (size_t)n;
-  }
-  CUDA_TRY(m, cudaMemcpyAsync(m->d_tq, q.data(), (size_t)n * sizeof(TriQuery), cudaMemcpyHostToDevice, m->stream),
-           "H2D trilinear");
+  se2m_status st = stage_queries(m, n, xyt);
+  if (st != SE2M_OK) return st;
   const float* f = field == 0 ? reinterpret_cast<const float*>(m->d_out) : m->d_sdf;
-  CUDA_TRY(m, launch_trilinear(f, field == 0 ? 4 : 1, nx, ny, (int)n, m->d_tq, (float)(1.0 / r), (float)(1.0 / dth),
-                               m->d_tout, m->stream), "trilinear kernel");
+  CUDA_TRY(m, launch_trilinear(f, field == 0 ? 4 : 1, field, query_geo(m), (int)n, m->d_qxyt, m->d_qout, m->d_qcnt,
+                               m->stream), "trilinear kernel");
   m->launches++;
   std::vector<float> out((size_t)n * 4);
-  CUDA_TRY(m, cudaMemcpyAsync(out.data(), m->d_tout, out.size() * sizeof(float), cudaMemcpyDeviceToHost, m->stream),
+  int n_out = 0;
+  CUDA_TRY(m, cudaMemcpyAsync(out.data(), m->d_qout, out.size() * sizeof(float), cudaMemcpyDeviceToHost, m->stream),
            "D2H trilinear");
+  CUDA_TRY(m, cudaMemcpyAsync(&n_out, m->d_qcnt, sizeof(int), cudaMemcpyDeviceToHost, m->stream), "D2H trilinear");
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(trilinear)");
-  for (int64_t t = 0; t < n; ++t) {
-    if (value) value[t] = out[t];
-    if (grad) { grad[3 * t] = out[n + t]; grad[3 * t + 1] = out[2 * n + t]; grad[3 * t + 2] = out[3 * n + t]; }
-  }
-  return any_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query_trilinear: some corners outside the window / not owned")
-                 : SE2M_OK;
+  if (value) memcpy(value, out.data(), n * sizeof(float));
+  if (grad)
+    for (int64_t t = 0; t < n; ++t) {
+      grad[3 * t] = out[n + t]; grad[3 * t + 1] = out[2 * n + t]; grad[3 * t + 2] = out[3 * n + t];
+    }
+  return n_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query_trilinear: some corners outside the window / not owned")
+               : SE2M_OK;
 }
 
 // SDF planes in logical order: out[k][j][i] for all n_yaw bins (bins k and k + n/2 share a layer).
