@@ -112,6 +112,18 @@ class Hills:
             h += self.rocks(x, y)
         return h
 
+    def surface(self, x, y):
+        """The continuous terrain surface (hills + rocks, no per-cell noise): what a LiDAR sees."""
+        lam, psi, phi, amp = self.components()
+        x = np.asarray(x, dtype=np.float64)
+        y = np.asarray(y, dtype=np.float64)
+        h = np.full(np.broadcast(x, y).shape, self.h0, dtype=np.float64)
+        for k in range(self.K):
+            h += amp[k] * np.sin(2.0 * math.pi / lam[k] * (x * math.cos(psi[k]) + y * math.sin(psi[k])) + phi[k])
+        if self.rock_density > 0:
+            h += self.rocks(x, y)
+        return h
+
     def rocks(self, x, y):
         """Sparse Gaussian bumps ('rocks'): at most one per rock_block-sized world block, placed and
         sized by a hash of (seed, block) so that they are a pure function of world position.
