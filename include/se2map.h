@@ -68,7 +68,21 @@ typedef struct {
   int32_t device;          /* CUDA device ordinal */
   int32_t reserved0;
   void* cuda_stream;       /* cudaStream_t to order all work on, or NULL: the library creates one */
+  /* NEXT-1 front-end (se2m_integrate_scan, readings R26-R30): */
+  double fe_z_min, fe_z_max; /* body-frame height band of used points, m (default -1.5, 1.5) */
+  double fe_gate;          /* Mahalanobis gate |z - h| / sqrt(s2 + s2_m) (default 2.0) */
+  double fe_ray_eps;       /* ray-cast margin, m (default 0.05) */
+  double fe_prior_var;     /* variance given to cells written by se2m_update_elevation, m^2 (default 1e-4) */
 } se2m_params;
+
+/* NEXT-1: one LiDAR frame.  Rotations row-major (world <- body, body <- sensor), covariances 3x3. */
+typedef struct {
+  double R_B[9], p_B[3];   /* robot attitude and position (world) */
+  double R_BS[9], p_BS[3]; /* LiDAR extrinsics: sensor -> body rotation, LiDAR position in the body frame */
+  double Sigma_S[9];       /* sensor point noise */
+  double Sigma_R[9];       /* attitude covariance, tangent space (right perturbation) */
+  double Sigma_B[9];       /* position covariance */
+} se2m_pose;
 
 /* Fill *p with the defaults above (thresholds from PAPER.md:291 / SPEC S:300). */
 void se2m_default_params(se2m_params* p);
@@ -130,6 +144,21 @@ se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, f
  * (ceil(nx/32) words per row, bits past nx zero).  Either pointer may be NULL; mem as in se2m_download.
  * Synchronises. */
 se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+
+/* NEXT-1: integrate one LiDAR frame into the elevation window (§V.A, Fig. 3):
+ * points (n x 3 float, sensor frame; host or device per mem) are transformed with the pose, points
+ * outside the window or outside the body-frame height band are ignored, each point gets the
+ * height variance of P:113-120; then every ray (LiDAR -> used point) resets to unknown the cells it
+ * crosses whose height exceeds the ray's highest height over the cell + fe_ray_eps (the
+ * point's own cell excluded), and the points are fused per cell in input order by a 1-D Kalman filter
+ * with the Mahalanobis gate / higher-wins rule.  FP64 arithmetic in a fixed order; cells
+ * keep float32 height and variance.  Marks the touched cells dirty.  Optional out_counts[5] = points
+ * used, outside the map, outside the band, with sigma^2 <= 0, and ray-reset events.  Synchronises. */
+se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int64_t n, const se2m_pose* pose,
+                                int32_t mem, int64_t* out_counts);
+
+/* Heights and variances of the window in logical order (ny x nx each, NaN height = unknown). */
+se2m_status se2m_download_elevation(se2m_map* m, float* heights, float* variances, int32_t mem);
 
 /* NEXT-2: signed distance field of the explicit obstacles (Risk = 1) of
  * every yaw layer, from the last assess ("the corresponding signed distance field (SDF)

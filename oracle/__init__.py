@@ -211,6 +211,7 @@ class Window:
         self.I_M, self.J_M = window_origin(x, y, r, nx, ny)
         self.heights = np.zeros((ny, nx), dtype=np.float32)
         self.known = np.zeros((ny, nx), dtype=np.uint8)
+        self.var = np.zeros((ny, nx), dtype=np.float32)   # cell height variance (front-end, NEXT-1)
 
     def shift(self, x: float, y: float) -> tuple[int, int]:
         """Recentre (Eq. 4); retained cells keep their values bit-exactly, cells that enter
@@ -220,13 +221,15 @@ class Window:
         di, dj = I_M - self.I_M, J_M - self.J_M
         h = np.zeros_like(self.heights)
         k = np.zeros_like(self.known)
+        v = np.zeros_like(self.var)
         for j in range(self.ny):
             for i in range(self.nx):
                 oi, oj = i + di, j + dj            # old logical index of new cell (i, j)
                 if 0 <= oi < self.nx and 0 <= oj < self.ny:
                     h[j, i] = self.heights[oj, oi]
                     k[j, i] = self.known[oj, oi]
-        self.heights, self.known = h, k
+                    v[j, i] = self.var[oj, oi]
+        self.heights, self.known, self.var = h, k, v
         self.I_M, self.J_M = I_M, J_M
         return di, dj
 

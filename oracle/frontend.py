@@ -97,12 +97,13 @@ def _cell_interval(sx, sy, dx, dy, x0, x1, y0, y1):
     return t0, t1
 
 
-def integrate_scan(win, var, points_s, pose: Pose, P: FrontendParams):
-    """One frame on an oracle.Window (heights/known float32/uint8 arrays) and a float32 variance array
-    of the same shape, both updated in place.  Returns per-point status (0 used, 1 outside map,
+def integrate_scan(win, points_s, pose: Pose, P: FrontendParams):
+    """One frame on an oracle.Window (its float32 heights / variances and uint8 known arrays are updated
+    in place).  Returns per-point status (0 used, 1 outside map,
     2 outside height band, 3 non-positive variance) and the number of cells reset by ray casting."""
     r = win.r
     nx, ny = win.nx, win.ny
+    var = win.var
     meas = []
     status = np.zeros(len(points_s), np.int32)
     for n, ps in enumerate(points_s):

@@ -229,31 +229,122 @@ __device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 
                        true, Gx, Gy, csk, p);
 }
 
-// border / unknown tiles: per-state moments (cell units for x, y; metres for h^)
-__device__ __forceinline__ bool assessable(float N, float Sx, float Sy, float Sxx, float Sxy, float Syy) {
-  if (N < 2.5f) return false;  // |P| < 3 (reading R8)
-  const double dN = N;         // collinear footprint cells: exact integer test (reading R22)
+// border / unknown tiles: per-state moments (cell units for x, y; metres for h^).
+// Footprint geometry (exact integers): a = N Sxx - Sx^2, b = N Syy - Sy^2, c = N Sxy - Sx Sy, in FP64.
+struct Shape {
+  bool ok;            // assessable: |P| >= 3 and not collinear
+  float a, b, c;      // N^2 x the cell-unit covariance of the footprint cells, rounded once
+};
+__device__ __forceinline__ Shape footprint_shape(float N, float Sx, float Sy, float Sxx, float Sxy, float Syy) {
+  const double dN = N;  // collinear footprint cells: exact integer test (reading R22)
   const double a = dN * Sxx - (double)Sx * Sx, b = dN * Syy - (double)Sy * Sy, c = dN * Sxy - (double)Sx * Sy;
-  return a * b - c * c > 1e-9 * a * b;
+  Shape s;
+  s.ok = N > 2.5f && a * b - c * c > 1e-9 * a * b;  // |P| < 3: unknown (reading R8)
+  s.a = (float)a; s.b = (float)b; s.c = (float)c;
+  return s;
 }
-__device__ __forceinline__ StateOut2 epilogue2_general(F2 N, F2 Sx, F2 Sy, F2 Sxx, F2 Sxy, F2 Syy, F2 S0, F2 S2, F2 SXH,
-                                                       F2 SYH, F2 zref, float gx, float gy, float2 csk,
-                                                       const AssessParams& p) {
-  const bool okl = assessable(lo(N), lo(Sx), lo(Sy), lo(Sxx), lo(Sxy), lo(Syy));
-  const bool okh = assessable(hi(N), hi(Sx), hi(Sy), hi(Sxx), hi(Sxy), hi(Syy));
-  const F2 iN = rcp2(sel2(okl, okh, N, bc(3.f)));
+// Covariance of (x, y, h) in metres (Alg. 1 lines 2-8) with the tile-plane correction applied
+// (h = h^ + gx x + gy y + const, x, y in cells); mx, my: footprint centroid offset (m); zz: mean height.
+struct Cov2 {
+  F2 c00, c01, c11, c02, c12, c22, mx, my, zz;
+};
+__device__ __forceinline__ Cov2 cov_general(F2 N, F2 Sx, F2 Sy, const Shape& sl, const Shape& sh, F2 S0, F2 S2,
+                                            F2 SXH, F2 SYH, F2 zref, float gx, float gy, float r) {
+  const F2 iN = rcp2(sel2(sl.ok, sh.ok, N, bc(3.f)));
   const F2 mxc = Sx * iN, myc = Sy * iN, mh = S0 * iN;
-  const F2 r = bc(p.r), r2 = bc(p.r * p.r);
-  const F2 C00 = r2 * fma2(neg2(mxc), mxc, Sxx * iN);
-  const F2 C01 = r2 * fma2(neg2(mxc), myc, Sxy * iN);
-  const F2 C11 = r2 * fma2(neg2(myc), myc, Syy * iN);
-  const F2 C02 = r * fma2(neg2(mxc), mh, SXH * iN);
-  const F2 C12 = r * fma2(neg2(myc), mh, SYH * iN);
-  const F2 C22 = fma2(neg2(mh), mh, S2 * iN);
-  // mean footprint height: tile plane at the footprint centroid + mean h^
-  const F2 zz = fma2(bc(gx), mxc, fma2(bc(gy), myc, zref + mh));
-  return solve2<true>(C00, C01, C11, C02, C12, C22, mxc * r, myc * r, zz, okl, okh, gx / p.r, gy / p.r, csk, p);
+  const F2 r2n = bc(r * r) * (iN * iN);
+  Cov2 c;
+  c.c00 = r2n * pk(sl.a, sh.a);
+  c.c01 = r2n * pk(sl.c, sh.c);
+  c.c11 = r2n * pk(sl.b, sh.b);
+  const F2 B02 = fma2(neg2(mxc), mh, SXH * iN), B12 = fma2(neg2(myc), mh, SYH * iN);  // (cell, m)
+  const F2 B22 = fma2(neg2(mh), mh, S2 * iN);
+  const F2 A00 = c.c00 * bc(1.f / (r * r)), A01 = c.c01 * bc(1.f / (r * r)), A11 = c.c11 * bc(1.f / (r * r));
+  const F2 A02 = fma2(bc(gx), A00, fma2(bc(gy), A01, B02));
+  const F2 A12 = fma2(bc(gx), A01, fma2(bc(gy), A11, B12));
+  c.c22 = fma2(bc(gx), B02 + A02, fma2(bc(gy), B12 + A12, B22));
+  c.c02 = A02 * bc(r);
+  c.c12 = A12 * bc(r);
+  c.mx = mxc * bc(r);
+  c.my = myc * bc(r);
+  c.zz = fma2(bc(gx), mxc, fma2(bc(gy), myc, zref + mh));  // tile plane at the centroid + mean h^
+  return c;
 }
+// One state in FP64 (footprints with few known cells, see kDirectN): the same steps as solve2 — trace
+// normalisation, adj(M) eigenvector (best-conditioned column) for the FP32 trigonometric lam0, refined
+// by Rayleigh-quotient iteration in FP64, Eqs. 2-3 angles (libdevice asin), risk and thresholds.
+// C: covariance in metres (c00, c01, c11, c02, c12, c22); (mx, my): centroid offset (m); zz: mean height.
+struct StateOut1 {
+  float risk, pitch, roll, z;
+  unsigned trav;
+};
+__device__ __noinline__ StateOut1 solve1_fp64(double C00, double C01, double C11, double C02, double C12,
+                                              double C22, double mx, double my, double zz, float2 csk,
+                                              float4 thr, float3 w) {
+  const double it = 1.0 / (C00 + C11 + C22);
+  const double c00 = C00 * it, c01 = C01 * it, c11 = C11 * it, c02 = C02 * it, c12 = C12 * it, c22 = C22 * it;
+  // seed shift: the FP32 trigonometric lam0 (accurate to ~1e-6 of the trace; the adj(M) column below is
+  // then dominated by the smallest eigenvector, and the Rayleigh-quotient iterations converge to it)
+  const float f00 = (float)c00 - 1.f / 3.f, f11 = (float)c11 - 1.f / 3.f, f22 = (float)c22 - 1.f / 3.f;
+  const float f01 = (float)c01, f02 = (float)c02, f12 = (float)c12;
+  const float fp2 = (f00 * f00 + f11 * f11 + f22 * f22 + 2.f * (f01 * f01 + f02 * f02 + f12 * f12)) * (1.f / 6.f);
+  const float fip = rsqrtf(fp2), fpp = fp2 * fip;
+  const float g00 = f00 * fip, g11 = f11 * fip, g22 = f22 * fip, h01 = f01 * fip, h02 = f02 * fip, h12 = f12 * fip;
+  const float fhr = 0.5f * (g00 * (g11 * g22 - h12 * h12) - h01 * (h01 * g22 - h12 * h02) +
+                            h02 * (h01 * h12 - g11 * h02));
+  const float fphi = lo(acos2(bc(fminf(1.f, fmaxf(-1.f, fhr))))) * (1.f / 3.f);
+  float fs, fc;
+  __sincosf(fphi, &fs, &fc);
+  const double lam0 = (double)(1.f / 3.f - fpp * fmaf(1.73205080756887729f, fs, fc));
+  double m00 = c00 - lam0, m11 = c11 - lam0, m22 = c22 - lam0;
+  // adj(M) columns r1 x r2, r2 x r0, r0 x r1: the longest one
+  double v0 = c01 * c12 - c02 * m11, v1 = c02 * c01 - m00 * c12, v2 = m00 * m11 - c01 * c01;  // r0 x r1
+  const double u0 = c01 * m22 - c02 * c12, u1 = c02 * c02 - m00 * m22, u2 = m00 * c12 - c01 * c02;  // r0 x r2
+  const double w0 = m11 * m22 - c12 * c12, w1 = c12 * c02 - c01 * m22, w2 = c01 * c12 - m11 * c02;  // r1 x r2
+  double nv = v0 * v0 + v1 * v1 + v2 * v2;
+  const double nu = u0 * u0 + u1 * u1 + u2 * u2, nw = w0 * w0 + w1 * w1 + w2 * w2;
+  if (nu > nv) { v0 = u0; v1 = u1; v2 = u2; nv = nu; }
+  if (nw > nv) { v0 = w0; v1 = w1; v2 = w2; nv = nw; }
+  double s = rsqrt(nv);
+  double n0 = v0 * s, n1 = v1 * s, n2 = v2 * s;
+  for (int iter = 0; iter < 3; ++iter) {  // Rayleigh-quotient iteration (cubic convergence)
+    const double rho = n0 * (c00 * n0 + c01 * n1 + c02 * n2) + n1 * (c01 * n0 + c11 * n1 + c12 * n2) +
+                       n2 * (c02 * n0 + c12 * n1 + c22 * n2);
+    m00 = c00 - rho; m11 = c11 - rho; m22 = c22 - rho;
+    const double A00 = m11 * m22 - c12 * c12, A11 = m00 * m22 - c02 * c02, A22 = m00 * m11 - c01 * c01;
+    const double A01 = c02 * c12 - c01 * m22, A02 = c01 * c12 - c02 * m11, A12 = c01 * c02 - m00 * c12;
+    const double y0 = A00 * n0 + A01 * n1 + A02 * n2, y1 = A01 * n0 + A11 * n1 + A12 * n2,
+                 y2 = A02 * n0 + A12 * n1 + A22 * n2;
+    const double yy = y0 * y0 + y1 * y1 + y2 * y2;
+    if (!(yy > 1e-280)) break;
+    s = rsqrt(yy);
+    n0 = y0 * s; n1 = y1 * s; n2 = y2 * s;
+  }
+  if (n2 < 0.0) { n0 = -n0; n1 = -n1; n2 = -n2; }  // z_b in S^2_+ 
+  const double rq = n0 * (c00 * n0 + c01 * n1 + c02 * n2) + n1 * (c01 * n0 + c11 * n1 + c12 * n2) +
+                    n2 * (c02 * n0 + c12 * n1 + c22 * n2);
+  const double kap = fmax(0.0, rq);
+  const double cs = csk.x, sn = csk.y;
+  const double u = n0 * cs + n1 * sn, t = n0 * sn - n1 * cs;
+  const double rs = rsqrt(n2 * n2 + t * t);
+  const double pitch = asin(-(n2 * u) * rs), roll = asin(t * rs);
+  const double ax = fabs(pitch), ay = fabs(roll);
+  StateOut1 o;
+  const bool valid = n2 > 0.0;  // NaN fails: unknown (reading R11)
+  const bool exceed = kap > thr.x || ax > thr.y || ay > thr.z;  // (kappa_max, phi_x_max, phi_y_max)
+  o.risk = (valid && !exceed) ? (float)(w.x * kap + w.y * ax + w.z * ay) : 1.f;
+  o.pitch = valid ? (float)pitch : __int_as_float(0x7fc00000);
+  o.roll = valid ? (float)roll : __int_as_float(0x7fc00000);
+  o.z = valid ? (float)(zz + (n0 * mx + n1 * my) / n2) : __int_as_float(0x7fc00000);
+  o.trav = (valid && !exceed) ? 1u : 0u;
+  return o;
+}
+
+// Footprints with few known cells (N < kDirectN): the prefix differences of the h^ moments cancel too
+// much there (a handful of cells out of a full halo row), so those moments are recomputed directly from
+// the tile's heights, shifted by the mean estimate m0 (a two-pass variance): exact up to FP32 rounding of
+// the small deviations.
+constexpr float kDirectN = 32.f;
 
 // ------------------------------------------------------------------------------------------
 // The assess kernel.
@@ -267,12 +358,12 @@ struct Geom {
   static constexpr int PW = HX + 1;          // prefix row length (exclusive prefix, entry 0 = 0)
   static constexpr int NR = 2 * R_T + 1;     // stencil rows
   static constexpr int CPL = (HX + 31) / 32;  // halo cells per lane in the row scan
+  static constexpr size_t E = (size_t)HY * PW;  // prefix entries
   static constexpr size_t raw_bytes = ((size_t)HX * HY * 4 + 127) / 128 * 128;
-  static constexpr size_t p02_off = raw_bytes;                              // float2 {P0, P2}
-  static constexpr size_t px_off = p02_off + (size_t)HY * PW * 8;           // float  PX
-  static constexpr size_t pv_off = px_off + (size_t)HY * PW * 4;            // float2 {PV, PVX}
-  static constexpr size_t pvxx_off = pv_off + (size_t)HY * PW * 8;          // float  PVXX
-  static constexpr size_t misc_off = (pvxx_off + (size_t)HY * PW * 4 + 15) / 16 * 16;
+  // float2 {P0, P2} | float PX | float2 {PV, PVX} | float PVXX (the last two: border / unknown tiles only)
+  static constexpr size_t p02_off = raw_bytes, px_off = p02_off + 8 * E;
+  static constexpr size_t pv_off = px_off + 4 * E, pvxx_off = pv_off + 8 * E;
+  static constexpr size_t misc_off = (pvxx_off + 4 * E + 15) / 16 * 16;
   static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
   static size_t bytes(int tab_cap) { return runs_off + (size_t)tab_cap * 16; }
 };
@@ -294,7 +385,12 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx_rel = (int)(blockIdx.x % (unsigned)p.tiles_x);
-  const int ty_rel = p.row_first + (int)(blockIdx.x / (unsigned)p.tiles_x) * p.row_mod;
+  // grid rows in the order [last, 0, 1, ..., last - 1]: the window's bottom and top tile rows (border
+  // tiles: the slower general path) are scheduled in the first wave instead of forming the tail
+  const int n_gr = (int)(gridDim.x / (unsigned)p.tiles_x);
+  int gr = (int)(blockIdx.x / (unsigned)p.tiles_x) - 1;
+  if (gr < 0) gr = n_gr - 1;
+  const int ty_rel = p.row_first + gr * p.row_mod;
   if (p.n_rects) {  // INCREMENTAL: only tiles that hold a state within R of a changed cell (CTA-uniform exit)
     bool hit = false;
     for (int q = 0; q < p.n_rects; ++q)
@@ -434,22 +530,22 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
-    float e[CPL], e2[CPL], ex[CPL], vv[CPL], vx[CPL], vxx[CPL];
-    float s0 = 0.f, s2 = 0.f, sx = 0.f, sv = 0.f, svx = 0.f, svxx = 0.f;
+    float hh[CPL], xp[CPL], vv[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const int col = lane * CPL + c;
-      float hv = (col < HX) ? raw[row * HX + col] : __int_as_float(0x7fc00000);
+      const float hv = (col < HX) ? raw[row * HX + col] : __int_as_float(0x7fc00000);
       const bool ok = !isnan(hv);
-      const float xp = (float)col - XC;
-      const float hh = ok ? (hv - href) - fmaf(pgx, xp, fmaf(pgy, (float)row - YC, pc)) : 0.f;
-      s0 += hh; s2 = fmaf(hh, hh, s2); sx = fmaf(xp, hh, sx);
+      xp[c] = (float)col - XC;
+      hh[c] = ok ? (hv - href) - fmaf(pgx, xp[c], fmaf(pgy, (float)row - YC, pc)) : 0.f;
+      vv[c] = ok ? 1.f : 0.f;
+    }
+    float e[CPL], e2[CPL], ex[CPL];
+    float s0 = 0.f, s2 = 0.f, sx = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      s0 += hh[c]; s2 = fmaf(hh[c], hh[c], s2); sx = fmaf(xp[c], hh[c], sx);
       e[c] = s0; e2[c] = s2; ex[c] = sx;
-      if (!fast) {
-        const float v = ok ? 1.f : 0.f;
-        sv += v; svx = fmaf(xp, v, svx); svxx = fmaf(xp * xp, v, svxx);
-        vv[c] = sv; vx[c] = svx; vxx[c] = svxx;
-      }
     }
     const float o0 = warp_incl_scan(s0, lane) - s0;
     const float o2 = warp_incl_scan(s2, lane) - s2;
@@ -462,7 +558,14 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const int col = lane * CPL + c;
       if (col < HX) { P02r[col + 1] = make_float2(o0 + e[c], o2 + e2[c]); PXr[col + 1] = ox + ex[c]; }
     }
-    if (!fast) {
+    if (!fast) {  // validity moments (exact integers in float)
+      float vs[CPL], vx[CPL], vxx[CPL];
+      float sv = 0.f, svx = 0.f, svxx = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        sv += vv[c]; svx = fmaf(xp[c], vv[c], svx); svxx = fmaf(xp[c] * xp[c], vv[c], svxx);
+        vs[c] = sv; vx[c] = svx; vxx[c] = svxx;
+      }
       const float ov = warp_incl_scan(sv, lane) - sv;
       const float ovx = warp_incl_scan(svx, lane) - svx;
       const float ovxx = warp_incl_scan(svxx, lane) - svxx;
@@ -472,7 +575,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         const int col = lane * CPL + c;
-        if (col < HX) { PVr[col + 1] = make_float2(ov + vv[c], ovx + vx[c]); PVXXr[col + 1] = ovxx + vxx[c]; }
+        if (col < HX) { PVr[col + 1] = make_float2(ov + vs[c], ovx + vx[c]); PVXXr[col + 1] = ovxx + vxx[c]; }
       }
     }
   }
@@ -607,17 +710,86 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
             Sxy[s] = fmaf(dj, sdi, Sxy[s]);
           }
         }
-        const StateOut2 o = epilogue2_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), pk(Sxx[0], Sxx[1]),
-                                              pk(Sxy[0], Sxy[1]), pk(Syy[0], Syy[1]), pk(S02[0].x, S02[1].x),
-                                              pk(S02[0].y, S02[1].y), pk(SXH[0], SXH[1]), pk(SYH[0], SYH[1]),
-                                              pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)),
-                                              pgx, pgy, csk, p);
+        const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
+        const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
+        Cov2 cv = cov_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), shl, shh, pk(S02[0].x, S02[1].x),
+                              pk(S02[0].y, S02[1].y), pk(SXH[0], SXH[1]), pk(SYH[0], SYH[1]),
+                              pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
         int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
 #pragma unroll
         for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
           if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
-        store(so0, st0, lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
-        store(so1, st1, hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+        // (states outside the window are not stored: they never take the direct path)
+        const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
+        const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
+        StateOut1 dres[2];
+        if (need0 | need1) {
+          // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
+          // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
+          const float m0[2] = {lo(cv.zz), hi(cv.zz)};
+          float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            unsigned msk = s ? need1 : need0;
+            while (msk) {
+              const int src = __ffs(msk) - 1;
+              msk &= msk - 1;
+              const float mu = __shfl_sync(0xffffffffu, m0[s], src);
+              const float* rb = raw + (warp + (sp + s) * NWARPS) * HX + src;  // state's halo row, column src
+              float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
+#pragma unroll 1
+              for (int d = 0; d < nr; ++d) {
+                const int4 o = rk[d];
+                const float dj = __int_as_float(o.w);
+                const int dr = (int)dj + R_T;  // stencil row -> halo row offset
+                const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
+                for (int c = c0 + lane; c < c1; c += 32) {
+                  const float hv = rb[dr * HX + c];
+                  if (!isnan(hv)) {
+                    const float dv = hv - mu;
+                    a0 += dv;
+                    a2 = fmaf(dv, dv, a2);
+                    ax = fmaf((float)(c - R_T), dv, ax);
+                    ay = fmaf(dj, dv, ay);
+                  }
+                }
+              }
+#pragma unroll
+              for (int w = 16; w >= 1; w >>= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, w);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, w);
+                ax += __shfl_xor_sync(0xffffffffu, ax, w);
+                ay += __shfl_xor_sync(0xffffffffu, ay, w);
+              }
+              if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
+            }
+          }
+          // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (s ? dh : dl) {
+              const double dN = N[s], iN = 1.0 / dN, r = p.r;
+              const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
+              const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
+                           c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
+              const double r2n = r * r * iN * iN;
+              dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
+                                    r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
+                                    (double)m0[s] + md, csk,
+                                    make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
+                                    make_float3(p.wk, p.wx, p.wy));
+            }
+          }
+        }
+        const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
+                                         shh.ok, 0.f, 0.f, csk, p);
+        // (store() holds a warp ballot: select first, store uniformly)
+        StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
+        StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
+        if (dl) ra = dres[0];
+        if (dh) rb = dres[1];
+        store(so0, st0, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
+        store(so1, st1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
       }
     }
   }
@@ -672,8 +844,9 @@ cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt,
   return cudaGetLastError();
 }
 
-__global__ void scatter_rect_kernel(float* h, int ldh, int nx, int ny, int px0, int py0, int w, int hgt,
-                                    const float* __restrict__ src, long long ld, const uint8_t* __restrict__ known) {
+__global__ void scatter_rect_kernel(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
+                                    int w, int hgt, const float* __restrict__ src, long long ld,
+                                    const uint8_t* __restrict__ known) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= w || j >= hgt) return;
@@ -683,13 +856,14 @@ __global__ void scatter_rect_kernel(float* h, int ldh, int nx, int ny, int px0, 
   float v = src[si];
   if (known && !known[si]) v = __int_as_float(0x7fc00000);
   h[(size_t)py * ldh + px] = v;
+  if (var) var[(size_t)py * ldh + px] = prior_var;
 }
 
-cudaError_t launch_scatter_rect(float* h, int ldh, int nx, int ny, int px0, int py0, int w, int hgt, const float* src,
-                                long long ld, const uint8_t* known, cudaStream_t s) {
+cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0, int w,
+                                int hgt, const float* src, long long ld, const uint8_t* known, cudaStream_t s) {
   if (w <= 0 || hgt <= 0) return cudaSuccess;
   dim3 grid((w + 255) / 256, hgt);
-  scatter_rect_kernel<<<grid, 256, 0, s>>>(h, ldh, nx, ny, px0, py0, w, hgt, src, ld, known);
+  scatter_rect_kernel<<<grid, 256, 0, s>>>(h, var, prior_var, ldh, nx, ny, px0, py0, w, hgt, src, ld, known);
   return cudaGetLastError();
 }
 

@@ -75,8 +75,8 @@ cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUt
 // Small helpers (same file as the kernels).
 cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt, int nx, int ny,
                               cudaStream_t s);
-cudaError_t launch_scatter_rect(float* h, int ldh, int nx, int ny, int px0, int py0, int w, int hgt,
-                                const float* src, long long ld, const uint8_t* known, cudaStream_t s);
+cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
+                                int w, int hgt, const float* src, long long ld, const uint8_t* known, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
 cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
@@ -93,6 +93,30 @@ struct QueryGeo {
 // nearest state (H10): out 5 x n (risk, pitch, roll, z, trav); *n_out += queries outside / not owned
 cudaError_t launch_query(const AssessParams& p, const QueryGeo& g, int n, const double* xyt, float* out, int* n_out,
                          cudaStream_t s);
+
+// ---- NEXT-1: elevation front-end (frontend.cu) -----------------------------------------------------
+struct FePose {
+  double R_B[9], p_B[3], R_BS[9], p_BS[3], Sigma_S[9], Sigma_R[9], Sigma_B[9];  // row-major 3x3
+};
+struct FrontendArgs {
+  FePose pose;
+  double r, z_min, z_max, gate, ray_eps;
+  double sx, sy, sz;     // LiDAR position in the world, R_B p_BS + p_B (host, fixed order)
+  long long I_M, J_M;
+  int nx, ny, ldh, pxM, pyM;
+};
+struct FrontendScratch {
+  int *key, *idx, *skey, *sidx;
+  double4* meas;         // (x, y, z_l, sigma^2) per point
+  int* counts;           // [5]: used, outside the map, outside the height band, bad variance, ray resets
+  int* bbox;             // [4]: logical i_min, i_max, j_min, j_max of the cells touched
+  void* temp;
+  size_t temp_bytes;
+  size_t cap;
+};
+cudaError_t frontend_run(const FrontendArgs& a, int n, const float* pts, FrontendScratch& s, float* h, float* var,
+                         cudaStream_t st);
+size_t frontend_temp_bytes(int n);
 
 // ---- NEXT-2: signed distance field of the Risk = 1 set per yaw layer (sdf.cu) ----------------------
 struct SdfParams {

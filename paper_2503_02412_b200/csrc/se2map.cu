@@ -48,6 +48,10 @@ struct se2m_map {
   float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
   float* d_sdf = nullptr;    // NEXT-2: SDF layers (representative bins), ring layout
+  float* d_var = nullptr;    // NEXT-1: cell height variance, ring layout like d_h
+  FrontendScratch fe{};
+  float* d_pts = nullptr;
+  size_t pts_cap = 0;
   bool sdf_valid = false;
   double sdf_dmax = 0;
   int4* d_full = nullptr;   // run-entry tables (see AssessParams)
@@ -266,6 +270,7 @@ extern "C" void se2m_default_params(se2m_params* p) {
   p->w_r[0] = 0.4; p->w_r[1] = 0.3; p->w_r[2] = 0.3;
   p->kappa_max = 0.1; p->phi_x_max = 0.52; p->phi_y_max = 0.52;
   p->world_size = 1;
+  p->fe_z_min = -1.5; p->fe_z_max = 1.5; p->fe_gate = 2.0; p->fe_ray_eps = 0.05; p->fe_prior_var = 1e-4;
 }
 
 static se2m_status validate(const se2m_params* p) {
@@ -280,6 +285,9 @@ static se2m_status validate(const se2m_params* p) {
   if (!isfinite(p->robot_x) || !isfinite(p->robot_y)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "robot position must be finite");
   if (p->world_size < 1 || p->rank < 0 || p->rank >= p->world_size) return fail(nullptr, SE2M_ERR_INVALID_ARG, "need 0 <= rank < world_size");
   if (p->shard_mode < 0 || p->shard_mode > 2) return fail(nullptr, SE2M_ERR_INVALID_ARG, "shard_mode must be 0, 1 or 2");
+  const bool fe_unset = p->fe_z_min == 0 && p->fe_z_max == 0 && p->fe_gate == 0 && p->fe_ray_eps == 0 && p->fe_prior_var == 0;
+  if (!fe_unset && (!(p->fe_z_min < p->fe_z_max) || !(p->fe_gate > 0) || !(p->fe_ray_eps >= 0) || !(p->fe_prior_var > 0)))
+    return fail(nullptr, SE2M_ERR_INVALID_ARG, "front-end params: need z_min < z_max, gate > 0, ray_eps >= 0, prior_var > 0");
   if (p->ellipse_ex / p->resolution > 32 || p->ellipse_ey / p->resolution > 32)
     return fail(nullptr, SE2M_ERR_UNSUPPORTED, "footprint radius > 32 cells is not built into this library");
   return SE2M_OK;
@@ -318,6 +326,11 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   se2m_map* m = new (std::nothrow) se2m_map();
   if (!m) return fail(nullptr, SE2M_ERR_OOM, "host allocation failed");
   m->prm = *p;
+  if (m->prm.fe_z_min == 0 && m->prm.fe_z_max == 0 && m->prm.fe_gate == 0 && m->prm.fe_ray_eps == 0 &&
+      m->prm.fe_prior_var == 0) {  // front-end block left zero: the documented defaults
+    m->prm.fe_z_min = -1.5; m->prm.fe_z_max = 1.5; m->prm.fe_gate = 2.0; m->prm.fe_ray_eps = 0.05;
+    m->prm.fe_prior_var = 1e-4;
+  }
   auto bail = [&](se2m_status s) {
     g_init_error = m->err;
     se2m_destroy(m);
@@ -362,6 +375,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   const size_t nst = plane * n;
   struct { void** ptr; size_t bytes; const char* what; } allocs[] = {
       {(void**)&m->d_h, (size_t)m->ldh * p->ny * 4, "heights"},
+      {(void**)&m->d_var, (size_t)m->ldh * p->ny * 4, "variances"},
       {(void**)&m->d_out, nst * sizeof(float4), "state records"},
       {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
       {(void**)&m->d_full, std::max<size_t>(1, full.size()) * sizeof(int4), "full table"},
@@ -387,6 +401,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       (e = cudaMemcpyAsync(m->d_geoc, geoc.data(), geoc.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemsetAsync(m->d_h, 0xff, (size_t)m->ldh * p->ny * 4, m->stream)) ||  // 0xffffffff = NaN: unknown
+      (e = cudaMemsetAsync(m->d_var, 0, (size_t)m->ldh * p->ny * 4, m->stream)) ||
       (e = cudaMemsetAsync(m->d_trav, 0, (size_t)n * p->ny * m->trav_words * 4, m->stream)) ||
       (e = cudaStreamSynchronize(m->stream))) {
     cuda_fail(m, e, "init upload");
@@ -400,7 +415,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
-  void* ptrs[] = {m->d_sdf, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
+  void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
+                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -434,7 +450,8 @@ extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0
     sld = w;
   }
   const int px0 = pmod(m->I_M + i0, m->prm.nx), py0 = pmod(m->J_M + j0, m->prm.ny);
-  CUDA_TRY(m, launch_scatter_rect(m->d_h, m->ldh, m->prm.nx, m->prm.ny, px0, py0, w, h, src, sld, kn, m->stream), "scatter");
+  CUDA_TRY(m, launch_scatter_rect(m->d_h, m->d_var, (float)m->prm.fe_prior_var, m->ldh, m->prm.nx, m->prm.ny, px0, py0,
+                                  w, h, src, sld, kn, m->stream), "scatter");
   m->launches++;
   m->have_data = true;
   m->dirty.push_back(Rect{m->I_M + i0, m->I_M + i0 + w, m->J_M + j0, m->J_M + j0 + h});
@@ -532,12 +549,14 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   }
   const int grid_rows = tiles_y > p.row_first ? (tiles_y - p.row_first + p.row_mod - 1) / p.row_mod : 0;
   const int n_tiles = p.tiles_x * grid_rows;
-  // yaw chunking: enough CTAs for >= 4 waves of 148 SMs, otherwise all bins per CTA (tile reuse)
+  // yaw chunking: all bins per CTA (tile reuse) unless that leaves SMs idle; then split the bins so the
+  // CTAs fill one wave (2 resident CTAs on each of the 148 SMs) — each CTA pays the tile load, plane fit
+  // and prefix build once, so more, shorter CTAs than that only add fixed cost
   const int nk = m->k_hi - m->k_lo;
   int chunk = nk;
   if (n_tiles > 0) {
-    const long long want = 4LL * 148;
-    chunk = (int)std::max<long long>(1, std::min<long long>(nk, (long long)n_tiles * nk / want));
+    const long long slots = 2LL * 148;
+    chunk = (int)std::max<long long>(1, std::min<long long>(nk, ((long long)n_tiles * nk + slots - 1) / slots));
   }
   chunk = std::max(1, chunk);
   if (m->period > 1) chunk = std::min(nk, (chunk + m->period - 1) / m->period * m->period);  // chain-aligned
@@ -715,6 +734,109 @@ extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint
     if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->stream), "D2H bits");
   }
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_compact)");
+  return SE2M_OK;
+}
+
+// ---- NEXT-1: LiDAR frame integration --------------------------------------------------------------------
+extern "C" se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int64_t n, const se2m_pose* pose,
+                                           int32_t mem, int64_t* out_counts) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (n < 0 || n > (1ll << 30) || (n > 0 && !points) || !pose || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(m, SE2M_ERR_INVALID_ARG, "integrate_scan: bad arguments");
+  if (out_counts) memset(out_counts, 0, 5 * sizeof(int64_t));
+  if (n == 0) return SE2M_OK;
+  FrontendScratch& s = m->fe;
+  if ((size_t)n > s.cap) {
+    cudaStreamSynchronize(m->stream);
+    void* old[] = {s.key, s.idx, s.skey, s.sidx, s.meas, s.temp, m->d_pts};
+    for (void* q : old) if (q) cudaFree(q);
+    s.key = s.idx = s.skey = s.sidx = nullptr; s.meas = nullptr; s.temp = nullptr; m->d_pts = nullptr;
+    s.cap = 0;
+    s.temp_bytes = frontend_temp_bytes((int)n);
+    CUDA_TRY(m, cudaMalloc(&s.key, n * sizeof(int)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&s.idx, n * sizeof(int)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&s.skey, n * sizeof(int)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&s.sidx, n * sizeof(int)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&s.meas, n * sizeof(double4)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&s.temp, std::max<size_t>(s.temp_bytes, 16)), "cudaMalloc(fe)");
+    CUDA_TRY(m, cudaMalloc(&m->d_pts, n * 3 * sizeof(float)), "cudaMalloc(fe)");
+    s.cap = (size_t)n;
+  }
+  if (!s.counts) CUDA_TRY(m, cudaMalloc(&s.counts, 5 * sizeof(int)), "cudaMalloc(fe)");
+  if (!s.bbox) CUDA_TRY(m, cudaMalloc(&s.bbox, 4 * sizeof(int)), "cudaMalloc(fe)");
+  const float* pts = points;
+  if (mem == SE2M_MEM_HOST) {
+    CUDA_TRY(m, cudaMemcpyAsync(m->d_pts, points, n * 3 * sizeof(float), cudaMemcpyHostToDevice, m->stream), "H2D points");
+    pts = m->d_pts;
+  }
+  const int bbox0[4] = {INT32_MAX, -1, INT32_MAX, -1};
+  CUDA_TRY(m, cudaMemsetAsync(s.counts, 0, 5 * sizeof(int), m->stream), "fe counts");
+  CUDA_TRY(m, cudaMemcpyAsync(s.bbox, bbox0, sizeof bbox0, cudaMemcpyHostToDevice, m->stream), "fe bbox");
+  FrontendArgs a;
+  memset(&a, 0, sizeof a);
+  memcpy(a.pose.R_B, pose->R_B, sizeof a.pose.R_B); memcpy(a.pose.p_B, pose->p_B, sizeof a.pose.p_B);
+  memcpy(a.pose.R_BS, pose->R_BS, sizeof a.pose.R_BS); memcpy(a.pose.p_BS, pose->p_BS, sizeof a.pose.p_BS);
+  memcpy(a.pose.Sigma_S, pose->Sigma_S, sizeof a.pose.Sigma_S);
+  memcpy(a.pose.Sigma_R, pose->Sigma_R, sizeof a.pose.Sigma_R);
+  memcpy(a.pose.Sigma_B, pose->Sigma_B, sizeof a.pose.Sigma_B);
+  a.r = m->prm.resolution; a.z_min = m->prm.fe_z_min; a.z_max = m->prm.fe_z_max;
+  a.gate = m->prm.fe_gate; a.ray_eps = m->prm.fe_ray_eps;
+  const double* RB = pose->R_B;
+  const double* pbs = pose->p_BS;
+  a.sx = (RB[0] * pbs[0] + RB[1] * pbs[1] + RB[2] * pbs[2]) + pose->p_B[0];  // R_B p_BS + p_B, left to right
+  a.sy = (RB[3] * pbs[0] + RB[4] * pbs[1] + RB[5] * pbs[2]) + pose->p_B[1];
+  a.sz = (RB[6] * pbs[0] + RB[7] * pbs[1] + RB[8] * pbs[2]) + pose->p_B[2];
+  a.I_M = m->I_M; a.J_M = m->J_M;
+  a.nx = m->prm.nx; a.ny = m->prm.ny; a.ldh = m->ldh;
+  a.pxM = pmod(m->I_M, m->prm.nx); a.pyM = pmod(m->J_M, m->prm.ny);
+  CUDA_TRY(m, frontend_run(a, (int)n, pts, s, m->d_h, m->d_var, m->stream), "front-end kernels");
+  m->launches += 3;
+  int cnt[5], bb[4];
+  CUDA_TRY(m, cudaMemcpyAsync(cnt, s.counts, sizeof cnt, cudaMemcpyDeviceToHost, m->stream), "D2H fe");
+  CUDA_TRY(m, cudaMemcpyAsync(bb, s.bbox, sizeof bb, cudaMemcpyDeviceToHost, m->stream), "D2H fe");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(fe)");
+  if (out_counts)
+    for (int i = 0; i < 5; ++i) out_counts[i] = cnt[i];
+  if (bb[1] >= 0) {  // touched cells -> dirty (H9)
+    m->dirty.push_back(Rect{m->I_M + bb[0], m->I_M + bb[1] + 1, m->J_M + bb[2], m->J_M + bb[3] + 1});
+    m->have_data = true;
+  }
+  return SE2M_OK;
+}
+
+static se2m_status ring_to_logical(se2m_map* m, const float* ring, float* dst_dev) {
+  // the ring (pitch ldh) in logical order (pitch nx): one 2-D copy per quadrant of the seam
+  const int nx = m->prm.nx, ny = m->prm.ny, pxM = pmod(m->I_M, nx), pyM = pmod(m->J_M, ny);
+  const int xs[2][3] = {{0, pxM, nx - pxM}, {nx - pxM, 0, pxM}};  // (logical x0, physical x0, width)
+  const int ys[2][3] = {{0, pyM, ny - pyM}, {ny - pyM, 0, pyM}};
+  for (auto& X : xs)
+    for (auto& Y : ys)
+      if (X[2] > 0 && Y[2] > 0)
+        CUDA_TRY(m, cudaMemcpy2DAsync(dst_dev + (size_t)Y[0] * nx + X[0], (size_t)nx * 4,
+                                      ring + (size_t)Y[1] * m->ldh + X[1], (size_t)m->ldh * 4, (size_t)X[2] * 4, Y[2],
+                                      cudaMemcpyDeviceToDevice, m->stream), "ring gather");
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_download_elevation(se2m_map* m, float* heights, float* variances, int32_t mem) {
+  if (!m || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE)) return SE2M_ERR_INVALID_ARG;
+  const size_t cells = (size_t)m->prm.nx * m->prm.ny;
+  const float* rings[2] = {m->d_h, m->d_var};
+  float* outs[2] = {heights, variances};
+  for (int q = 0; q < 2; ++q) {
+    if (!outs[q]) continue;
+    float* target = outs[q];
+    if (mem == SE2M_MEM_HOST) {
+      se2m_status st = ensure_stage(m, cells * 4);
+      if (st != SE2M_OK) return st;
+      target = m->d_stage;
+    }
+    se2m_status st = ring_to_logical(m, rings[q], target);
+    if (st != SE2M_OK) return st;
+    if (mem == SE2M_MEM_HOST)
+      CUDA_TRY(m, cudaMemcpyAsync(outs[q], target, cells * 4, cudaMemcpyDeviceToHost, m->stream), "D2H elevation");
+    CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_elevation)");
+  }
   return SE2M_OK;
 }
 

@@ -30,7 +30,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
-           "se2m_query_trilinear"]
+           "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation"]
 
 
 class Params(ctypes.Structure):
@@ -41,7 +41,25 @@ class Params(ctypes.Structure):
                 ("phi_x_max", ctypes.c_double), ("phi_y_max", ctypes.c_double),
                 ("robot_x", ctypes.c_double), ("robot_y", ctypes.c_double),
                 ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p)]
+                ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
+                ("fe_z_min", ctypes.c_double), ("fe_z_max", ctypes.c_double), ("fe_gate", ctypes.c_double),
+                ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double)]
+
+
+class Pose(ctypes.Structure):
+    """se2m_pose: row-major 3x3 rotations / covariances (NEXT-1 front-end)."""
+    _fields_ = [("R_B", ctypes.c_double * 9), ("p_B", ctypes.c_double * 3), ("R_BS", ctypes.c_double * 9),
+                ("p_BS", ctypes.c_double * 3), ("Sigma_S", ctypes.c_double * 9), ("Sigma_R", ctypes.c_double * 9),
+                ("Sigma_B", ctypes.c_double * 9)]
+
+    @classmethod
+    def from_arrays(cls, R_B, p_B, R_BS, p_BS, Sigma_S, Sigma_R, Sigma_B):
+        q = cls()
+        for name, v in (("R_B", R_B), ("p_B", p_B), ("R_BS", R_BS), ("p_BS", p_BS), ("Sigma_S", Sigma_S),
+                        ("Sigma_R", Sigma_R), ("Sigma_B", Sigma_B)):
+            flat = np.ascontiguousarray(v, dtype=np.float64).ravel()
+            setattr(q, name, (ctypes.c_double * len(flat))(*flat))
+        return q
 
 
 _lib = ctypes.CDLL(_LIB_PATH)
@@ -64,6 +82,8 @@ _lib.se2m_compute_sdf.argtypes = [_vp, _f64]
 _lib.se2m_download_sdf.argtypes = [_vp, _vp, _i32]
 _lib.se2m_sdf_from_mask.argtypes = [_vp, _i32, _i32, _i32, _f64, _f64, _vp, _i32, _i32]
 _lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
+_lib.se2m_integrate_scan.argtypes = [_vp, _vp, _i64, ctypes.POINTER(Pose), _i32, _vp]
+_lib.se2m_download_elevation.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_launch_count.argtypes = [_vp]
@@ -73,7 +93,8 @@ _lib.se2m_last_error.restype = ctypes.c_char_p
 for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_assess_se2", "se2m_query",
               "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info",
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
-              "se2m_sdf_from_mask", "se2m_query_trilinear"):
+              "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
+              "se2m_download_elevation"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -278,6 +299,27 @@ class Se2Map:
         st = _lib.se2m_query_trilinear(self.h, n, xyt.ctypes.data, field, v.ctypes.data, g.ctypes.data)
         self._check(st, ok=(SE2M_OK, SE2M_ERR_OUT_OF_RANGE))
         return v, g, st
+
+    def integrate_scan(self, points, pose: Pose):
+        """NEXT-1: one LiDAR frame (points (n, 3) float32 sensor frame: NumPy host or CUDA tensor).
+        Returns counts (used, outside map, outside band, bad variance, ray-reset events)."""
+        if hasattr(points, "is_cuda"):
+            pp, mem, keep = _ptr_nocopy(points)
+            n = points.shape[0]
+        else:
+            points = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+            pp, mem, keep = points.ctypes.data, SE2M_MEM_HOST, points
+            n = len(points)
+        cnt = np.zeros(5, np.int64)
+        self._check(_lib.se2m_integrate_scan(self.h, pp, n, ctypes.byref(pose), mem, cnt.ctypes.data))
+        return cnt
+
+    def download_elevation(self):
+        P = self.params
+        h = np.empty((P.ny, P.nx), np.float32)
+        v = np.empty((P.ny, P.nx), np.float32)
+        self._check(_lib.se2m_download_elevation(self.h, h.ctypes.data, v.ctypes.data, SE2M_MEM_HOST))
+        return h, v
 
     def origin(self):
         I, J = _i64(), _i64()

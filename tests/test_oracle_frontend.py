@@ -55,7 +55,7 @@ def test_variance_matches_monte_carlo():
 
 def _window(nx=12, ny=10, r=0.1):
     w = oracle.Window(nx, ny, r, 0.55, 0.55)
-    return w, np.zeros((ny, nx), np.float32)
+    return w, w.var
 
 
 def _point_at(w, i, j, z, pose_z=0.0):
@@ -71,18 +71,18 @@ def test_kf_worked_examples():
     w, var = _window()
     w.known[4, 5] = 1; w.heights[4, 5] = 0.0; var[4, 5] = 1.0
     pose = Pose(R_B=np.eye(3), p_B=np.zeros(3), Sigma_S=np.eye(3))            # sigma_m^2 = 1
-    integrate_scan(w, var, [_point_at(w, 5, 4, 1.0)], pose, P)
+    integrate_scan(w, [_point_at(w, 5, 4, 1.0)], pose, P)
     assert (w.heights[4, 5], var[4, 5]) == (np.float32(0.5), np.float32(0.5))
     w, var = _window()
     pose = Pose(R_B=np.eye(3), p_B=np.zeros(3), Sigma_S=np.eye(3) * 0.04)
-    integrate_scan(w, var, [_point_at(w, 2, 3, 2.0)], pose, P)
+    integrate_scan(w, [_point_at(w, 2, 3, 2.0)], pose, P)
     assert (w.known[3, 2], w.heights[3, 2], var[3, 2]) == (1, np.float32(2.0), np.float32(0.04))
     w, var = _window()
     w.known[4, 5] = 1; w.heights[4, 5] = 0.0; var[4, 5] = 1e-4
     pose = Pose(R_B=np.eye(3), p_B=np.zeros(3), Sigma_S=np.eye(3) * 1e-4)
-    integrate_scan(w, var, [_point_at(w, 5, 4, 0.5)], pose, P)                 # d = 35.36 > 2, higher
+    integrate_scan(w, [_point_at(w, 5, 4, 0.5)], pose, P)                 # d = 35.36 > 2, higher
     assert (w.heights[4, 5], var[4, 5]) == (np.float32(0.5), np.float32(1e-4))
-    integrate_scan(w, var, [_point_at(w, 5, 4, -0.5)], pose, P)                # gate fails, lower: discarded
+    integrate_scan(w, [_point_at(w, 5, 4, -0.5)], pose, P)                # gate fails, lower: discarded
     assert (w.heights[4, 5], var[4, 5]) == (np.float32(0.5), np.float32(1e-4))
 
 
@@ -98,7 +98,7 @@ def test_kf_properties():
         pose = Pose(R_B=np.eye(3), p_B=np.zeros(3), Sigma_S=np.eye(3) * 1e-4)
         prev = var[4, 5]
         for t in order:
-            integrate_scan(w, var, [_point_at(w, 5, 4, zs[t])], pose, P)
+            integrate_scan(w, [_point_at(w, 5, 4, zs[t])], pose, P)
             assert var[4, 5] <= prev
             prev = var[4, 5]
         res.append((float(w.heights[4, 5]), float(var[4, 5])))
@@ -121,7 +121,7 @@ def test_raycast_worked_examples_and_filters():
     pt = np.array([(w.I_M + 25.5) * 0.1, (w.J_M + 5.5) * 0.1, 0.0]) - pose.p_B
     far = np.array([100.0, 0.0, 0.0])
     high = np.array([0.2, 0.0, 5.0])
-    status, n_reset = integrate_scan(w, var, [pt, far, high], pose, P)
+    status, n_reset = integrate_scan(w, [pt, far, high], pose, P)
     assert list(status) == [0, 1, 2]
     assert w.known[5, 10] == 0 and w.known[5, 12] == 1 and n_reset == 1
     assert w.known[5, 25] == 1 and w.heights[5, 25] == np.float32(0.0)

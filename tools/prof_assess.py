@@ -1,0 +1,65 @@
+#!/usr/bin/env python
+"""Time (or, under ncu, just launch) one configuration's FULL assess through the C ABI.
+
+    python tools/prof_assess.py --config large [--holes 0.02] [--reps 10]
+
+--holes f: that fraction of cells is unknown, in 3x3 blobs at random places (LiDAR shadows), which
+sends most tiles down the general (border / unknown) path.  Prints ms per FULL assess (host wall clock
+around assess + synchronize; the kernel dominates at these sizes).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from synth.terrain import CONFIGS, world_heights  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
+    ap.add_argument("--holes", type=float, default=0.0)
+    ap.add_argument("--reps", type=int, default=10)
+    a = ap.parse_args()
+    from paper_2503_02412_b200.se2map import Se2Map
+    import oracle
+
+    c = CONFIGS[a.config]
+    nx, ny, r = c["nx"], c["ny"], c["r"]
+    x, y = c["robot"]
+    I_M, J_M = oracle.window_origin(x, y, r, nx, ny)
+    h = world_heights(c["terrain"], I_M, J_M, nx, ny, r)
+    known = None
+    if a.holes > 0:
+        rng = np.random.default_rng(0)
+        known = np.ones((ny, nx), np.uint8)
+        nb = int(a.holes * nx * ny / 9)
+        ci, cj = rng.integers(1, nx - 1, nb), rng.integers(1, ny - 1, nb)
+        for di in (-1, 0, 1):
+            for dj in (-1, 0, 1):
+                known[cj + dj, ci + di] = 0
+    m = Se2Map(nx=nx, ny=ny, n_yaw=c["n_yaw"], resolution=r, ellipse_ex=c["ex"], ellipse_ey=c["ey"],
+               robot_x=x, robot_y=y)
+    m.update_elevation(h, known)
+    m.assess_se2(0)
+    m.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        t = time.perf_counter()
+        m.assess_se2(0)
+        m.synchronize()
+        ts.append(time.perf_counter() - t)
+    print(json.dumps(dict(config=a.config, holes=a.holes, unknown_frac=0.0 if known is None else
+                          float(1 - known.mean()), ms_median=1e3 * float(np.median(ts)),
+                          ms_min=1e3 * float(np.min(ts)))))
+
+
+if __name__ == "__main__":
+    main()
