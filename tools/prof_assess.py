@@ -27,10 +27,14 @@ def main():
     ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
     ap.add_argument("--holes", type=float, default=0.0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--scan", action="store_true",
+                    help="the bench's paper_pipeline map instead: 180x180x30 built from 4 LiDAR frames")
     a = ap.parse_args()
     from paper_2503_02412_b200.se2map import Se2Map
     import oracle
 
+    if a.scan:
+        return scan_map(a, Se2Map)
     c = CONFIGS[a.config]
     nx, ny, r = c["nx"], c["ny"], c["r"]
     x, y = c["robot"]
@@ -59,6 +63,31 @@ def main():
     print(json.dumps(dict(config=a.config, holes=a.holes, unknown_frac=0.0 if known is None else
                           float(1 - known.mean()), ms_median=1e3 * float(np.median(ts)),
                           ms_min=1e3 * float(np.min(ts)))))
+
+
+def scan_map(a, Se2Map):
+    from paper_2503_02412_b200 import se2map as S
+    from synth.lidar import scan
+    from synth.terrain import Hills
+    terrain = Hills(seed=31)
+    path = [(0.37 + 0.15 * t, 0.61 + 0.05 * t, 0.3 + 0.02 * t) for t in range(4)]
+    m = Se2Map(nx=180, ny=180, n_yaw=30, resolution=0.1, robot_x=path[0][0], robot_y=path[0][1])
+    for t, (x, y, yaw) in enumerate(path):
+        fr = scan(terrain, x, y, yaw, seed=500 + t, n_az=1800)
+        m.shift_window(x, y)
+        m.integrate_scan(fr.points_s, S.Pose.from_arrays(fr.R_B, fr.p_B, fr.R_BS, fr.p_BS, fr.Sigma_S,
+                                                         fr.Sigma_R, fr.Sigma_B))
+    h, _ = m.download_elevation()
+    m.assess_se2(0)
+    m.synchronize()
+    ts = []
+    for _ in range(a.reps):
+        t = time.perf_counter()
+        m.assess_se2(0)
+        m.synchronize()
+        ts.append(time.perf_counter() - t)
+    print(json.dumps(dict(config="scan180", unknown_frac=float(np.isnan(h).mean()),
+                          ms_median=1e3 * float(np.median(ts)), ms_min=1e3 * float(np.min(ts)))))
 
 
 if __name__ == "__main__":
