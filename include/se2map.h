@@ -73,6 +73,12 @@ typedef struct {
   double fe_gate;          /* Mahalanobis gate |z - h| / sqrt(s2 + s2_m) (default 2.0) */
   double fe_ray_eps;       /* ray-cast margin, m (default 0.05) */
   double fe_prior_var;     /* variance given to cells written by se2m_update_elevation, m^2 (default 1e-4) */
+  /* NEXT-4 ("the GPU will compute the traversability ... using the inpainted elevation map"):
+   * 0 = assess reads the map as it is (unknown cells are excluded from footprints, reading R9);
+   * 1 = assess reads the nearest-neighbour inpainted view of the map (se2m_inpaint, reading R31),
+   *     refreshed automatically when the map changed since the last refresh. */
+  int32_t inpaint;
+  int32_t reserved1;
 } se2m_params;
 
 /* NEXT-1: one LiDAR frame.  Rotations row-major (world <- body, body <- sensor), covariances 3x3. */
@@ -159,6 +165,18 @@ se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int64_t n, con
 
 /* Heights and variances of the window in logical order (ny x nx each, NaN height = unknown). */
 se2m_status se2m_download_elevation(se2m_map* m, float* heights, float* variances, int32_t mem);
+
+/* NEXT-4: nearest-neighbour inpainting ("can be inpainted by classical methods", PAPER.md:248
+ * "Both methods utilize nearest-neighbor interpolation for elevation inpainting").  Reading R31: every
+ * unknown cell of the window takes the height of its nearest known cell of the window (Euclidean distance
+ * on grid indices; ties to the known cell first in row-major (j, i) order); known cells keep theirs.  The
+ * result is a separate view: the map itself (the Kalman state) keeps its unknown cells.  Cells whose view
+ * value changed are marked dirty for INCREMENTAL assessment.  SE2M_ERR_STATE when no cell of the window
+ * is known (the view is then all unknown).  Synchronises (reads back a counter and a bounding box). */
+se2m_status se2m_inpaint(se2m_map* m);
+
+/* The inpainted view in logical order (ny x nx; refreshed first if the map changed). */
+se2m_status se2m_download_inpainted(se2m_map* m, float* heights, int32_t mem);
 
 /* NEXT-2: signed distance field of the explicit obstacles (Risk = 1) of
  * every yaw layer, from the last assess ("the corresponding signed distance field (SDF)

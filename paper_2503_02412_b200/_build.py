@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libse2map.so")
-SOURCES = ["assess.cu", "sdf.cu", "frontend.cu", "se2map.cu"]
+SOURCES = ["assess.cu", "sdf.cu", "frontend.cu", "inpaint.cu", "se2map.cu"]
 HEADERS = ["se2m_internal.h", os.path.join("..", "..", "include", "se2map.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -140,4 +140,13 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s);
 cudaError_t launch_trilinear(const float* field, int stride_elems, int is_sdf, const QueryGeo& g, int n,
                              const double* xyt, float* out, int* n_out, cudaStream_t s);
 
+// ---- NEXT-4: nearest-neighbour inpainting of unknown cells (inpaint.cu) ------------------------------
+// h: the elevation ring (NaN = unknown); site: logical [ny][nx] int scratch (nearest known row of the
+// column); view: output ring (same layout as h); ctr[0] = known cells (zeroed by the caller), ctr[1..4] =
+// logical bounding box (i_min, i_max, j_min, j_max) of the view cells whose value changed
+// segs: inpaint_seg_ints(nx, ny) ints of scratch (per-segment first / last known rows)
+cudaError_t launch_inpaint(const float* h, int ldh, int nx, int ny, int pxM, int pyM, int* site, float* view,
+                           int* ctr, int* segs, cudaStream_t s);
+size_t inpaint_seg_ints(int nx, int ny);
+
 }  // namespace se2m

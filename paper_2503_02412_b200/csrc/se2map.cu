@@ -72,6 +72,14 @@ struct se2m_map {
   size_t q_cap = 0;
   CUtensorMap tmap;
   bool tma_ok = false;
+  // NEXT-4: nearest-neighbour inpainted view (ring layout like d_h), allocated on first use
+  float* d_hin = nullptr;
+  int* d_site = nullptr;
+  int* d_ipc = nullptr;      // [0] known cells, [1..4] changed-cell box (logical i0, i1, j0, j1)
+  int* h_ipc = nullptr;      // pinned copy
+  CUtensorMap tmap_in;
+  bool tma_in_ok = false;
+  bool inpaint_valid = false;
   bool force_general = false;  // a full stencil is degenerate (R22): every tile takes the general path
   bool have_data = false;
   bool all_dirty = true;
@@ -207,7 +215,7 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
   m->chain_off[m->H] = (int)chain.size();
 }
 
-static bool make_tensor_map(se2m_map* m) {
+static bool make_tensor_map(se2m_map* m, CUtensorMap* tm, float* base) {
   typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -222,7 +230,7 @@ static bool make_tensor_map(se2m_map* m) {
   cuuint64_t strides[1] = {(cuuint64_t)m->ldh * 4};
   cuuint32_t box[2] = {(cuuint32_t)HX, (cuuint32_t)HY};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = ((EncodeFn)fn)(&m->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, m->d_h, dims, strides, box, estr,
+  CUresult r = ((EncodeFn)fn)(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -288,6 +296,7 @@ static se2m_status validate(const se2m_params* p) {
   const bool fe_unset = p->fe_z_min == 0 && p->fe_z_max == 0 && p->fe_gate == 0 && p->fe_ray_eps == 0 && p->fe_prior_var == 0;
   if (!fe_unset && (!(p->fe_z_min < p->fe_z_max) || !(p->fe_gate > 0) || !(p->fe_ray_eps >= 0) || !(p->fe_prior_var > 0)))
     return fail(nullptr, SE2M_ERR_INVALID_ARG, "front-end params: need z_min < z_max, gate > 0, ray_eps >= 0, prior_var > 0");
+  if (p->inpaint != 0 && p->inpaint != 1) return fail(nullptr, SE2M_ERR_INVALID_ARG, "inpaint must be 0 or 1");
   if (p->ellipse_ex / p->resolution > 32 || p->ellipse_ey / p->resolution > 32)
     return fail(nullptr, SE2M_ERR_UNSUPPORTED, "footprint radius > 32 cells is not built into this library");
   return SE2M_OK;
@@ -407,7 +416,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     cuda_fail(m, e, "init upload");
     return bail(SE2M_ERR_CUDA);
   }
-  m->tma_ok = make_tensor_map(m);
+  m->tma_ok = make_tensor_map(m, &m->tmap, m->d_h);
   *out = m;
   return SE2M_OK;
 }
@@ -417,9 +426,10 @@ extern "C" void se2m_destroy(se2m_map* m) {
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
                   m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
-                  m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt};
+                  m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc};
   for (void* q : ptrs)
     if (q) cudaFree(q);
+  if (m->h_ipc) cudaFreeHost(m->h_ipc);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -454,6 +464,7 @@ extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0
                                   w, h, src, sld, kn, m->stream), "scatter");
   m->launches++;
   m->have_data = true;
+  m->inpaint_valid = false;
   m->dirty.push_back(Rect{m->I_M + i0, m->I_M + i0 + w, m->J_M + j0, m->J_M + j0 + h});
   return SE2M_OK;
 }
@@ -480,6 +491,7 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
     m->launches++;
     m->all_dirty = true;
     m->dirty.clear();
+    m->inpaint_valid = false;
     return SE2M_OK;
   }
   // cells entering the window (their physical slots held cells that left): set unknown.
@@ -496,6 +508,7 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
     CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, pxM, (pyM + l0) % ny, nx, hgt, nx, ny, m->stream), "clear rows");
     m->launches++;
   }
+  m->inpaint_valid = false;
   // dirty: the entered strips of the new window and the vacated strips of the old one (H9)
   if (di > 0) { m->dirty.push_back(Rect{old_w.I1, new_w.I1, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{old_w.I0, new_w.I0, old_w.J0, old_w.J1}); }
   if (di < 0) { m->dirty.push_back(Rect{new_w.I0, old_w.I0, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{new_w.I1, old_w.I1, old_w.J0, old_w.J1}); }
@@ -505,11 +518,54 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
 }
 
 
+// NEXT-4: (re)compute the inpainted view; cells whose view value changed become dirty.  Synchronises.
+static se2m_status run_inpaint(se2m_map* m, int* n_known) {
+  const int nx = m->prm.nx, ny = m->prm.ny;
+  if (!m->d_hin) {
+    CUDA_TRY(m, cudaMalloc(&m->d_hin, (size_t)m->ldh * ny * 4), "cudaMalloc(inpainted view)");
+    CUDA_TRY(m, cudaMalloc(&m->d_site, ((size_t)nx * ny + inpaint_seg_ints(nx, ny)) * 4), "cudaMalloc(inpaint scratch)");
+    CUDA_TRY(m, cudaMalloc(&m->d_ipc, 8 * sizeof(int)), "cudaMalloc(inpaint counters)");
+    CUDA_TRY(m, cudaMallocHost(&m->h_ipc, 8 * sizeof(int)), "cudaMallocHost(inpaint counters)");
+    CUDA_TRY(m, cudaMemsetAsync(m->d_hin, 0xff, (size_t)m->ldh * ny * 4, m->stream), "init view");  // NaN
+    m->tma_in_ok = m->tma_ok && make_tensor_map(m, &m->tmap_in, m->d_hin);
+  }
+  CUDA_TRY(m, cudaMemsetAsync(m->d_ipc, 0, sizeof(int), m->stream), "inpaint counters");
+  CUDA_TRY(m, launch_inpaint(m->d_h, m->ldh, nx, ny, pmod(m->I_M, nx), pmod(m->J_M, ny), m->d_site, m->d_hin,
+                             m->d_ipc, m->d_site + (size_t)nx * ny, m->stream), "inpaint kernels");
+  m->launches += 3;
+  CUDA_TRY(m, cudaMemcpyAsync(m->h_ipc, m->d_ipc, 5 * sizeof(int), cudaMemcpyDeviceToHost, m->stream), "D2H inpaint");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(inpaint)");
+  const int* c = m->h_ipc;
+  if (c[2] >= 0) m->dirty.push_back(Rect{m->I_M + c[1], m->I_M + c[2] + 1, m->J_M + c[3], m->J_M + c[4] + 1});
+  m->inpaint_valid = true;
+  if (n_known) *n_known = c[0];
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_inpaint(se2m_map* m) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  int n_known = 0;
+  se2m_status st = run_inpaint(m, &n_known);
+  if (st != SE2M_OK) return st;
+  if (n_known == 0) return fail(m, SE2M_ERR_STATE, "inpaint: no known cell in the window");
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   if (!m) return SE2M_ERR_INVALID_ARG;
   if (mode != SE2M_FULL && mode != SE2M_INCREMENTAL) return fail(m, SE2M_ERR_INVALID_ARG, "assess: bad mode");
   if (!m->have_data) return fail(m, SE2M_ERR_STATE, "assess before any update_elevation");
+  if (m->prm.inpaint && !m->inpaint_valid) {  // NEXT-4: assess the inpainted view
+    se2m_status st = run_inpaint(m, nullptr);
+    if (st != SE2M_OK) return st;
+  }
   AssessParams p = make_params(m);
+  const CUtensorMap* tmap = &m->tmap;
+  if (m->prm.inpaint) {
+    p.h = m->d_hin;
+    tmap = &m->tmap_in;
+    p.use_tma = m->tma_in_ok ? 1 : 0;
+  }
   const int nx = m->prm.nx, ny = m->prm.ny;
   const int TY = tile_rows(m->R_T);
   // dense grid of world tiles intersecting the window
@@ -568,7 +624,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   }
   p.tab_cap = cap;
   if (n_tiles > 0 && nk > 0) {
-    cudaError_t e = launch_assess(p, m->R_T, n_tiles, &m->tmap, m->stream);
+    cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
     m->launches++;
   }
@@ -800,6 +856,7 @@ extern "C" se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int
   if (bb[1] >= 0) {  // touched cells -> dirty (H9)
     m->dirty.push_back(Rect{m->I_M + bb[0], m->I_M + bb[1] + 1, m->J_M + bb[2], m->J_M + bb[3] + 1});
     m->have_data = true;
+    m->inpaint_valid = false;
   }
   return SE2M_OK;
 }
@@ -837,6 +894,25 @@ extern "C" se2m_status se2m_download_elevation(se2m_map* m, float* heights, floa
       CUDA_TRY(m, cudaMemcpyAsync(outs[q], target, cells * 4, cudaMemcpyDeviceToHost, m->stream), "D2H elevation");
     CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_elevation)");
   }
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_download_inpainted(se2m_map* m, float* heights, int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!heights || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(m, SE2M_ERR_INVALID_ARG, "download_inpainted: bad pointer / mem");
+  if (!m->inpaint_valid) {
+    se2m_status st = run_inpaint(m, nullptr);
+    if (st != SE2M_OK) return st;
+  }
+  const size_t bytes = (size_t)m->prm.nx * m->prm.ny * 4;
+  if (mem == SE2M_MEM_DEVICE) return ring_to_logical(m, m->d_hin, heights);
+  se2m_status st = ensure_stage(m, bytes);
+  if (st != SE2M_OK) return st;
+  st = ring_to_logical(m, m->d_hin, m->d_stage);
+  if (st != SE2M_OK) return st;
+  CUDA_TRY(m, cudaMemcpyAsync(heights, m->d_stage, bytes, cudaMemcpyDeviceToHost, m->stream), "D2H inpainted");
+  CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync");
   return SE2M_OK;
 }
 

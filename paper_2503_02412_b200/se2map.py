@@ -30,7 +30,8 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_assess_se2", "se2m_query", "se2m_download", "se2m_get_origin", "se2m_stencil_info",
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
-           "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation"]
+           "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
+           "se2m_download_inpainted"]
 
 
 class Params(ctypes.Structure):
@@ -43,7 +44,8 @@ class Params(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("fe_z_min", ctypes.c_double), ("fe_z_max", ctypes.c_double), ("fe_gate", ctypes.c_double),
-                ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double)]
+                ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double),
+                ("inpaint", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class Pose(ctypes.Structure):
@@ -84,6 +86,8 @@ _lib.se2m_sdf_from_mask.argtypes = [_vp, _i32, _i32, _i32, _f64, _f64, _vp, _i32
 _lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
 _lib.se2m_integrate_scan.argtypes = [_vp, _vp, _i64, ctypes.POINTER(Pose), _i32, _vp]
 _lib.se2m_download_elevation.argtypes = [_vp, _vp, _vp, _i32]
+_lib.se2m_inpaint.argtypes = [_vp]
+_lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_launch_count.argtypes = [_vp]
@@ -320,6 +324,16 @@ class Se2Map:
         v = np.empty((P.ny, P.nx), np.float32)
         self._check(_lib.se2m_download_elevation(self.h, h.ctypes.data, v.ctypes.data, SE2M_MEM_HOST))
         return h, v
+
+    def inpaint(self):
+        """NEXT-4: refresh the nearest-neighbour inpainted view (raises if no cell is known)."""
+        self._check(_lib.se2m_inpaint(self.h))
+
+    def download_inpainted(self):
+        P = self.params
+        h = np.empty((P.ny, P.nx), np.float32)
+        self._check(_lib.se2m_download_inpainted(self.h, h.ctypes.data, SE2M_MEM_HOST))
+        return h
 
     def origin(self):
         I, J = _i64(), _i64()
