@@ -77,6 +77,8 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a
 // MUFU approximations (relative error ~1 ulp); the eigenvector refinement absorbs them.
 __device__ __forceinline__ float frcp(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
 __device__ __forceinline__ float fsqrt(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+// MUFU.RSQ without the subnormal-input rescaling rsqrtf() carries (4 instructions less per call)
+__device__ __forceinline__ float frsqrt(float x) { float r; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
 // ------------------------------------------------------------------------------------------
 // Packed two-state epilogue for interior tiles (all footprint cells known and inside the window).
 // Every FP32 add/mul/fma runs as one sm_100a FADD2/FMUL2/FFMA2 on (state a, state b); MUFU, compares
@@ -97,7 +99,7 @@ __device__ __forceinline__ F2 operator-(F2 a, F2 b) { return __fadd2_rn(a, neg2(
 __device__ __forceinline__ F2 operator*(F2 a, F2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ F2 fma2(F2 a, F2 b, F2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ F2 abs2(F2 x) { return pk(fabsf(lo(x)), fabsf(hi(x))); }
-__device__ __forceinline__ F2 rsqrt2(F2 x) { return pk(rsqrtf(lo(x)), rsqrtf(hi(x))); }
+__device__ __forceinline__ F2 rsqrt2(F2 x) { return pk(frsqrt(lo(x)), frsqrt(hi(x))); }
 __device__ __forceinline__ F2 rcp2(F2 x) { return pk(frcp(lo(x)), frcp(hi(x))); }
 __device__ __forceinline__ F2 sqrt2abs(F2 x) { return pk(fsqrt(fabsf(lo(x))), fsqrt(fabsf(hi(x)))); }
 __device__ __forceinline__ F2 copysign2(F2 m, F2 sg) { return pk(copysignf(lo(m), lo(sg)), copysignf(hi(m), hi(sg))); }
@@ -603,6 +605,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 
   // per state s (tile row warp + s NWARPS): record index in a bin plane, traversable-word index (-1: the
   // state's row is outside the window)
+  int tmy = -1;  // interior tiles: lane s < RPW writes the traversable word of state s
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
@@ -611,35 +614,47 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
     soff[s] = (py >= 0 && col_in) ? py * p.nx + pxs : -1;
     stoff[s] = (py >= 0 && col_any && lane == 0) ? py * p.trav_words + gword : -1;
+    if (lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
   }
 
   float2 S02[RPW];            // interior tiles: moments carried along the yaw chain
   float SXH[RPW], SYH[RPW];
-  for (int k = kb; k < ke; ++k) {
+  // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
+  const size_t twplane = (size_t)p.ny * p.trav_words;
+  float4* outk = p.out + (size_t)kb * plane;
+  float4* outk2 = outk + (size_t)p.H * plane;
+  uint32_t* travk = p.trav + (size_t)kb * twplane;
+  uint32_t* travk2 = travk + (size_t)p.H * twplane;
+  int kc = kb % p.period;     // position in the yaw chain (restart at 0)
+  for (int k = kb; k < ke; ++k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
     const int e0 = __ldg(tab_off + k);
     const int4* rk = runs_s + (e0 - tab_base);
     const int nr = __ldg(tab_off + k + 1) - e0;
     const float2 csk = __ldg(p.cs + k);
-    float4* outk = p.out + (size_t)k * plane;
-    float4* outk2 = p.out + (size_t)(k + p.H) * plane;
-    uint32_t* travk = p.trav + (size_t)k * p.ny * p.trav_words;
-    uint32_t* travk2 = p.trav + (size_t)(k + p.H) * p.ny * p.trav_words;
-    auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
+    const bool restart = k == kb || kc == 0;
+    if (++kc == p.period) kc = 0;
+    auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
       if (off >= 0) {  // write-once stream: evict-first stores
         __stcs(outk + off, make_float4(risk, pitch, roll, z));
         if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
       }
-      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-      const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
+    };
+    // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
+    auto store_trav = [&](int toff, unsigned tmask) {
       if (toff >= 0) {
         travk[toff] = tmask;
         if (p.paired) travk2[toff] = tmask;
       }
     };
+    auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
+      store_rec(off, risk, pitch, roll, z);
+      const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
+      store_trav(lane == 0 ? toff : -1, tmask);
+    };
     if (fast) {
       // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.
       // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
-      if (k == kb || k % p.period == 0) {
+      if (restart) {
 #pragma unroll
         for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
       }
@@ -659,20 +674,27 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           const float bxv = *reinterpret_cast<const float*>(pb4 + s * RS4);
           const float2 dd = sub2(B, A);  // (run sum of h^, run sum of h^2)
           S02[s] = add2(S02[s], dd);
-          SXH[s] += fmaf(-xs, dd.x, bxv - ax);
+          SXH[s] += bxv - ax;  // sum of x' h^ (x' from the tile centre); -xs S0 is applied once below
           SYH[s] = fmaf(dj, dd.x, SYH[s]);
         }
       }
       const float4 gc = __ldg(p.geoc + 2 * k), gd = __ldg(p.geoc + 2 * k + 1);
+      unsigned tmine = 0;
 #pragma unroll
       for (int s = 0; s < RPW; s += 2) {
-        const StateOut2 o = epilogue2(pk(S02[s].x, S02[s + 1].x), pk(S02[s].y, S02[s + 1].y), pk(SXH[s], SXH[s + 1]),
+        const F2 S0p = pk(S02[s].x, S02[s + 1].x);
+        const StateOut2 o = epilogue2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
                                       pk(SYH[s], SYH[s + 1]),
                                       pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gx, Gy,
                                       gc, gd, csk, p);
-        store(soff[s], stoff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a);
-        store(soff[s + 1], stoff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b);
+        store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
+        store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
+        const unsigned ma = __ballot_sync(0xffffffffu, soff[s] >= 0 && o.trav_a);
+        const unsigned mb = __ballot_sync(0xffffffffu, soff[s + 1] >= 0 && o.trav_b);
+        if (lane == s) tmine = ma;
+        if (lane == s + 1) tmine = mb;
       }
+      store_trav(tmy, tmine);  // lane s writes state s's word
     } else {
       // ---- border / unknown tile: also the validity moments (N, sum di, sum di^2, ...), two states at a time
 #pragma unroll 1
