@@ -220,15 +220,75 @@ __device__ __forceinline__ StateOut2 solve2(F2 C00, F2 C01, F2 C11, F2 Cp02, F2 
   return o;
 }
 
-// interior tiles: geometry constants per bin gc = (C00, C01, C11, 1/N), gd = (r/N, -, -, -);
-// zref = tile-plane height at each state (the footprint is centred, so the mean height is zref + mean h^)
-__device__ __forceinline__ StateOut2 epilogue2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zref, float Gx, float Gy, float4 gc,
-                                               float4 gd, float2 csk, const AssessParams& p) {
-  const F2 mh = S0 * bc(gc.w);
-  const F2 C22 = fma2(neg2(mh), mh, S2 * bc(gc.w));
-  const F2 z0 = bc(0.f);
-  return solve2<false>(bc(gc.x), bc(gc.y), bc(gc.z), SXH * bc(gd.x), SYH * bc(gd.x), C22, z0, z0, zref + mh, true,
-                       true, Gx, Gy, csk, p);
+// Interior tiles (full, centred footprints: Σdi = Σdj = 0).  In the eigenbasis (q1, q2) of the per-bin
+// footprint geometry A = Cov(x, y) (a1 <= a2, host FP64) the covariance of Alg. 1 is the arrowhead matrix
+//   [[a1, 0, c1], [0, a2, c2], [c1, c2, d]],   c_i = q_i . Cov((x, y), h),   d = Var(h),
+// whose smallest eigenpair is (lam, (x, y, 1)) with x = -c1 / (a1 - lam), y = -c2 / (a2 - lam) (the third
+// component is 1: n_z > 0 by construction) and lam the smallest root of the secular equation
+// f(lam) = d - lam - c1^2 / (a1 - lam) - c2^2 / (a2 - lam) = 0 (lam < a1 by interlacing).  lam: the
+// trigonometric closed form (trace-normalised), polished by one Newton step on f (|f'| >= 1, so lam is then
+// accurate to a few ulp of the trace and the eigenvector to ~ulp / gap).  kappa = lam (reading R1).
+// Per bin: gc = (C00, C01, C11, 1/N), gd = (r/N, a1, a2, a1 + a2), ge = (q1x, q1y, q1.e, q2.e),
+// gf = (q1.e', q2.e', -, -) with e = (cos, sin) theta_k, e' = (sin, -cos) theta_k.  Tile plane: h = h^ +
+// G.(x, y) + const (G per metre): Gq1 = G.q1, Gq2 = G.q2; aG1 = a1 Gq1, aG2 = a2 Gq2 (A q_i = a_i q_i).
+__device__ __forceinline__ StateOut2 arrow2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zref, float Gq1, float Gq2, float aG1,
+                                            float aG2, float4 gc, float4 gd, float4 ge, float4 gf,
+                                            const AssessParams& p) {
+  const F2 iN = bc(gc.w), rN = bc(gd.x);
+  const F2 mh = S0 * iN;
+  const F2 Cp22 = fma2(neg2(mh), mh, S2 * iN);          // Var(h^)
+  const F2 Cx = SXH * rN, Cy = SYH * rN;                 // Cov(x, h^), Cov(y, h^)  (m^2)
+  const F2 cp1 = fma2(bc(ge.x), Cx, bc(ge.y) * Cy);     // q1 . Cov((x, y), h^)
+  const F2 cp2 = fma2(bc(ge.x), Cy, bc(-ge.y) * Cx);    // q2 . Cov((x, y), h^)
+  const F2 c1 = cp1 + bc(aG1), c2 = cp2 + bc(aG2);      // q_i . Cov((x, y), h)
+  const F2 d = fma2(bc(Gq1), cp1 + c1, fma2(bc(Gq2), cp2 + c2, Cp22));  // Var(h)
+  const F2 it = rcp2(d + bc(gd.w));                      // 1 / trace
+  const F2 A1 = bc(gd.y) * it, A2 = bc(gd.z) * it, D = d * it, E1 = c1 * it, E2 = c2 * it;
+  // smallest root of det(M - lam I), M = the normalised arrowhead (trace 1): trigonometric form
+  const F2 third = bc(1.f / 3.f);
+  const F2 b1 = A1 - third, b2 = A2 - third, b3 = D - third;
+  const F2 E11 = E1 * E1, E22 = E2 * E2, ee = E11 + E22;
+  const F2 p2 = fma2(b1, b1, fma2(b2, b2, fma2(b3, b3, ee + ee))) * bc(1.f / 6.f);
+  const F2 ip = rsqrt2(p2);
+  const F2 pp = p2 * ip;
+  const F2 det = fma2(b1, fma2(b2, b3, neg2(E22)), neg2(E11 * b2));   // det(M - I/3)
+  const F2 hr = det * ((ip * ip) * (ip * bc(0.5f)));                  // det((M - I/3) / p) / 2
+  const F2 phi = acos2(hr) * third;
+  float sl, cl, sh, ch;
+  __sincosf(lo(phi), &sl, &cl);
+  __sincosf(hi(phi), &sh, &ch);
+  F2 lam = fma2(neg2(pp), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), third);
+  // one Newton step on the secular equation: lam += f / (1 + t1^2 + t2^2), t_i = E_i / (A_i - lam)
+  {
+    const F2 t1 = E1 * rcp2(A1 - lam), t2 = E2 * rcp2(A2 - lam);
+    const F2 f = fma2(neg2(E1), t1, fma2(neg2(E2), t2, D - lam));
+    const F2 fp = fma2(t1, t1, fma2(t2, t2, bc(1.f)));
+    lam = fma2(f, rcp2(fp), lam);
+  }
+  const F2 x = neg2(E1 * rcp2(A1 - lam)), y = neg2(E2 * rcp2(A2 - lam));  // normal ~ (x, y, 1)
+  const F2 kap = pk(fmaxf(0.f, lo(lam)), fmaxf(0.f, hi(lam)));
+  // Eqs. 2-3 reduced (as in solve2) for the unnormalised normal n = (x q1 + y q2, 1): u = n.e, t = n.e'
+  const F2 u = fma2(x, bc(ge.z), y * bc(ge.w));
+  const F2 t = fma2(x, bc(gf.x), y * bc(gf.y));
+  // b3.y_b = t / |n x e| (scale-free); b3.x_b = -n_z u / (|n| |n x e|), |n x e|^2 = 1 + t^2, |n|^2 = 1 + t^2 + u^2
+  const F2 w = fma2(t, t, bc(1.f));
+  const F2 rs = rsqrt2(w);
+  const F2 pitch = asin2(neg2(u) * (rs * rsqrt2(fma2(u, u, w))));
+  const F2 roll = asin2(t * rs);
+  const F2 ax = abs2(pitch), ay = abs2(roll);
+  const F2 rk = fma2(bc(p.wk), kap, fma2(bc(p.wx), ax, ay * bc(p.wy)));
+  const bool el = lo(kap) > p.kappa_max || lo(ax) > p.phi_x_max || lo(ay) > p.phi_y_max;
+  const bool eh = hi(kap) > p.kappa_max || hi(ax) > p.phi_x_max || hi(ay) > p.phi_y_max;
+  const bool vl = lo(ax) <= 2.f && lo(ay) <= 2.f, vh = hi(ax) <= 2.f && hi(ay) <= 2.f;  // NaN: unknown (R11)
+  const F2 qn = bc(__int_as_float(0x7fc00000));
+  StateOut2 o;
+  o.risk = sel2(vl && !el, vh && !eh, rk, bc(1.f));
+  o.pitch = sel2(vl, vh, pitch, qn);
+  o.roll = sel2(vl, vh, roll, qn);
+  o.z = sel2(vl, vh, zref + mh, qn);  // z = f_1 at the state centre = the footprint centroid (R14)
+  o.trav_a = (vl && !el) ? 1u : 0u;
+  o.trav_b = (vh && !eh) ? 1u : 0u;
+  return o;
 }
 
 // border / unknown tiles: per-state moments (cell units for x, y; metres for h^).
@@ -381,6 +441,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   float* pxh = reinterpret_cast<float*>(smem + G::px_off);
   float2* pv = reinterpret_cast<float2*>(smem + G::pv_off);
   float* pvxx = reinterpret_cast<float*>(smem + G::pvxx_off);
+  float* hh_s = reinterpret_cast<float*>(smem + G::pv_off);  // interior tiles only (aliases PV)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
   float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
@@ -527,7 +588,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const int tab_base = __ldg(tab_off + kb);
   for (int idx = tid; idx < __ldg(tab_off + ke) - tab_base; idx += NTHREADS) {
     const int4 e = __ldg(tab + tab_base + idx);
-    runs_s[idx] = make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
+    runs_s[idx] = fast ? e : make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
   }
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
@@ -554,11 +615,16 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     const float ox = warp_incl_scan(sx, lane) - sx;
     float2* P02r = p02 + row * PW;
     float* PXr = pxh + row * PW;
+    float* HHr = hh_s + row * PW;  // interior tiles: h^ itself, for the single-cell chain entries
     if (lane == 0) { P02r[0] = make_float2(0.f, 0.f); PXr[0] = 0.f; }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const int col = lane * CPL + c;
-      if (col < HX) { P02r[col + 1] = make_float2(o0 + e[c], o2 + e2[c]); PXr[col + 1] = ox + ex[c]; }
+      if (col < HX) {
+        P02r[col + 1] = make_float2(o0 + e[c], o2 + e2[c]);
+        PXr[col + 1] = ox + ex[c];
+        if (fast) HHr[col] = hh[c];
+      }
     }
     if (!fast) {  // validity moments (exact integers in float)
       float vs[CPL], vx[CPL], vxx[CPL];
@@ -601,6 +667,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(warp * PW + lane) * 4;
   const char* bv8 = reinterpret_cast<const char*>(pv) + (size_t)(warp * PW + lane) * 8;
   const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(warp * PW + lane) * 4;
+  const char* bh = reinterpret_cast<const char*>(hh_s) + (size_t)(warp * PW + lane) * 4;
   constexpr int RS8 = NWARPS * PW * 8, RS4 = NWARPS * PW * 4;  // state s -> s * NWARPS halo rows lower
 
   // per state s (tile row warp + s NWARPS): record index in a bin plane, traversable-word index (-1: the
@@ -658,8 +725,9 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 #pragma unroll
         for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
       }
+      const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
 #pragma unroll 2
-      for (int d = 0; d < nr; ++d) {
+      for (int d = 0; d < npre; ++d) {
         const int4 o = rk[d];
         const float dj = __int_as_float(o.w);
         const char* pa8 = b8 + o.x;
@@ -678,15 +746,35 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           SYH[s] = fmaf(dj, dd.x, SYH[s]);
         }
       }
-      const float4 gc = __ldg(p.geoc + 2 * k), gd = __ldg(p.geoc + 2 * k + 1);
+      // single cells entering / leaving the footprint since bin k-1: one h^ load per state
+#pragma unroll 2
+      for (int d = npre; d < nr; ++d) {
+        const int4 o = rk[d];
+        const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
+        const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
+        const char* ph = bh + o.x;
+#pragma unroll
+        for (int s = 0; s < RPW; ++s) {
+          const float h = *reinterpret_cast<const float*>(ph + s * RS4);
+          const float sh = sg * h;
+          S02[s].x += sh;
+          S02[s].y = fmaf(sh, h, S02[s].y);
+          SXH[s] = fmaf(cx, h, SXH[s]);
+          SYH[s] = fmaf(sdj, h, SYH[s]);
+        }
+      }
+      const float4 gc = __ldg(p.geoc + 4 * k), gd = __ldg(p.geoc + 4 * k + 1);
+      const float4 ge = __ldg(p.geoc + 4 * k + 2), gf = __ldg(p.geoc + 4 * k + 3);
+      const float Gq1 = fmaf(Gx, ge.x, Gy * ge.y), Gq2 = fmaf(Gy, ge.x, -Gx * ge.y);
+      const float aG1 = gd.y * Gq1, aG2 = gd.z * Gq2;
       unsigned tmine = 0;
 #pragma unroll
       for (int s = 0; s < RPW; s += 2) {
         const F2 S0p = pk(S02[s].x, S02[s + 1].x);
-        const StateOut2 o = epilogue2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
-                                      pk(SYH[s], SYH[s + 1]),
-                                      pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gx, Gy,
-                                      gc, gd, csk, p);
+        const StateOut2 o = arrow2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
+                                   pk(SYH[s], SYH[s + 1]),
+                                   pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
+                                   aG1, aG2, gc, gd, ge, gf, p);
         store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
         store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
         const unsigned ma = __ballot_sync(0xffffffffu, soff[s] >= 0 && o.trav_a);

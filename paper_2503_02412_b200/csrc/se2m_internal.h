@@ -42,12 +42,19 @@ struct AssessParams {
   // k-1 to bin k (moments carried along the yaw chain).  Entries of bin k: [off[k], off[k+1]).
   const int4* full;
   const int* full_off;   // [H+1]
+  // chain (interior tiles) is stored in the kernel's shared-memory format: per bin first the prefix
+  // entries (8 e_minus, 8 e_plus, 4 e_minus, float dj) — byte offsets into {P0, P2} and PX — then, from
+  // chain_mid[k], single-cell entries (4 e, float sgn, float sgn di, float sgn dj): a cell that enters
+  // (sgn = +1) or leaves (-1) the footprint between bins k-1 and k, e = its element offset into the h^
+  // plane (stride PW, like the prefix rows).  Endpoint moves of <= 2 cells (nearly all at 5-degree bins)
+  // become cell entries (one 4-byte load per state instead of four prefix loads).
   const int4* chain;
   const int* chain_off;  // [H+1]
+  const int* chain_mid;  // [H]
   int period;            // yaw-chain restart period (1 = no chain); chunks start at multiples of it
   int tab_cap;           // max entries of one CTA's chunk (shared-memory table size)
   const float4* geo;     // [H] full-stencil (N, Sxx, Sxy, Syy) in cell units (Sx = Sy = 0)
-  const float4* geoc;    // [H][2] full-stencil covariance: (C00, C01, C11, 1/N), (r/N, C00+C11, C01^2, 0), metres
+  const float4* geoc;    // [H][4] full-stencil geometry for interior tiles (see assess.cu, arrow2), metres
   const float2* cs;      // [H] (cos, sin) of theta_k, k < H (reading R3)
   float r;               // resolution (m)
   // risk (Alg. 1 lines 10-18), all float

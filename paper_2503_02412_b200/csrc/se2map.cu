@@ -58,7 +58,8 @@ struct se2m_map {
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
   int* d_chain_off = nullptr;
-  std::vector<int> full_off, chain_off;
+  std::vector<int> full_off, chain_off, chain_mid;
+  int* d_chain_mid = nullptr;
   int period = 1;
   float4* d_geo = nullptr;
   float4* d_geoc = nullptr;
@@ -151,13 +152,24 @@ static bool build_stencils(se2m_map* m, std::vector<int4>& runs, std::vector<int
   runs.assign((size_t)m->H * NR, make_int4(0, -1, 0, 0));
   nrows.assign(m->H, 0);
   geo.resize(m->H);
-  geoc.resize(2 * (size_t)m->H);
+  geoc.resize(4 * (size_t)m->H);
   for (int k = 0; k < m->H; ++k) {
     // full-stencil covariance of the cell-centre offsets, metres^2, FP64 then rounded (Sx = Sy = 0)
     const double N = m->ncells[k], r = P.resolution;
     const double c00 = r * r * Sxx[k] / N, c01 = r * r * Sxy[k] / N, c11 = r * r * Syy[k] / N;
-    geoc[2 * k] = make_float4((float)c00, (float)c01, (float)c11, (float)(1.0 / N));
-    geoc[2 * k + 1] = make_float4((float)(r / N), (float)(c00 + c11), (float)(c01 * c01), 0.f);
+    // eigen-decomposition of the footprint geometry A = [[c00, c01], [c01, c11]] = a1 q1 q1^T + a2 q2 q2^T
+    // (a1 <= a2, q2 = (-q1y, q1x)), and the projections of q1, q2 on the bin's heading e = (cos, sin) and
+    // on (sin, -cos): the interior-tile solver works in this basis (assess.cu, arrow2)
+    const double hm = 0.5 * (c00 + c11), hd = 0.5 * (c00 - c11);
+    const double rad = sqrt(hd * hd + c01 * c01);
+    const double a1 = hm - rad, a2 = hm + rad;
+    const double psi = 0.5 * atan2(2.0 * c01, c00 - c11);  // direction of the a2 axis
+    const double q1x = -sin(psi), q1y = cos(psi), q2x = -q1y, q2y = q1x;
+    const double th = -M_PI + 2.0 * M_PI * (double)k / (double)P.n_yaw, ct = cos(th), st = sin(th);
+    geoc[4 * k] = make_float4((float)c00, (float)c01, (float)c11, (float)(1.0 / N));
+    geoc[4 * k + 1] = make_float4((float)(r / N), (float)a1, (float)a2, (float)(a1 + a2));
+    geoc[4 * k + 2] = make_float4((float)q1x, (float)q1y, (float)(q1x * ct + q1y * st), (float)(q2x * ct + q2y * st));
+    geoc[4 * k + 3] = make_float4((float)(q1x * st - q1y * ct), (float)(q2x * st - q2y * ct), 0.f, 0.f);
     for (int dj = -std::min(Rs, m->R_T); dj <= std::min(Rs, m->R_T); ++dj) {
       const Run& q = rr[k][dj + Rs];
       if (q.hi >= q.lo) runs[(size_t)k * NR + nrows[k]++] = make_int4(q.lo, q.hi, dj + m->R_T, 0);
@@ -184,8 +196,15 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
   };
   auto ea = [&](int d, int a) { return d * PW + RT + a; };
   auto eb = [&](int d, int b) { return d * PW + RT + b + 1; };
+  auto fbits = [](float f) { int i; memcpy(&i, &f, 4); return i; };
+  // chain prefix entry in shared-memory format: run sum = P[y] - P[x] (byte offsets into {P0,P2} / PX)
+  auto pent = [&](int x, int y, int d) { return make_int4(8 * x, 8 * y, 4 * x, fbits((float)(d - RT))); };
+  auto cent = [&](int d, int di, int sg) {
+    return make_int4(4 * ea(d, di), fbits((float)sg), fbits((float)(sg * di)), fbits((float)(sg * (d - RT))));
+  };
   m->full_off.assign(m->H + 1, 0);
   m->chain_off.assign(m->H + 1, 0);
+  m->chain_mid.assign(m->H, 0);
   full.clear();
   chain.clear();
   std::vector<int2> prev;
@@ -195,20 +214,36 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
     for (int d = 0; d < NR; ++d)
       if (cur[d].y >= cur[d].x) full.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
     m->chain_off[k] = (int)chain.size();
+    std::vector<int4> cells;
     if (k % m->period == 0) {
       for (int d = 0; d < NR; ++d)
-        if (cur[d].y >= cur[d].x) chain.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
+        if (cur[d].y >= cur[d].x) chain.push_back(pent(ea(d, cur[d].x), eb(d, cur[d].y), d));
     } else {
-      // run(k) - run(k-1) = (P[eb2] - P[eb1]) + (P[ea1] - P[ea2]) per row (empty run: P[x] - P[x] = 0)
+      // run(k) - run(k-1) per row: cells [lo, hi] entering (sg = +1) or leaving (-1); <= 2 cells become
+      // cell entries, longer spans a prefix entry P[eb(hi)] - P[ea(lo)] (sign by endpoint order)
+      auto span = [&](int d, int lo, int hi, int sg) {
+        if (hi < lo) return;
+        if (hi - lo + 1 <= 2) {
+          for (int di = lo; di <= hi; ++di) cells.push_back(cent(d, di, sg));
+        } else if (sg > 0) {
+          chain.push_back(pent(ea(d, lo), eb(d, hi), d));
+        } else {
+          chain.push_back(pent(eb(d, hi), ea(d, lo), d));
+        }
+      };
       for (int d = 0; d < NR; ++d) {
         const bool e1 = prev[d].y < prev[d].x, e2 = cur[d].y < cur[d].x;
         if (e1 && e2) continue;
-        if (e1) { chain.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0)); continue; }
-        if (e2) { chain.push_back(make_int4(eb(d, prev[d].y), ea(d, prev[d].x), d, 0)); continue; }
-        if (cur[d].x != prev[d].x) chain.push_back(make_int4(ea(d, cur[d].x), ea(d, prev[d].x), d, 0));
-        if (cur[d].y != prev[d].y) chain.push_back(make_int4(eb(d, prev[d].y), eb(d, cur[d].y), d, 0));
+        if (e1) { span(d, cur[d].x, cur[d].y, +1); continue; }
+        if (e2) { span(d, prev[d].x, prev[d].y, -1); continue; }
+        if (cur[d].x < prev[d].x) span(d, cur[d].x, prev[d].x - 1, +1);
+        if (cur[d].x > prev[d].x) span(d, prev[d].x, cur[d].x - 1, -1);
+        if (cur[d].y > prev[d].y) span(d, prev[d].y + 1, cur[d].y, +1);
+        if (cur[d].y < prev[d].y) span(d, cur[d].y + 1, prev[d].y, -1);
       }
     }
+    m->chain_mid[k] = (int)chain.size();
+    chain.insert(chain.end(), cells.begin(), cells.end());
     prev = cur;
   }
   m->full_off[m->H] = (int)full.size();
@@ -246,7 +281,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.out = m->d_out; p.trav = m->d_trav;
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
-  p.full = m->d_full; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off;
+  p.full = m->d_full; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off; p.chain_mid = m->d_chain_mid;
   p.period = m->period;
   p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
@@ -391,6 +426,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       {(void**)&m->d_full_off, m->full_off.size() * sizeof(int), "full offsets"},
       {(void**)&m->d_chain, std::max<size_t>(1, chain.size()) * sizeof(int4), "chain table"},
       {(void**)&m->d_chain_off, m->chain_off.size() * sizeof(int), "chain offsets"},
+      {(void**)&m->d_chain_mid, m->chain_mid.size() * sizeof(int), "chain cell offsets"},
       {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
       {(void**)&m->d_geoc, geoc.size() * sizeof(float4), "geoc"},
       {(void**)&m->d_cs, cs.size() * sizeof(float2), "cs"},
@@ -406,6 +442,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       (e = cudaMemcpyAsync(m->d_full_off, m->full_off.data(), m->full_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_chain, chain.data(), chain.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_chain_off, m->chain_off.data(), m->chain_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_chain_mid, m->chain_mid.data(), m->chain_mid.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_geo, geo.data(), geo.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_geoc, geoc.data(), geoc.size() * sizeof(float4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_cs, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice, m->stream)) ||
@@ -425,7 +462,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
-                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_geo, m->d_geoc,
+                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc};
   for (void* q : ptrs)
     if (q) cudaFree(q);
