@@ -425,7 +425,8 @@ struct Geom {
   // float2 {P0, P2} | float PX | float2 {PV, PVX} | float PVXX (the last two: border / unknown tiles only)
   static constexpr size_t p02_off = raw_bytes, px_off = p02_off + 8 * E;
   static constexpr size_t pv_off = px_off + 4 * E, pvxx_off = pv_off + 8 * E;
-  static constexpr size_t misc_off = (pvxx_off + 4 * E + 15) / 16 * 16;
+  static constexpr size_t hh_off = pvxx_off + 4 * E;  // h^ per halo cell (single-cell chain entries)
+  static constexpr size_t misc_off = (hh_off + 4 * E + 15) / 16 * 16;
   static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
   static size_t bytes(int tab_cap) { return runs_off + (size_t)tab_cap * 16; }
 };
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   float* pxh = reinterpret_cast<float*>(smem + G::px_off);
   float2* pv = reinterpret_cast<float2*>(smem + G::pv_off);
   float* pvxx = reinterpret_cast<float*>(smem + G::pvxx_off);
-  float* hh_s = reinterpret_cast<float*>(smem + G::pv_off);  // interior tiles only (aliases PV)
+  float* hh_s = reinterpret_cast<float*>(smem + G::hh_off);  // h^ (NaN = unknown), stride PW
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
   float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
@@ -583,12 +584,18 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 
   // run entries of this CTA's bins as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj)
   // (interior tiles: the yaw chain table; border tiles: full rows)
-  const int4* tab = fast ? p.chain : p.full;
-  const int* tab_off = fast ? p.chain_off : p.full_off;
+  // run tables of the chunk's bins: the yaw-chain table (shared-memory format) for every tile, and for
+  // border / unknown tiles also the full rows of each bin (the direct path walks whole footprints)
+  const int* tab_off = p.chain_off;
   const int tab_base = __ldg(tab_off + kb);
-  for (int idx = tid; idx < __ldg(tab_off + ke) - tab_base; idx += NTHREADS) {
-    const int4 e = __ldg(tab + tab_base + idx);
-    runs_s[idx] = fast ? e : make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
+  const int n_chain = __ldg(tab_off + ke) - tab_base;
+  const int full_base = __ldg(p.full_off + kb);
+  for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
+  if (!fast) {
+    for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS) {
+      const int4 e = __ldg(p.full + full_base + idx);
+      runs_s[n_chain + idx] = make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
+    }
   }
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
@@ -623,7 +630,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       if (col < HX) {
         P02r[col + 1] = make_float2(o0 + e[c], o2 + e2[c]);
         PXr[col + 1] = ox + ex[c];
-        if (fast) HHr[col] = hh[c];
+        HHr[col] = vv[c] != 0.f ? hh[c] : __int_as_float(0x7fc00000);  // h^, NaN = unknown
       }
     }
     if (!fast) {  // validity moments (exact integers in float)
@@ -693,214 +700,271 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   uint32_t* travk = p.trav + (size_t)kb * twplane;
   uint32_t* travk2 = travk + (size_t)p.H * twplane;
   int kc = kb % p.period;     // position in the yaw chain (restart at 0)
-  for (int k = kb; k < ke; ++k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
-    const int e0 = __ldg(tab_off + k);
-    const int4* rk = runs_s + (e0 - tab_base);
-    const int nr = __ldg(tab_off + k + 1) - e0;
-    const float2 csk = __ldg(p.cs + k);
-    const bool restart = k == kb || kc == 0;
-    if (++kc == p.period) kc = 0;
-    auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
-      if (off >= 0) {  // write-once stream: evict-first stores
-        __stcs(outk + off, make_float4(risk, pitch, roll, z));
-        if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
+  if (fast) {
+    for (int k = kb; k < ke; ++k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
+      const int e0 = __ldg(tab_off + k);
+      const int4* rk = runs_s + (e0 - tab_base);
+      const int nr = __ldg(tab_off + k + 1) - e0;
+      const float2 csk = __ldg(p.cs + k);
+      const bool restart = k == kb || kc == 0;
+      if (++kc == p.period) kc = 0;
+      auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
+        if (off >= 0) {  // write-once stream: evict-first stores
+          __stcs(outk + off, make_float4(risk, pitch, roll, z));
+          if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
+        }
+      };
+      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
+      auto store_trav = [&](int toff, unsigned tmask) {
+        if (toff >= 0) {
+          travk[toff] = tmask;
+          if (p.paired) travk2[toff] = tmask;
+        }
+      };
+      {
+        // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.
+        // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
+        if (restart) {
+  #pragma unroll
+          for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
+        }
+        const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
+  #pragma unroll 2
+        for (int d = 0; d < npre; ++d) {
+          const int4 o = rk[d];
+          const float dj = __int_as_float(o.w);
+          const char* pa8 = b8 + o.x;
+          const char* pb8 = b8 + o.y;
+          const char* pa4 = b4 + o.z;
+          const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
+  #pragma unroll
+          for (int s = 0; s < RPW; ++s) {
+            const float2 A = *reinterpret_cast<const float2*>(pa8 + s * RS8);
+            const float2 B = *reinterpret_cast<const float2*>(pb8 + s * RS8);
+            const float ax = *reinterpret_cast<const float*>(pa4 + s * RS4);
+            const float bxv = *reinterpret_cast<const float*>(pb4 + s * RS4);
+            const float2 dd = sub2(B, A);  // (run sum of h^, run sum of h^2)
+            S02[s] = add2(S02[s], dd);
+            SXH[s] += bxv - ax;  // sum of x' h^ (x' from the tile centre); -xs S0 is applied once below
+            SYH[s] = fmaf(dj, dd.x, SYH[s]);
+          }
+        }
+        // single cells entering / leaving the footprint since bin k-1: one h^ load per state
+  #pragma unroll 2
+        for (int d = npre; d < nr; ++d) {
+          const int4 o = rk[d];
+          const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
+          const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
+          const char* ph = bh + o.x;
+  #pragma unroll
+          for (int s = 0; s < RPW; ++s) {
+            const float h = *reinterpret_cast<const float*>(ph + s * RS4);
+            const float sh = sg * h;
+            S02[s].x += sh;
+            S02[s].y = fmaf(sh, h, S02[s].y);
+            SXH[s] = fmaf(cx, h, SXH[s]);
+            SYH[s] = fmaf(sdj, h, SYH[s]);
+          }
+        }
+        const float4 gc = __ldg(p.geoc + 4 * k), gd = __ldg(p.geoc + 4 * k + 1);
+        const float4 ge = __ldg(p.geoc + 4 * k + 2), gf = __ldg(p.geoc + 4 * k + 3);
+        const float Gq1 = fmaf(Gx, ge.x, Gy * ge.y), Gq2 = fmaf(Gy, ge.x, -Gx * ge.y);
+        const float aG1 = gd.y * Gq1, aG2 = gd.z * Gq2;
+        unsigned tmine = 0;
+  #pragma unroll
+        for (int s = 0; s < RPW; s += 2) {
+          const F2 S0p = pk(S02[s].x, S02[s + 1].x);
+          const StateOut2 o = arrow2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
+                                     pk(SYH[s], SYH[s + 1]),
+                                     pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
+                                     aG1, aG2, gc, gd, ge, gf, p);
+          store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
+          store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
+          const unsigned ma = __ballot_sync(0xffffffffu, soff[s] >= 0 && o.trav_a);
+          const unsigned mb = __ballot_sync(0xffffffffu, soff[s + 1] >= 0 && o.trav_b);
+          if (lane == s) tmine = ma;
+          if (lane == s + 1) tmine = mb;
+        }
+        store_trav(tmy, tmine);  // lane s writes state s's word
       }
-    };
-    // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-    auto store_trav = [&](int toff, unsigned tmask) {
-      if (toff >= 0) {
-        travk[toff] = tmask;
-        if (p.paired) travk2[toff] = tmask;
-      }
-    };
-    auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
-      store_rec(off, risk, pitch, roll, z);
-      const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
-      store_trav(lane == 0 ? toff : -1, tmask);
-    };
-    if (fast) {
-      // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.
-      // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
+    }
+    return;
+  }
+  // ---- border / unknown tile: two states at a time along the whole yaw chunk; per state also the validity
+  // moments (N, sum di, sum dj, sum di^2, sum di dj, sum dj^2), all carried along the yaw chain like the
+  // interior moments (prefix entries with validity prefixes, then single cells: h^ or NaN = unknown)
+#pragma unroll 1
+  for (int sp = 0; sp < RPW; sp += 2) {
+    float2 S02g[2];
+    float SXHg[2], SYHg[2], N[2], Sx[2], Sy[2], Sxx[2], Sxy[2], Syy[2];
+    const int so8 = sp * RS8, so4 = sp * RS4;
+    int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
+#pragma unroll
+    for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
+      if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
+    int kc = kb % p.period;
+#pragma unroll 1
+    for (int k = kb; k < ke; ++k) {
+      const int e0 = __ldg(tab_off + k);
+      const int4* rk = runs_s + (e0 - tab_base);
+      const int nr = __ldg(tab_off + k + 1) - e0;
+      const int npre = __ldg(p.chain_mid + k) - e0;
+      const int f0 = __ldg(p.full_off + k);
+      const int4* rkf = runs_s + n_chain + (f0 - full_base);
+      const int nf = __ldg(p.full_off + k + 1) - f0;
+      const float2 csk = __ldg(p.cs + k);
+      const bool restart = k == kb || kc == 0;
+      if (++kc == p.period) kc = 0;
       if (restart) {
 #pragma unroll
-        for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
+        for (int s = 0; s < 2; ++s) {
+          S02g[s] = make_float2(0.f, 0.f);
+          SXHg[s] = SYHg[s] = N[s] = Sx[s] = Sy[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f;
+        }
       }
-      const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
-#pragma unroll 2
+#pragma unroll 1
       for (int d = 0; d < npre; ++d) {
         const int4 o = rk[d];
         const float dj = __int_as_float(o.w);
-        const char* pa8 = b8 + o.x;
-        const char* pb8 = b8 + o.y;
-        const char* pa4 = b4 + o.z;
-        const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
+        const int ob4 = o.z + ((o.y - o.x) >> 1);
 #pragma unroll
-        for (int s = 0; s < RPW; ++s) {
-          const float2 A = *reinterpret_cast<const float2*>(pa8 + s * RS8);
-          const float2 B = *reinterpret_cast<const float2*>(pb8 + s * RS8);
-          const float ax = *reinterpret_cast<const float*>(pa4 + s * RS4);
-          const float bxv = *reinterpret_cast<const float*>(pb4 + s * RS4);
-          const float2 dd = sub2(B, A);  // (run sum of h^, run sum of h^2)
-          S02[s] = add2(S02[s], dd);
-          SXH[s] += bxv - ax;  // sum of x' h^ (x' from the tile centre); -xs S0 is applied once below
-          SYH[s] = fmaf(dj, dd.x, SYH[s]);
+        for (int s = 0; s < 2; ++s) {
+          const float2 A = *reinterpret_cast<const float2*>(b8 + so8 + o.x + s * RS8);
+          const float2 B = *reinterpret_cast<const float2*>(b8 + so8 + o.y + s * RS8);
+          const float ax = *reinterpret_cast<const float*>(b4 + so4 + o.z + s * RS4);
+          const float bxv = *reinterpret_cast<const float*>(b4 + so4 + ob4 + s * RS4);
+          const float2 VA = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + s * RS8);
+          const float2 VB = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + s * RS8);
+          const float wa = *reinterpret_cast<const float*>(bv4 + so4 + o.z + s * RS4);
+          const float wb = *reinterpret_cast<const float*>(bv4 + so4 + ob4 + s * RS4);
+          const float2 dd = sub2(B, A);
+          const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
+          const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
+          S02g[s] = add2(S02g[s], dd);
+          SXHg[s] += fmaf(-xs, dd.x, bxv - ax);
+          SYHg[s] = fmaf(dj, dd.x, SYHg[s]);
+          N[s] += cnt;
+          Sx[s] += sdi;
+          Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
+          Sy[s] = fmaf(dj, cnt, Sy[s]);
+          Syy[s] = fmaf(dj * dj, cnt, Syy[s]);
+          Sxy[s] = fmaf(dj, sdi, Sxy[s]);
         }
       }
-      // single cells entering / leaving the footprint since bin k-1: one h^ load per state
-#pragma unroll 2
-      for (int d = npre; d < nr; ++d) {
+#pragma unroll 1
+      for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
         const int4 o = rk[d];
-        const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
-        const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
-        const char* ph = bh + o.x;
+        const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
+        const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
 #pragma unroll
-        for (int s = 0; s < RPW; ++s) {
-          const float h = *reinterpret_cast<const float*>(ph + s * RS4);
-          const float sh = sg * h;
-          S02[s].x += sh;
-          S02[s].y = fmaf(sh, h, S02[s].y);
-          SXH[s] = fmaf(cx, h, SXH[s]);
-          SYH[s] = fmaf(sdj, h, SYH[s]);
+        for (int s = 0; s < 2; ++s) {
+          const float h = *reinterpret_cast<const float*>(bh + so4 + o.x + s * RS4);
+          const bool ok = !isnan(h);
+          const float v = ok ? 1.f : 0.f, hv = ok ? h : 0.f;
+          const float sh = sg * hv;
+          S02g[s].x += sh;
+          S02g[s].y = fmaf(sh, hv, S02g[s].y);
+          SXHg[s] = fmaf(sdi, hv, SXHg[s]);
+          SYHg[s] = fmaf(sdj, hv, SYHg[s]);
+          N[s] = fmaf(sg, v, N[s]);
+          Sx[s] = fmaf(sdi, v, Sx[s]);
+          Sy[s] = fmaf(sdj, v, Sy[s]);
+          Sxx[s] = fmaf(cxx, v, Sxx[s]);
+          Sxy[s] = fmaf(cxy, v, Sxy[s]);
+          Syy[s] = fmaf(cyy, v, Syy[s]);
         }
       }
-      const float4 gc = __ldg(p.geoc + 4 * k), gd = __ldg(p.geoc + 4 * k + 1);
-      const float4 ge = __ldg(p.geoc + 4 * k + 2), gf = __ldg(p.geoc + 4 * k + 3);
-      const float Gq1 = fmaf(Gx, ge.x, Gy * ge.y), Gq2 = fmaf(Gy, ge.x, -Gx * ge.y);
-      const float aG1 = gd.y * Gq1, aG2 = gd.z * Gq2;
-      unsigned tmine = 0;
-#pragma unroll
-      for (int s = 0; s < RPW; s += 2) {
-        const F2 S0p = pk(S02[s].x, S02[s + 1].x);
-        const StateOut2 o = arrow2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
-                                   pk(SYH[s], SYH[s + 1]),
-                                   pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
-                                   aG1, aG2, gc, gd, ge, gf, p);
-        store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
-        store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
-        const unsigned ma = __ballot_sync(0xffffffffu, soff[s] >= 0 && o.trav_a);
-        const unsigned mb = __ballot_sync(0xffffffffu, soff[s + 1] >= 0 && o.trav_b);
-        if (lane == s) tmine = ma;
-        if (lane == s + 1) tmine = mb;
-      }
-      store_trav(tmy, tmine);  // lane s writes state s's word
-    } else {
-      // ---- border / unknown tile: also the validity moments (N, sum di, sum di^2, ...), two states at a time
-#pragma unroll 1
-      for (int sp = 0; sp < RPW; sp += 2) {
-        float2 S02[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        float SXH[2] = {0.f, 0.f}, SYH[2] = {0.f, 0.f}, N[2] = {0.f, 0.f}, Sx[2] = {0.f, 0.f}, Sy[2] = {0.f, 0.f};
-        float Sxx[2] = {0.f, 0.f}, Sxy[2] = {0.f, 0.f}, Syy[2] = {0.f, 0.f};
-        const int so8 = sp * RS8, so4 = sp * RS4;
-#pragma unroll 1
-        for (int d = 0; d < nr; ++d) {
-          const int4 o = rk[d];
-          const float dj = __int_as_float(o.w);
-          const int ob4 = o.z + ((o.y - o.x) >> 1);
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const float2 A = *reinterpret_cast<const float2*>(b8 + so8 + o.x + s * RS8);
-            const float2 B = *reinterpret_cast<const float2*>(b8 + so8 + o.y + s * RS8);
-            const float ax = *reinterpret_cast<const float*>(b4 + so4 + o.z + s * RS4);
-            const float bxv = *reinterpret_cast<const float*>(b4 + so4 + ob4 + s * RS4);
-            const float2 VA = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + s * RS8);
-            const float2 VB = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + s * RS8);
-            const float wa = *reinterpret_cast<const float*>(bv4 + so4 + o.z + s * RS4);
-            const float wb = *reinterpret_cast<const float*>(bv4 + so4 + ob4 + s * RS4);
-            const float2 dd = sub2(B, A);
-            const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
-            const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
-            S02[s] = add2(S02[s], dd);
-            SXH[s] += fmaf(-xs, dd.x, bxv - ax);
-            SYH[s] = fmaf(dj, dd.x, SYH[s]);
-            N[s] += cnt;
-            Sx[s] += sdi;
-            Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
-            Sy[s] = fmaf(dj, cnt, Sy[s]);
-            Syy[s] = fmaf(dj * dj, cnt, Syy[s]);
-            Sxy[s] = fmaf(dj, sdi, Sxy[s]);
-          }
+      float4* outk = p.out + (size_t)k * plane;
+      float4* outk2 = p.out + (size_t)(k + p.H) * plane;
+      uint32_t* travk = p.trav + (size_t)k * twplane;
+      uint32_t* travk2 = p.trav + (size_t)(k + p.H) * twplane;
+      auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
+        if (off >= 0) {
+          __stcs(outk + off, make_float4(risk, pitch, roll, z));
+          if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
         }
-        const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
-        const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
-        Cov2 cv = cov_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), shl, shh, pk(S02[0].x, S02[1].x),
-                              pk(S02[0].y, S02[1].y), pk(SXH[0], SXH[1]), pk(SYH[0], SYH[1]),
-                              pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
-        int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
-#pragma unroll
-        for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
-          if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
-        // (states outside the window are not stored: they never take the direct path)
-        const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
-        const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
-        StateOut1 dres[2];
-        if (need0 | need1) {
-          // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
-          // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
-          const float m0[2] = {lo(cv.zz), hi(cv.zz)};
-          float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            unsigned msk = s ? need1 : need0;
-            while (msk) {
-              const int src = __ffs(msk) - 1;
-              msk &= msk - 1;
-              const float mu = __shfl_sync(0xffffffffu, m0[s], src);
-              const float* rb = raw + (warp + (sp + s) * NWARPS) * HX + src;  // state's halo row, column src
-              float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
-#pragma unroll 1
-              for (int d = 0; d < nr; ++d) {
-                const int4 o = rk[d];
-                const float dj = __int_as_float(o.w);
-                const int dr = (int)dj + R_T;  // stencil row -> halo row offset
-                const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
-                for (int c = c0 + lane; c < c1; c += 32) {
-                  const float hv = rb[dr * HX + c];
-                  if (!isnan(hv)) {
-                    const float dv = hv - mu;
-                    a0 += dv;
-                    a2 = fmaf(dv, dv, a2);
-                    ax = fmaf((float)(c - R_T), dv, ax);
-                    ay = fmaf(dj, dv, ay);
+        const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
+        if (lane == 0 && toff >= 0) {
+          travk[toff] = tmask;
+          if (p.paired) travk2[toff] = tmask;
+        }
+      };
+          const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
+          const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
+          Cov2 cv = cov_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), shl, shh, pk(S02g[0].x, S02g[1].x),
+                                pk(S02g[0].y, S02g[1].y), pk(SXHg[0], SXHg[1]), pk(SYHg[0], SYHg[1]),
+                                pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
+          // (states outside the window are not stored: they never take the direct path)
+          const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
+          const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
+          StateOut1 dres[2];
+          if (need0 | need1) {
+            // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
+            // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
+            const float m0[2] = {lo(cv.zz), hi(cv.zz)};
+            float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
+  #pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              unsigned msk = s ? need1 : need0;
+              while (msk) {
+                const int src = __ffs(msk) - 1;
+                msk &= msk - 1;
+                const float mu = __shfl_sync(0xffffffffu, m0[s], src);
+                const float* rb = raw + (warp + (sp + s) * NWARPS) * HX + src;  // state's halo row, column src
+                float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
+  #pragma unroll 1
+                for (int d = 0; d < nf; ++d) {
+                  const int4 o = rkf[d];
+                  const float dj = __int_as_float(o.w);
+                  const int dr = (int)dj + R_T;  // stencil row -> halo row offset
+                  const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
+                  for (int c = c0 + lane; c < c1; c += 32) {
+                    const float hv = rb[dr * HX + c];
+                    if (!isnan(hv)) {
+                      const float dv = hv - mu;
+                      a0 += dv;
+                      a2 = fmaf(dv, dv, a2);
+                      ax = fmaf((float)(c - R_T), dv, ax);
+                      ay = fmaf(dj, dv, ay);
+                    }
                   }
                 }
+  #pragma unroll
+                for (int w = 16; w >= 1; w >>= 1) {
+                  a0 += __shfl_xor_sync(0xffffffffu, a0, w);
+                  a2 += __shfl_xor_sync(0xffffffffu, a2, w);
+                  ax += __shfl_xor_sync(0xffffffffu, ax, w);
+                  ay += __shfl_xor_sync(0xffffffffu, ay, w);
+                }
+                if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
               }
-#pragma unroll
-              for (int w = 16; w >= 1; w >>= 1) {
-                a0 += __shfl_xor_sync(0xffffffffu, a0, w);
-                a2 += __shfl_xor_sync(0xffffffffu, a2, w);
-                ax += __shfl_xor_sync(0xffffffffu, ax, w);
-                ay += __shfl_xor_sync(0xffffffffu, ay, w);
+            }
+            // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
+  #pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              if (s ? dh : dl) {
+                const double dN = N[s], iN = 1.0 / dN, r = p.r;
+                const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
+                const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
+                             c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
+                const double r2n = r * r * iN * iN;
+                dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
+                                      r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
+                                      (double)m0[s] + md, csk,
+                                      make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
+                                      make_float3(p.wk, p.wx, p.wy));
               }
-              if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
             }
           }
-          // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            if (s ? dh : dl) {
-              const double dN = N[s], iN = 1.0 / dN, r = p.r;
-              const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
-              const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
-                           c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
-              const double r2n = r * r * iN * iN;
-              dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
-                                    r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
-                                    (double)m0[s] + md, csk,
-                                    make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
-                                    make_float3(p.wk, p.wx, p.wy));
-            }
-          }
-        }
-        const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
-                                         shh.ok, 0.f, 0.f, csk, p);
-        // (store() holds a warp ballot: select first, store uniformly)
-        StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
-        StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
-        if (dl) ra = dres[0];
-        if (dh) rb = dres[1];
-        store(so0, st0, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
-        store(so1, st1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
-      }
+          const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
+                                           shh.ok, 0.f, 0.f, csk, p);
+          // (store() holds a warp ballot: select first, store uniformly)
+          StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
+          StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
+          if (dl) ra = dres[0];
+          if (dh) rb = dres[1];
+          store(so0, st0, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
+          store(so1, st1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
     }
   }
 }

@@ -657,7 +657,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   int cap = 1;
   for (int kb = m->k_lo; kb < m->k_hi; kb += chunk) {
     const int ke = std::min(kb + chunk, m->k_hi);
-    cap = std::max(cap, std::max(m->full_off[ke] - m->full_off[kb], m->chain_off[ke] - m->chain_off[kb]));
+    cap = std::max(cap, (m->full_off[ke] - m->full_off[kb]) + (m->chain_off[ke] - m->chain_off[kb]));
   }
   p.tab_cap = cap;
   if (n_tiles > 0 && nk > 0) {
