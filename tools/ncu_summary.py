@@ -100,6 +100,10 @@ def main():
         "sm_frequency_ghz": ("GPU Speed Of Light Throughput", "SM Frequency"),
     }
     s = {k: num(d.get(v, ("", ""))[0]) for k, v in pick.items()}
+    dur, unit = d.get(pick["duration_ms"], ("", ""))
+    scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
+    if num(dur) is not None and unit in scale:  # ncu prints the unit it chose (us or ms)
+        s["duration_ms"] = num(dur) * scale[unit]
     rw = raw(a.rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
                      "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                      "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
