@@ -253,19 +253,19 @@ __device__ __forceinline__ StateOut2 arrow2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zre
   const F2 pp = p2 * ip;
   const F2 det = fma2(b1, fma2(b2, b3, neg2(E22)), neg2(E11 * b2));   // det(M - I/3)
   const F2 hr = det * ((ip * ip) * (ip * bc(0.5f)));                  // det((M - I/3) / p) / 2
-  const F2 phi = acos2(hr) * third;
-  float sl, cl, sh, ch;
-  __sincosf(lo(phi), &sl, &cl);
-  __sincosf(hi(phi), &sh, &ch);
-  F2 lam = fma2(neg2(pp), fma2(bc(1.73205080756887729f), pk(sl, sh), pk(cl, ch)), third);
+  // lam0 = 1/3 + 2 p cos(phi + 2 pi / 3), phi = acos(hr) / 3 (one MUFU.COS)
+  const F2 phi = fma2(acos2(hr), third, bc(2.09439510239319549f));
+  F2 lam = fma2(pp + pp, pk(__cosf(lo(phi)), __cosf(hi(phi))), third);
   // one Newton step on the secular equation: lam += f / (1 + t1^2 + t2^2), t_i = E_i / (A_i - lam)
-  {
-    const F2 t1 = E1 * rcp2(A1 - lam), t2 = E2 * rcp2(A2 - lam);
-    const F2 f = fma2(neg2(E1), t1, fma2(neg2(E2), t2, D - lam));
-    const F2 fp = fma2(t1, t1, fma2(t2, t2, bc(1.f)));
-    lam = fma2(f, rcp2(fp), lam);
-  }
-  const F2 x = neg2(E1 * rcp2(A1 - lam)), y = neg2(E2 * rcp2(A2 - lam));  // normal ~ (x, y, 1)
+  const F2 r1 = rcp2(A1 - lam), r2 = rcp2(A2 - lam);
+  const F2 t1 = E1 * r1, t2 = E2 * r2;
+  const F2 f = fma2(neg2(E1), t1, fma2(neg2(E2), t2, D - lam));
+  const F2 fp = fma2(t1, t1, fma2(t2, t2, bc(1.f)));
+  const F2 dl = f * rcp2(fp);
+  lam = lam + dl;
+  // 1 / (A_i - lam - dl) = r_i / (1 - r_i dl) ~ r_i (1 + r_i dl): the relative error (r_i dl)^2 ~ (dl / gap)^2
+  // is below FP32 rounding wherever the eigenvector is well conditioned
+  const F2 x = neg2(t1 * fma2(r1, dl, bc(1.f))), y = neg2(t2 * fma2(r2, dl, bc(1.f)));  // normal ~ (x, y, 1)
   const F2 kap = pk(fmaxf(0.f, lo(lam)), fmaxf(0.f, hi(lam)));
   // Eqs. 2-3 reduced (as in solve2) for the unnormalised normal n = (x q1 + y q2, 1): u = n.e, t = n.e'
   const F2 u = fma2(x, bc(ge.z), y * bc(ge.w));
