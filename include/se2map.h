@@ -151,6 +151,16 @@ se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, f
  * Synchronises. */
 se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
 
+/* The same compact map without its redundant half: Risk and traversability are pi-periodic in theta
+ * (bins k and k + n_yaw/2 have the same footprint and pitch / roll of opposite sign, and Alg. 1 uses only
+ * their absolute values: PAPER.md:145-151, readings R13 / R23), so for even n_yaw only the n_rep =
+ * n_yaw / 2 representative planes are written — plane k serves bins k and k + n_rep — with the layout of
+ * se2m_download_compact (n_rep instead of n_yaw planes; odd n_yaw: all planes).  Host destinations are
+ * filled ASYNCHRONOUSLY from double-buffered device staging on the map's copy stream, so the transfer
+ * overlaps the next update / assess; the buffers may be read after se2m_synchronize.  Device
+ * destinations are written on the map's stream. */
+se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+
 /* NEXT-1: integrate one LiDAR frame into the elevation window (§V.A, Fig. 3):
  * points (n x 3 float, sensor frame; host or device per mem) are transformed with the pose, points
  * outside the window or outside the body-frame height band are ignored, each point gets the
@@ -216,7 +226,7 @@ se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, in
  * tile row TJ = floor(J / TY) to rank TJ mod world_size). */
 se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_t* tile_y);
 
-/* Block until all work queued on the handle's stream is done. */
+/* Block until all work queued on the handle's streams (its stream and its copy stream) is done. */
 se2m_status se2m_synchronize(se2m_map* m);
 
 /* Kernel launches issued by this handle since creation (for the bench's gpu_launches). */

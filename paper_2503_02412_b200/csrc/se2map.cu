@@ -81,6 +81,12 @@ struct se2m_map {
   CUtensorMap tmap_in;
   bool tma_in_ok = false;
   bool inpaint_valid = false;
+  // se2m_download_compact_rep: copy stream, double-buffered staging, events (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_gathered[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
+  char* d_rep[2] = {nullptr, nullptr};
+  size_t rep_bytes = 0;
+  int rep_slot = 0;
   bool force_general = false;  // a full stencil is degenerate (R22): every tile takes the general path
   bool have_data = false;
   bool all_dirty = true;
@@ -467,6 +473,15 @@ extern "C" void se2m_destroy(se2m_map* m) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (m->h_ipc) cudaFreeHost(m->h_ipc);
+  if (m->copy_stream) {
+    cudaStreamSynchronize(m->copy_stream);
+    cudaStreamDestroy(m->copy_stream);
+  }
+  for (int b = 0; b < 2; ++b) {
+    if (m->d_rep[b]) cudaFree(m->d_rep[b]);
+    if (m->ev_gathered[b]) cudaEventDestroy(m->ev_gathered[b]);
+    if (m->ev_copied[b]) cudaEventDestroy(m->ev_copied[b]);
+  }
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -830,6 +845,56 @@ extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint
   return SE2M_OK;
 }
 
+extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact_rep: bad mem");
+  const int wpr = (m->prm.nx + 31) / 32;
+  const int n_rep = m->paired ? m->H : m->prm.n_yaw;
+  const size_t plane = (size_t)m->prm.nx * m->prm.ny;
+  const size_t rb = risk_q ? plane * n_rep * 2 : 0, bb = trav_bits ? (size_t)n_rep * m->prm.ny * wpr * 4 : 0;
+  if (!rb && !bb) return SE2M_OK;
+  AssessParams p = make_params(m);
+  p.n_yaw = n_rep;  // planes [0, n_rep): the representative bins (or all bins when n_yaw is odd)
+  const int klo = m->k_lo, khi = m->k_hi;  // owned representative bins (others: 65535 / 0)
+  if (mem == SE2M_MEM_DEVICE) {
+    CUDA_TRY(m, launch_gather_compact(p, klo, khi, risk_q, trav_bits, wpr, m->stream), "gather_compact");
+    m->launches++;
+    return SE2M_OK;
+  }
+  if (!m->copy_stream) {
+    CUDA_TRY(m, cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate(copy)");
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_gathered[b], cudaEventDisableTiming), "cudaEventCreate");
+      CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_copied[b], cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  if (m->rep_bytes < rb + bb) {
+    CUDA_TRY(m, cudaStreamSynchronize(m->copy_stream), "sync(copy stream)");
+    CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync");
+    for (int b = 0; b < 2; ++b) {
+      if (m->d_rep[b]) cudaFree(m->d_rep[b]);
+      m->d_rep[b] = nullptr;
+    }
+    m->rep_bytes = 0;
+    for (int b = 0; b < 2; ++b) CUDA_TRY(m, cudaMalloc(&m->d_rep[b], rb + bb), "cudaMalloc(rep staging)");
+    m->rep_bytes = rb + bb;
+  }
+  const int b = m->rep_slot;
+  m->rep_slot ^= 1;
+  uint16_t* dr = risk_q ? reinterpret_cast<uint16_t*>(m->d_rep[b]) : nullptr;
+  uint32_t* db = trav_bits ? reinterpret_cast<uint32_t*>(m->d_rep[b] + rb) : nullptr;
+  // staging b is reused only after its previous D2H finished; the D2H waits for the gather
+  CUDA_TRY(m, cudaStreamWaitEvent(m->stream, m->ev_copied[b], 0), "wait(copied)");
+  CUDA_TRY(m, launch_gather_compact(p, klo, khi, dr, db, wpr, m->stream), "gather_compact");
+  m->launches++;
+  CUDA_TRY(m, cudaEventRecord(m->ev_gathered[b], m->stream), "record(gathered)");
+  CUDA_TRY(m, cudaStreamWaitEvent(m->copy_stream, m->ev_gathered[b], 0), "wait(gathered)");
+  if (risk_q) CUDA_TRY(m, cudaMemcpyAsync(risk_q, dr, rb, cudaMemcpyDeviceToHost, m->copy_stream), "D2H risk_q");
+  if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->copy_stream), "D2H bits");
+  CUDA_TRY(m, cudaEventRecord(m->ev_copied[b], m->copy_stream), "record(copied)");
+  return SE2M_OK;
+}
+
 // ---- NEXT-1: LiDAR frame integration --------------------------------------------------------------------
 extern "C" se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int64_t n, const se2m_pose* pose,
                                            int32_t mem, int64_t* out_counts) {
@@ -1091,6 +1156,7 @@ extern "C" se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* 
 extern "C" se2m_status se2m_synchronize(se2m_map* m) {
   if (!m) return SE2M_ERR_INVALID_ARG;
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "synchronize");
+  if (m->copy_stream) CUDA_TRY(m, cudaStreamSynchronize(m->copy_stream), "synchronize(copy stream)");
   return SE2M_OK;
 }
 

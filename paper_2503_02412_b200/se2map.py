@@ -31,7 +31,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
-           "se2m_download_inpainted"]
+           "se2m_download_inpainted", "se2m_download_compact_rep"]
 
 
 class Params(ctypes.Structure):
@@ -87,6 +87,7 @@ _lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
 _lib.se2m_integrate_scan.argtypes = [_vp, _vp, _i64, ctypes.POINTER(Pose), _i32, _vp]
 _lib.se2m_download_elevation.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_inpaint.argtypes = [_vp]
+_lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
@@ -283,6 +284,24 @@ class Se2Map:
             raise ValueError("both outputs must be host or both device")
         mem = mem if out.get("risk_q") is not None else mem2
         self._check(_lib.se2m_download_compact(self.h, rp, bp, mem))
+        return out
+
+    def download_compact_rep(self, out=None):
+        """Representative planes only (Risk and traversability are pi-periodic in theta: plane k serves bins k
+        and k + n_yaw/2).  Host outputs (pinned, for overlap) are filled asynchronously: call synchronize()
+        before reading them."""
+        P = self.params
+        n_rep = P.n_yaw // 2 if P.n_yaw % 2 == 0 else P.n_yaw
+        wpr = (P.nx + 31) // 32
+        if out is None:
+            out = {"risk_q": np.empty((n_rep, P.ny, P.nx), np.uint16),
+                   "trav_bits": np.empty((n_rep, P.ny, wpr), np.uint32)}
+        rp, mem, k1 = _ptr_nocopy(out.get("risk_q"))
+        bp, mem2, k2 = _ptr_nocopy(out.get("trav_bits"))
+        if out.get("risk_q") is not None and out.get("trav_bits") is not None and mem != mem2:
+            raise ValueError("both outputs must be host or both device")
+        mem = mem if out.get("risk_q") is not None else mem2
+        self._check(_lib.se2m_download_compact_rep(self.h, rp, bp, mem))
         return out
 
     def compute_sdf(self, d_max: float = 2.0):

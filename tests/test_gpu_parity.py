@@ -169,3 +169,32 @@ def test_download_compact_matches_download(nx, ny, robot):
     t[:, :, :nx] = g["trav"]
     exp_bits = (t.reshape(-1, ny, wpr, 32) << np.arange(32, dtype=np.uint64)).sum(-1).astype(np.uint32)
     assert np.array_equal(c["trav_bits"], exp_bits)
+
+
+@pytest.mark.parametrize("n_yaw", [36, 9])
+def test_download_compact_rep_is_the_pi_periodic_half(n_yaw):
+    """Representative planes (R13 / R23): risk and traversability of bins k and k + n/2 are identical, so
+    the rep download equals the first n/2 planes of the full compact download AND its second half;
+    asynchronous host copies into two buffers in flight, read after synchronize(); device destinations."""
+    import torch
+    cfg = dict(CONFIGS["paper"], n_yaw=n_yaw)
+    m, h, g, orc, rep = run_config(cfg=cfg)
+    full = m.download_compact()
+    n_rep = n_yaw // 2 if n_yaw % 2 == 0 else n_yaw
+    outs = []
+    for _ in range(2):
+        outs.append({"risk_q": torch.empty((n_rep, 100, 100), dtype=torch.int16).pin_memory(),
+                     "trav_bits": torch.empty((n_rep, 100, 4), dtype=torch.int32).pin_memory()})
+        m.download_compact_rep(out=outs[-1])
+    m.synchronize()
+    for o in outs:
+        rq = o["risk_q"].numpy().view(np.uint16)
+        tb = o["trav_bits"].numpy().view(np.uint32)
+        assert np.array_equal(rq, full["risk_q"][:n_rep]) and np.array_equal(tb, full["trav_bits"][:n_rep])
+        if n_yaw % 2 == 0:
+            assert np.array_equal(rq, full["risk_q"][n_rep:]) and np.array_equal(tb, full["trav_bits"][n_rep:])
+    dev = {"risk_q": torch.empty((n_rep, 100, 100), dtype=torch.int16, device="cuda"),
+           "trav_bits": torch.empty((n_rep, 100, 4), dtype=torch.int32, device="cuda")}
+    m.download_compact_rep(out=dev)
+    m.synchronize()
+    assert np.array_equal(dev["risk_q"].cpu().numpy().view(np.uint16), full["risk_q"][:n_rep])
