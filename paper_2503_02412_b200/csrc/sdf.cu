@@ -3,11 +3,17 @@
 // "the distance to the edge of the nearest region, with negative values inside obstacles"); reading R24:
 // centre-to-centre Euclidean distance to the nearest cell of the other class, clamped to +-d_max.
 //
-// Exact within d_max: one CTA per 32 x 32 tile of one layer loads the class of every cell of the tile
-// plus a W = ceil(d_max / r) halo into shared memory, computes per column the distance (in rows) to the
-// nearest obstacle / free cell within W (separable first pass of an EDT), then per cell the minimum of
-// dx^2 + g(x + dx)^2 over |dx| <= W with early exit once dx^2 exceeds the best (second pass).  The
-// column distances come from per-column bit masks (ffs / clz), O(1) per entry.
+// Exact within d_max by the separable Euclidean distance transform, in two kernels over whole layers:
+//   sdf_cols_kernel  one thread per (column, 128-row segment): a downward and an upward sweep over the
+//                    segment plus W = ceil(d_max / r) rows on each side give, per cell, the row distance
+//                    to the nearest obstacle and to the nearest free cell of its column (255 beyond W);
+//                    the class bit of a column is one word load + shift per row (consecutive threads =
+//                    consecutive columns: the words are shared);
+//   sdf_rows_kernel  one thread per cell: min over |dx| <= W of dx^2 + g(x + dx)^2 with g the column
+//                    distance to the other class (squares staged in shared memory, "none" = a large
+//                    sentinel, so the loop is branch-free), stopping once dx^2 reaches the best; a
+//                    row-prefix count of the columns that have such a cell within W rejects cells with
+//                    none in O(1).
 #include <math.h>
 #include <stdint.h>
 
@@ -15,120 +21,134 @@
 
 namespace se2m {
 
-constexpr int SDF_T = 32;
-constexpr int SDF_THREADS = 256;
+constexpr int SDF_SEG = 128;    // rows per column-pass thread
+constexpr int SDF_ROWT = 256;   // columns per row-pass CTA
 
-__global__ void __launch_bounds__(SDF_THREADS) sdf_kernel(const SdfParams p) {
-  extern __shared__ unsigned char sm[];
-  const int W = p.W, RW = SDF_T + 2 * W;  // region width / height
-  unsigned char* cls = sm;                 // [RW][RW]: 0 free, 1 obstacle, 2 outside the window
-  unsigned char* gO = cls + RW * RW;       // [SDF_T][RW]: rows to the nearest obstacle in the column (255 none)
-  unsigned char* gF = gO + SDF_T * RW;     // ... to the nearest free cell
-  const int tiles_x = (p.nx + SDF_T - 1) / SDF_T;
-  const int i0 = (blockIdx.x % tiles_x) * SDF_T, j0 = (blockIdx.x / tiles_x) * SDF_T;
-  const int L = blockIdx.y;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < RW * RW; idx += SDF_THREADS) {
-    const int rj = idx / RW, ri = idx - rj * RW;
-    const int i = i0 - W + ri, j = j0 - W + rj;
-    unsigned char c = 2;
-    if (i >= 0 && i < p.nx && j >= 0 && j < p.ny) {
-      if (p.trav) {
-        int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
-        const long long I = p.I_M + i;
-        const long long g = I >= 0 ? I / 32 : -((-I + 31) / 32);
-        const int w = (int)(((g % p.trav_words) + p.trav_words) % p.trav_words);
-        const uint32_t word = p.trav[((size_t)L * p.ny + py) * p.trav_words + w];
-        c = ((word >> (int)(I - g * 32)) & 1u) ? 0 : 1;  // traversable -> free, Risk = 1 -> obstacle
-      } else {
-        c = p.mask[((size_t)L * p.ny + j) * p.nx + i] ? 1 : 0;
-      }
-    }
-    cls[idx] = c;
+__global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = blockIdx.z;
+  if (i >= p.nx) return;
+  const int j0 = blockIdx.y * SDF_SEG, j1 = min(p.ny, j0 + SDF_SEG);
+  const int W = p.W;
+  // class source of column i: map mode = one bit of a traversable word per row (physical rows, ring
+  // order: the pointer wraps at ny); mask mode = one byte per row
+  const uint32_t* tw = nullptr;
+  int bit = 0;
+  size_t tstride = 0;
+  if (p.trav) {
+    const long long I = p.I_M + i;
+    const long long gI = I >= 0 ? I / 32 : -((-I + 31) / 32);
+    const int wpos = (int)(((gI % p.trav_words) + p.trav_words) % p.trav_words);
+    bit = (int)(I - gI * 32);
+    tw = p.trav + (size_t)L * p.ny * p.trav_words + wpos;
+    tstride = p.trav_words;
   }
-  __syncthreads();
-  // pass 1: per region column a bit mask over the region's rows of obstacle / free cells (one thread per
-  // column), then per (tile row, column) the distance to the nearest set bit by ffs / clz (O(1))
-  uint64_t* mO = reinterpret_cast<uint64_t*>(((uintptr_t)(gF + SDF_T * RW) + 7) & ~(uintptr_t)7);
-  const int NWd = (RW + 63) >> 6;          // 64-bit words per column mask (<= 4 for W <= 96)
-  uint64_t* mF = mO + (size_t)RW * NWd;
-  for (int c = tid; c < RW; c += SDF_THREADS) {
-    for (int w = 0; w < NWd; ++w) {
-      uint64_t o = 0, f = 0;
-      for (int b = 0; b < 64; ++b) {
-        const int rr = w * 64 + b;
-        if (rr >= RW) break;
-        const unsigned char v = cls[rr * RW + c];
-        o |= (uint64_t)(v == 1) << b;
-        f |= (uint64_t)(v == 0) << b;
-      }
-      mO[c * NWd + w] = o;
-      mF[c * NWd + w] = f;
-    }
-  }
-  __syncthreads();
-  auto nearest = [&](const uint64_t* m, int r) {  // rows from row r to the nearest set bit, 255 beyond W
-    const int w = r >> 6, b = r & 63;
-    int up = 1 << 20, dn = 1 << 20;
-    const uint64_t x = m[w] >> b;
-    if (x) up = __ffsll((long long)x) - 1;
-    else
-      for (int w2 = w + 1; w2 < NWd; ++w2)
-        if (m[w2]) { up = w2 * 64 + __ffsll((long long)m[w2]) - 1 - r; break; }
-    const uint64_t y = m[w] << (63 - b);
-    if (y) dn = __clzll((long long)y);
-    else
-      for (int w2 = w - 1; w2 >= 0; --w2)
-        if (m[w2]) { dn = r - (w2 * 64 + 63 - __clzll((long long)m[w2])); break; }
-    const int d = min(up, dn);
-    return d <= W ? d : 255;
+  const uint8_t* mk = p.mask ? p.mask + (size_t)L * p.ny * p.nx + i : nullptr;
+  auto obstacle = [&](int j, int py) -> int {
+    return tw ? (int)(((__ldg(tw + py * tstride) >> bit) & 1u) ^ 1u) : (__ldg(mk + (size_t)j * p.nx) ? 1 : 0);
   };
-  for (int idx = tid; idx < SDF_T * RW; idx += SDF_THREADS) {
-    const int ty = idx / RW, c = idx - ty * RW;
-    gO[ty * RW + c] = (unsigned char)nearest(mO + c * NWd, ty + W);
-    gF[ty * RW + c] = (unsigned char)nearest(mF + c * NWd, ty + W);
+  uint16_t* g = p.g + (size_t)L * p.ny * p.nx + i;  // (dO | dF << 8) per cell, logical [j][i]
+  // downward: rows since the last obstacle / free cell, from W rows above the segment
+  int dO = 255, dF = 255;
+  int j = max(0, j0 - W);
+  int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+  for (; j < j1; ++j) {
+    const int ob = obstacle(j, py);
+    dO = ob ? 0 : min(dO + 1, 255);
+    dF = ob ? min(dF + 1, 255) : 0;
+    if (j >= j0) g[(size_t)j * p.nx] = (uint16_t)(dO | (dF << 8));
+    if (++py == p.ny) py = 0;
+  }
+  // upward, from W rows below the segment; keep the nearer one, clamp beyond W
+  dO = dF = 255;
+  j = min(p.ny, j1 + W) - 1;
+  py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+  for (; j >= j0; --j) {
+    const int ob = obstacle(j, py);
+    dO = ob ? 0 : min(dO + 1, 255);
+    dF = ob ? min(dF + 1, 255) : 0;
+    if (j < j1) {
+      const uint16_t v = g[(size_t)j * p.nx];
+      int o = min(dO, (int)(v & 0xff)), f = min(dF, (int)(v >> 8));
+      if (o > W) o = 255;
+      if (f > W) f = 255;
+      g[(size_t)j * p.nx] = (uint16_t)(o | (f << 8));
+    }
+    if (--py < 0) py = p.ny - 1;
+  }
+}
+
+__global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
+  extern __shared__ unsigned char sm[];
+  const int W = p.W, RW = SDF_ROWT + 2 * W;
+  int* g2O = reinterpret_cast<int*>(sm);          // [RW] dO^2 (kFar: none within W / outside)
+  int* g2F = g2O + RW;                            // [RW] dF^2
+  unsigned short* cO = reinterpret_cast<unsigned short*>(g2F + RW);  // [RW + 1] prefix counts of dO <= W
+  unsigned short* cF = cO + RW + 1;                                  // ... of dF <= W
+  constexpr int kFar = 1 << 24;
+  const int L = blockIdx.z, j = blockIdx.y, x0 = blockIdx.x * SDF_ROWT - W;
+  const uint16_t* grow = p.g + ((size_t)L * p.ny + j) * p.nx;
+  for (int c = threadIdx.x; c < RW; c += SDF_ROWT) {
+    const int x = x0 + c;
+    const uint16_t v = (x >= 0 && x < p.nx) ? grow[x] : (uint16_t)0xffff;  // outside the window: no cell
+    const int o = v & 0xff, f = v >> 8;
+    g2O[c] = o != 255 ? o * o : kFar;
+    g2F[c] = f != 255 ? f * f : kFar;
   }
   __syncthreads();
-  // pass 2: per tile cell, nearest cell of the other class
-  for (int idx = tid; idx < SDF_T * SDF_T; idx += SDF_THREADS) {
-    const int ty = idx / SDF_T, tx = idx - ty * SDF_T;
-    const int i = i0 + tx, j = j0 + ty;
-    if (i >= p.nx || j >= p.ny) continue;
-    const int c = tx + W;
-    const unsigned char self = cls[(ty + W) * RW + c];
-    const unsigned char* g = (self == 1 ? gF : gO) + ty * RW;
-    int best = 0x7fffffff;
-    for (int dx = 0; dx <= W && dx * dx < best; ++dx) {
-      const int a = g[c - dx], b = g[c + dx];
-      if (a != 255) best = min(best, dx * dx + a * a);
-      if (b != 255) best = min(best, dx * dx + b * b);
+  if (threadIdx.x < 64) {  // two warps: inclusive prefix counts along the region row (sequential chunks)
+    const int lane = threadIdx.x & 31, which = threadIdx.x >> 5;
+    unsigned short* cnt = which ? cF : cO;
+    const int* g2 = which ? g2F : g2O;
+    const int chunk = (RW + 31) / 32, c0 = min(RW, lane * chunk), c1 = min(RW, c0 + chunk);
+    int run = 0;
+    for (int c = c0; c < c1; ++c) run += g2[c] != kFar;
+    int incl = run;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
     }
-    float d = best == 0x7fffffff ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
-    if (self == 1) d = -d;
-    size_t o;
-    if (p.trav) {
-      int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
-      int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
-      o = ((size_t)L * p.ny + py) * p.nx + px;
-    } else {
-      o = ((size_t)L * p.ny + j) * p.nx + i;
+    int acc = incl - run;
+    if (lane == 0) cnt[0] = 0;
+    for (int c = c0; c < c1; ++c) {
+      acc += g2[c] != kFar;
+      cnt[c + 1] = (unsigned short)acc;
     }
-    p.out[o] = d;
   }
+  __syncthreads();
+  const int x = x0 + W + threadIdx.x;
+  if (x >= p.nx) return;
+  const int c = W + threadIdx.x;
+  const bool obst = g2O[c] == 0;          // own row distance to an obstacle is 0: the cell is one
+  const int* g2 = obst ? g2F : g2O;       // distance to the other class
+  const unsigned short* cnt = obst ? cF : cO;
+  int best = kFar;
+  if (cnt[c + W + 1] != cnt[c - W]) {     // some column within W has a cell of the other class
+    best = g2[c];
+    for (int dx = 1, dx2 = 1; dx <= W && dx2 < best; dx2 += 2 * dx + 1, ++dx)
+      best = min(best, dx2 + min(g2[c - dx], g2[c + dx]));
+  }
+  float d = best >= kFar ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
+  if (obst) d = -d;
+  size_t o;
+  if (p.trav) {
+    int px = p.pxM + x; if (px >= p.nx) px -= p.nx;
+    int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
+    o = ((size_t)L * p.ny + py) * p.nx + px;
+  } else {
+    o = ((size_t)L * p.ny + j) * p.nx + x;
+  }
+  p.out[o] = d;
 }
 
 cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   if (p.layers <= 0 || p.nx <= 0 || p.ny <= 0) return cudaSuccess;
-  const int RW = SDF_T + 2 * p.W;
-  const size_t smem = (size_t)RW * RW + 2 * (size_t)SDF_T * RW + 8 + 2 * (size_t)RW * ((RW + 63) / 64) * 8;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(sdf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  const int tiles = ((p.nx + SDF_T - 1) / SDF_T) * ((p.ny + SDF_T - 1) / SDF_T);
-  sdf_kernel<<<dim3(tiles, p.layers), SDF_THREADS, smem, s>>>(p);
+  sdf_cols_kernel<<<dim3((p.nx + 127) / 128, (p.ny + SDF_SEG - 1) / SDF_SEG, p.layers), 128, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int RW = SDF_ROWT + 2 * p.W;
+  const size_t smem = (size_t)RW * 8 + 2 * (size_t)(RW + 1) * 2;
+  sdf_rows_kernel<<<dim3((p.nx + SDF_ROWT - 1) / SDF_ROWT, p.ny, p.layers), SDF_ROWT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

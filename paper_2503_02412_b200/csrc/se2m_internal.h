@@ -138,6 +138,9 @@ struct SdfParams {
   const uint8_t* mask;
   // output: map mode -> physical ring layout [layer][py][px]; mask mode -> logical [layer][j][i]
   float* out;
+  // scratch: per cell the column distances (rows) to the nearest obstacle / free cell, (dO | dF << 8),
+  // logical [layer][j][i]
+  uint16_t* g;
 };
 cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s);
 

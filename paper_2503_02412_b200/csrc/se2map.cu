@@ -48,6 +48,7 @@ struct se2m_map {
   float4* d_out = nullptr;  // state records [k][ny][nx] (risk, pitch, roll, z), ring layout
   uint32_t* d_trav = nullptr;
   float* d_sdf = nullptr;    // NEXT-2: SDF layers (representative bins), ring layout
+  uint16_t* d_sdf_g = nullptr;  // NEXT-2 scratch: column distances
   float* d_var = nullptr;    // NEXT-1: cell height variance, ring layout like d_h
   FrontendScratch fe{};
   float* d_pts = nullptr;
@@ -469,7 +470,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
                   m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
-                  m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc};
+                  m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc, m->d_sdf_g};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (m->h_ipc) cudaFreeHost(m->h_ipc);
@@ -1031,6 +1032,7 @@ extern "C" se2m_status se2m_compute_sdf(se2m_map* m, double d_max) {
   if (!m->have_data) return fail(m, SE2M_ERR_STATE, "compute_sdf before any assess");
   const size_t plane = (size_t)m->prm.nx * m->prm.ny;
   if (!m->d_sdf) CUDA_TRY(m, cudaMalloc(&m->d_sdf, plane * m->H * sizeof(float)), "cudaMalloc(sdf)");
+  if (!m->d_sdf_g) CUDA_TRY(m, cudaMalloc(&m->d_sdf_g, plane * m->H * sizeof(uint16_t)), "cudaMalloc(sdf scratch)");
   SdfParams sp;
   memset(&sp, 0, sizeof sp);
   sp.nx = m->prm.nx; sp.ny = m->prm.ny; sp.layers = m->k_hi - m->k_lo;
@@ -1039,8 +1041,9 @@ extern "C" se2m_status se2m_compute_sdf(se2m_map* m, double d_max) {
   sp.trav_words = m->trav_words; sp.pxM = pmod(m->I_M, m->prm.nx); sp.pyM = pmod(m->J_M, m->prm.ny);
   sp.I_M = m->I_M;
   sp.out = m->d_sdf + plane * m->k_lo;
-  CUDA_TRY(m, launch_sdf(sp, m->stream), "sdf kernel");
-  m->launches++;
+  sp.g = m->d_sdf_g;
+  CUDA_TRY(m, launch_sdf(sp, m->stream), "sdf kernels");
+  m->launches += 2;
   m->sdf_valid = true;
   m->sdf_dmax = d_max;
   return SE2M_OK;
@@ -1068,9 +1071,16 @@ extern "C" se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32
   memset(&sp, 0, sizeof sp);
   sp.nx = nx; sp.ny = ny; sp.layers = layers; sp.r = (float)resolution; sp.d_max = (float)d_max; sp.W = W;
   sp.mask = dm; sp.out = dout;
+  uint16_t* dg = nullptr;
+  if (e == cudaSuccess && cudaMalloc(&dg, n * sizeof(uint16_t)) != cudaSuccess) {
+    if (mem == SE2M_MEM_HOST) { cudaFree(dm); cudaFree(dout); }
+    return fail(nullptr, SE2M_ERR_OOM, "cudaMalloc(sdf scratch)");
+  }
+  sp.g = dg;
   if (e == cudaSuccess) e = launch_sdf(sp, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess && mem == SE2M_MEM_HOST) e = cudaMemcpy(out, dout, n * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dg);
   if (mem == SE2M_MEM_HOST) { cudaFree(dm); cudaFree(dout); }
   return e == cudaSuccess ? SE2M_OK : fail(nullptr, SE2M_ERR_CUDA, cudaGetErrorString(e));
 }

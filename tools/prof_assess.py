@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
     ap.add_argument("--holes", type=float, default=0.0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--sdf", type=float, default=0.0, help="also time compute_sdf(d_max) after the assess")
     ap.add_argument("--scan", action="store_true",
                     help="the bench's paper_pipeline map instead: 180x180x30 built from 4 LiDAR frames")
     a = ap.parse_args()
@@ -60,9 +61,19 @@ def main():
         m.assess_se2(0)
         m.synchronize()
         ts.append(time.perf_counter() - t)
-    print(json.dumps(dict(config=a.config, holes=a.holes, unknown_frac=0.0 if known is None else
-                          float(1 - known.mean()), ms_median=1e3 * float(np.median(ts)),
-                          ms_min=1e3 * float(np.min(ts)))))
+    res = dict(config=a.config, holes=a.holes, unknown_frac=0.0 if known is None else float(1 - known.mean()),
+               ms_median=1e3 * float(np.median(ts)), ms_min=1e3 * float(np.min(ts)))
+    if a.sdf > 0:
+        m.compute_sdf(a.sdf)
+        m.synchronize()
+        ts = []
+        for _ in range(a.reps):
+            t = time.perf_counter()
+            m.compute_sdf(a.sdf)
+            m.synchronize()
+            ts.append(time.perf_counter() - t)
+        res["sdf_ms_median"] = 1e3 * float(np.median(ts))
+    print(json.dumps(res))
 
 
 def scan_map(a, Se2Map):
