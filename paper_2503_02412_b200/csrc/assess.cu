@@ -121,19 +121,28 @@ __device__ __forceinline__ F2 acos2(F2 x) {
   const F2 r = sqrt2abs(bc(1.f) - a) * pz;  // acos(|x|)
   return bc(kPi2) - copysign2(bc(kPi2) - r, x);
 }
-// asin on [-1, 1], branch-free and odd: asin(x) = sign(x) (pi/2 - sqrt(1 - |x|) P7(|x|)) (A&S 4.4.46,
-// |error| <= 2e-8 in exact arithmetic, ~1.2e-7 absolute in FP32 near 0).  P7(0) is set to the FP32 pi/2
-// so that asin(0) = 0 exactly (flat terrain gives exactly zero pitch and roll, pin Q1).
+// asin on [-1, 1], branch-free and odd: asin(x) = sign(x) (pi/2 - sqrt(1 - |x|) P(|x|)).  P(0) is the
+// FP32 pi/2 so that asin(0) = 0 exactly (flat terrain gives exactly zero pitch and roll, pin Q1).
 __device__ __forceinline__ F2 asin2(F2 x) {
+  // degree-5 minimax fit of (acos(a) / sqrt(1 - a) - pi/2) / a on [0, 1] (constant term pinned to the
+  // FP32 pi/2): |error| <= 9e-7 rad evaluated in FP32, two FFMA2 fewer than A&S 4.4.46
   const F2 a = abs2(x);
-  F2 pz = fma2(bc(-0.0012624911f), a, bc(0.0066700901f));
-  pz = fma2(pz, a, bc(-0.0170881256f));
-  pz = fma2(pz, a, bc(0.0308918810f));
-  pz = fma2(pz, a, bc(-0.0501743046f));
-  pz = fma2(pz, a, bc(0.0889789874f));
-  pz = fma2(pz, a, bc(-0.2145988016f));
+  F2 pz = fma2(bc(-0.005068998f), a, bc(0.021005174f));
+  pz = fma2(pz, a, bc(-0.046262898f));
+  pz = fma2(pz, a, bc(0.088295855f));
+  pz = fma2(pz, a, bc(-0.214561f));
   pz = fma2(pz, a, bc(kPi2));
   return copysign2(fma2(neg2(sqrt2abs(bc(1.f) - a)), pz, bc(kPi2)), x);
+}
+// acos for the arrowhead solver's seed only (polished by a Newton step): degree-4 fit, |error| <= 6e-6
+__device__ __forceinline__ F2 acos2_seed(F2 x) {
+  const F2 a = abs2(x);
+  F2 pz = fma2(bc(0.010058168f), a, bc(-0.038249232f));
+  pz = fma2(pz, a, bc(0.086035036f));
+  pz = fma2(pz, a, bc(-0.21436888f));
+  pz = fma2(pz, a, bc(kPi2));
+  const F2 r = sqrt2abs(bc(1.f) - a) * pz;  // acos(|x|)
+  return bc(kPi2) - copysign2(bc(kPi2) - r, x);
 }
 
 struct StateOut2 {
@@ -254,7 +263,7 @@ __device__ __forceinline__ StateOut2 arrow2(F2 S0, F2 S2, F2 SXH, F2 SYH, F2 zre
   const F2 det = fma2(b1, fma2(b2, b3, neg2(E22)), neg2(E11 * b2));   // det(M - I/3)
   const F2 hr = det * ((ip * ip) * (ip * bc(0.5f)));                  // det((M - I/3) / p) / 2
   // lam0 = 1/3 + 2 p cos(phi + 2 pi / 3), phi = acos(hr) / 3 (one MUFU.COS)
-  const F2 phi = fma2(acos2(hr), third, bc(2.09439510239319549f));
+  const F2 phi = fma2(acos2_seed(hr), third, bc(2.09439510239319549f));
   F2 lam = fma2(pp + pp, pk(__cosf(lo(phi)), __cosf(hi(phi))), third);
   // one Newton step on the secular equation: lam += f / (1 + t1^2 + t2^2), t_i = E_i / (A_i - lam)
   const F2 r1 = rcp2(A1 - lam), r2 = rcp2(A2 - lam);
