@@ -22,6 +22,12 @@
 
 #include "se2m_internal.h"
 
+#ifndef SE2M_UNROLL_PRE
+#define SE2M_UNROLL_PRE 2
+#endif
+#ifndef SE2M_UNROLL_CELL
+#define SE2M_UNROLL_CELL 2
+#endif
 #ifndef SE2M_MINB
 #define SE2M_MINB(R_T) 2
 #endif
@@ -106,6 +112,7 @@ __device__ __forceinline__ F2 copysign2(F2 m, F2 sg) { return pk(copysignf(lo(m)
 __device__ __forceinline__ F2 sel2(bool cl, bool ch, F2 a, F2 b) { return pk(cl ? lo(a) : lo(b), ch ? hi(a) : hi(b)); }
 
 constexpr float kPi2 = 1.57079632679489662f;
+constexpr int kUnrollPre = SE2M_UNROLL_PRE, kUnrollCell = SE2M_UNROLL_CELL;  // interior moment loops
 
 // acos on [-1, 1] (Abramowitz & Stegun 4.4.46: acos(a) = sqrt(1 - a) P7(a), a in [0, 1]),
 // branch-free: acos(x) = pi/2 - sign(x) (pi/2 - acos(|x|)).  |1 - a| absorbs a 1-ulp overshoot.
@@ -738,7 +745,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
         }
         const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
-  #pragma unroll 2
+#pragma unroll kUnrollPre
         for (int d = 0; d < npre; ++d) {
           const int4 o = rk[d];
           const float dj = __int_as_float(o.w);
@@ -759,7 +766,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           }
         }
         // single cells entering / leaving the footprint since bin k-1: one h^ load per state
-  #pragma unroll 2
+#pragma unroll kUnrollCell
         for (int d = npre; d < nr; ++d) {
           const int4 o = rk[d];
           const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
