@@ -441,8 +441,10 @@ struct Geom {
   // float2 {P0, P2} | float PX | float2 {PV, PVX} | float PVXX (the last two: border / unknown tiles only)
   static constexpr size_t p02_off = raw_bytes, px_off = p02_off + 8 * E;
   static constexpr size_t pv_off = px_off + 4 * E, pvxx_off = pv_off + 8 * E;
-  static constexpr size_t hh_off = pvxx_off + 4 * E;  // h^ per halo cell (single-cell chain entries)
-  static constexpr size_t misc_off = (hh_off + 4 * E + 15) / 16 * 16;
+  static constexpr bool CB = chain_border(R_T);      // border tiles on the yaw chain (separate h^ plane)
+  // h^ per halo cell (single-cell chain entries); at R_T = 32 it aliases PV (interior tiles only)
+  static constexpr size_t hh_off = CB ? pvxx_off + 4 * E : pv_off;
+  static constexpr size_t misc_off = ((CB ? hh_off : pvxx_off) + 4 * E + 15) / 16 * 16;
   static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
   static size_t bytes(int tab_cap) { return runs_off + (size_t)tab_cap * 16; }
 };
@@ -604,7 +606,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   // border / unknown tiles also the full rows of each bin (the direct path walks whole footprints)
   const int* tab_off = p.chain_off;
   const int tab_base = __ldg(tab_off + kb);
-  const int n_chain = __ldg(tab_off + ke) - tab_base;
+  const int n_chain = (fast || G::CB) ? __ldg(tab_off + ke) - tab_base : 0;
   const int full_base = __ldg(p.full_off + kb);
   for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
   if (!fast) {
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       if (col < HX) {
         P02r[col + 1] = make_float2(o0 + e[c], o2 + e2[c]);
         PXr[col + 1] = ox + ex[c];
-        HHr[col] = vv[c] != 0.f ? hh[c] : __int_as_float(0x7fc00000);  // h^, NaN = unknown
+        if (G::CB || fast) HHr[col] = vv[c] != 0.f ? hh[c] : __int_as_float(0x7fc00000);  // h^, NaN = unknown
       }
     }
     if (!fast) {  // validity moments (exact integers in float)
@@ -821,15 +823,16 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     int kc = kb % p.period;
 #pragma unroll 1
     for (int k = kb; k < ke; ++k) {
-      const int e0 = __ldg(tab_off + k);
-      const int4* rk = runs_s + (e0 - tab_base);
-      const int nr = __ldg(tab_off + k + 1) - e0;
-      const int npre = __ldg(p.chain_mid + k) - e0;
       const int f0 = __ldg(p.full_off + k);
       const int4* rkf = runs_s + n_chain + (f0 - full_base);
       const int nf = __ldg(p.full_off + k + 1) - f0;
+      // the yaw chain, or (R_T = 32) the full rows of every bin as prefix entries
+      const int e0 = G::CB ? __ldg(tab_off + k) : 0;
+      const int4* rk = G::CB ? runs_s + (e0 - tab_base) : rkf;
+      const int nr = G::CB ? __ldg(tab_off + k + 1) - e0 : nf;
+      const int npre = G::CB ? __ldg(p.chain_mid + k) - e0 : nf;
       const float2 csk = __ldg(p.cs + k);
-      const bool restart = k == kb || kc == 0;
+      const bool restart = k == kb || kc == 0 || !G::CB;
       if (++kc == p.period) kc = 0;
       if (restart) {
 #pragma unroll
@@ -992,13 +995,28 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
   static int configured_bytes = 0;
   if ((int)smem > configured_bytes) {
     cudaError_t e = cudaFuncSetAttribute(assess_kernel<R_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      cudaGetLastError();  // not sticky: leave no stale error for the next call
+      return e;
+    }
     configured_bytes = (int)smem;
   }
   const int nk = p.k_end - p.k_begin;
   dim3 grid(n_tiles, (nk + p.k_chunk - 1) / p.k_chunk);
   assess_kernel<R_T><<<grid, NTHREADS, smem, stream>>>(p, *tmap);
   return cudaGetLastError();
+}
+
+size_t assess_smem_bytes(int R_T, int tab_cap) {
+  switch (R_T) {
+    case 4: return Geom<4>::bytes(tab_cap);
+    case 8: return Geom<8>::bytes(tab_cap);
+    case 12: return Geom<12>::bytes(tab_cap);
+    case 16: return Geom<16>::bytes(tab_cap);
+    case 24: return Geom<24>::bytes(tab_cap);
+    case 32: return Geom<32>::bytes(tab_cap);
+    default: return 0;
+  }
 }
 
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {

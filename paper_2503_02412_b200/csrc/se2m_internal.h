@@ -16,6 +16,10 @@ constexpr int NWARPS = NTHREADS / 32;
 #define SE2M_TY_SMALL 32
 #endif
 constexpr int tile_rows(int R_T) { return R_T <= 12 ? SE2M_TY_SMALL : 16; }
+// shared-memory layout choice of the assess kernel: up to R_T = 24 the h^ plane is separate and border
+// tiles also run on the yaw chain (both run tables in shared memory); at R_T = 32 the plane aliases the
+// validity prefixes (interior tiles only) and border tiles take the full rows of every bin
+constexpr bool chain_border(int R_T) { return R_T <= 24; }
 
 // Stencil radii the assess kernel is instantiated for (R_T >= the footprint radius R).
 constexpr int kRadii[] = {4, 8, 12, 16, 24, 32};
@@ -76,6 +80,8 @@ struct AssessParams {
 };
 
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.
+// dynamic shared memory of one assess CTA (halo, prefix planes, h^ plane, run tables of tab_cap entries)
+size_t assess_smem_bytes(int R_T, int tab_cap);
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
                           cudaStream_t stream);
 

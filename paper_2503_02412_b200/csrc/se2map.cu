@@ -74,6 +74,7 @@ struct se2m_map {
   size_t q_cap = 0;
   CUtensorMap tmap;
   bool tma_ok = false;
+  int smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the device
   // NEXT-4: nearest-neighbour inpainted view (ring layout like d_h), allocated on first use
   float* d_hin = nullptr;
   int* d_site = nullptr;
@@ -461,6 +462,11 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     return bail(SE2M_ERR_CUDA);
   }
   m->tma_ok = make_tensor_map(m, &m->tmap, m->d_h);
+  {
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device) == cudaSuccess && optin > 0)
+      m->smem_optin = optin;
+  }
   *out = m;
   return SE2M_OK;
 }
@@ -669,12 +675,23 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   }
   chunk = std::max(1, chunk);
   if (m->period > 1) chunk = std::min(nk, (chunk + m->period - 1) / m->period * m->period);  // chain-aligned
-  p.k_chunk = chunk;
+  // run tables of a chunk must fit the CTA's shared memory next to the tile planes: large footprints take
+  // fewer bins per CTA (whole chain periods)
   int cap = 1;
-  for (int kb = m->k_lo; kb < m->k_hi; kb += chunk) {
-    const int ke = std::min(kb + chunk, m->k_hi);
-    cap = std::max(cap, (m->full_off[ke] - m->full_off[kb]) + (m->chain_off[ke] - m->chain_off[kb]));
+  for (;;) {
+    cap = 1;
+    for (int kb = m->k_lo; kb < m->k_hi; kb += chunk) {
+      const int ke = std::min(kb + chunk, m->k_hi);
+      const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
+      cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
+    }
+    const int step = m->period > 1 ? m->period : 1;
+    if (assess_smem_bytes(m->R_T, cap) <= (size_t)m->smem_optin || chunk <= step) break;
+    chunk = std::max(step, (chunk / 2 + step - 1) / step * step);
   }
+  if (assess_smem_bytes(m->R_T, cap) > (size_t)m->smem_optin)
+    return fail(m, SE2M_ERR_UNSUPPORTED, "assess: footprint tables exceed the shared memory of a CTA");
+  p.k_chunk = chunk;
   p.tab_cap = cap;
   if (n_tiles > 0 && nk > 0) {
     cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream);

@@ -54,3 +54,38 @@ def test_fullsize_sampled_parity(name):
     print(name, rep)
     assert rep["ok"], rep
     assert rep["normal"] > 0.95 * rep["n"]
+
+
+@pytest.mark.parametrize("ex,ey,holes", [(1.15, 0.7, 0.0), (1.55, 1.05, 0.0), (1.15, 0.7, 0.03)])
+def test_chain_map_big_footprints_sampled_parity(ex, ey, holes):
+    """Yaw-chain maps (>= 512^2 cells: period-9 chain, single-cell entries) with footprints of radius 23
+    and 31 cells at 0.05 m (kernel tiles R_T = 24 and 32, TY = 16), with and without unknown blobs
+    (border / unknown tiles on the chain with validity moments), against the oracle on sampled states."""
+    nx, ny, r, n_yaw = 560, 528, 0.05, 72
+    terrain = CONFIGS["highres"]["terrain"]
+    robot = (-7.31, 4.43)
+    m = make_map(nx, ny, r, n_yaw, ex=ex, ey=ey, robot=robot)
+    I_M, J_M = m.origin()
+    h = world_heights(terrain, I_M, J_M, nx, ny, r)
+    known = None
+    if holes:
+        rng = np.random.default_rng(5)
+        known = np.ones((ny, nx), np.uint8)
+        nb = int(holes * nx * ny / 49)
+        cj, ci = rng.integers(0, ny - 7, nb), rng.integers(0, nx - 7, nb)
+        for dj in range(7):
+            for di in range(7):
+                known[cj + dj, ci + di] = 0
+    m.update_elevation(h, known)
+    m.assess_se2(0)
+    R = m.stencil_info(0)[1]
+    assert R >= 22
+    ijk = _samples(nx, ny, n_yaw, R, np.random.default_rng(23), n_uniform=12000, n_edge=4000)
+    x = (I_M + ijk[:, 0] + 0.5) * r
+    y = (J_M + ijk[:, 1] + 0.5) * r
+    th = -math.pi + 2 * math.pi * ijk[:, 2] / n_yaw
+    q = m.query(np.stack([x, y, th], axis=1))
+    orc = oracle.assess_states(oracle_params(nx, ny, r, n_yaw, ex, ey), h, ijk, known=known)
+    rep = compare({k: q[k] for k in ("risk", "pitch", "roll", "z", "trav")}, orc)
+    print(ex, ey, holes, rep)
+    assert rep["ok"], rep
