@@ -172,6 +172,16 @@ def cpu_oracle_rate(cfg, h, budget_s=15.0, seed=0, nthreads=None):
     return done / t_tot, done, t_tot, nthreads
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -386,15 +396,18 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         h = world_heights(cfg["terrain"], *m.origin(), nx, ny, r)
         rate, n_done, secs, thr = cpu_oracle_rate(cfg, h, budget_s=float(os.environ.get("BENCH_CPU_S", "15")))
+        rate1, n1, secs1, _ = cpu_oracle_rate(cfg, h, budget_s=2.0, seed=1, nthreads=1)
         cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": "%d uniform random (i,j,k) states of the %s window (FP64 C oracle, %.1f s)"
-                         % (n_done, args.config, secs)}
+                         % (n_done, args.config, secs),
+               "single_thread_value": rate1, "cpu_model": cpu_model()}
 
     extras = {}
     if not args.no_extras and world == 1:
         extras = small_configs(S, stream, torch)
         extras.update(next_rows(m, stream, torch, cfg))
         extras.update(paper_pipeline(S, stream, torch))
+        extras.update(highres_update(S, stream, torch))
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -409,6 +422,8 @@ def main():
                        "step": "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
                                "query(%d states)" % args.queries},
             "ms_per_full_update": kern_s / K * 1e3,
+            "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
+            "ms_per_full_update_p10_p50_p90": [float(np.percentile(kern_ms, q)) for q in (10, 50, 90)],
             "gpu_launches": int(launches), "clocks": clocks, "roofline": roofline, "e2e": e2e,
             "cpu_baseline": cpu, "extras": extras,
             "setup": {"terrain_gen_s": round(gen_s, 2)}}
@@ -455,6 +470,33 @@ def next_rows(m, stream, torch, cfg, d_max=2.0, n_queries=1 << 20):
     out["inpaint_ms"] = (time.perf_counter() - t0) / 5 * 1e3
     out["inpaint_note"] = "se2m_inpaint on the bench map, host wall clock incl. its counter read-back"
     return out
+
+
+def highres_update(S, stream, torch, reps=10):
+    """BASELINE.json's other large config (800 x 800 @ 0.05 m x 72 bins = 46 M states, footprint radius
+    16 cells): device time of one FULL assess, median over reps."""
+    cfg = CONFIGS["highres"]
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
+                 robot_x=cfg["robot"][0], robot_y=cfg["robot"][1], cuda_stream=stream.cuda_stream)
+    h = world_heights(cfg["terrain"], *m.origin(), nx, ny, r)
+    with torch.cuda.stream(stream):
+        m.update_elevation(h)
+        for _ in range(3):
+            m.assess_se2(0)
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            m.assess_se2(0)
+            e1.record(stream)
+            ts.append((e0, e1))
+        stream.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in ts)
+    m.close()
+    n = nx * ny * n_yaw
+    return {"highres_ms": ms[len(ms) // 2], "highres_states": n, "highres_states_per_s": n / (ms[len(ms) // 2] * 1e-3),
+            "highres_W_ops_per_state": 4 * stencil_cells(cfg) + 200}
 
 
 def paper_pipeline(S, stream, torch, n_frames=6, n_iters=40, warm=4):
