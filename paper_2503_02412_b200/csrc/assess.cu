@@ -726,11 +726,10 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const float2 csk = __ldg(p.cs + k);
       const bool restart = k == kb || kc == 0;
       if (++kc == p.period) kc = 0;
+      // interior tiles lie inside the window (their whole halo does), so every state is stored
       auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
-        if (off >= 0) {  // write-once stream: evict-first stores
-          __stcs(outk + off, make_float4(risk, pitch, roll, z));
-          if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
-        }
+        __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
+        if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
       };
       // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
       auto store_trav = [&](int toff, unsigned tmask) {
@@ -798,8 +797,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
                                      aG1, aG2, gc, gd, ge, gf, p);
           store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
           store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
-          const unsigned ma = __ballot_sync(0xffffffffu, soff[s] >= 0 && o.trav_a);
-          const unsigned mb = __ballot_sync(0xffffffffu, soff[s + 1] >= 0 && o.trav_b);
+          const unsigned ma = __ballot_sync(0xffffffffu, o.trav_a);
+          const unsigned mb = __ballot_sync(0xffffffffu, o.trav_b);
           if (lane == s) tmine = ma;
           if (lane == s + 1) tmine = mb;
         }
