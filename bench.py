@@ -601,12 +601,9 @@ def small_configs(S, stream, torch):
                 for t in range(1, len(path)):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                    di, dj = m.shift_window(*path[t])
-                    I_M, J_M = m.origin()
-                    for (i0, j0, w, hh) in exposed_strips(di, dj, nx, ny):
-                        m.update_elevation(wh[J_M - J0 + j0:J_M - J0 + j0 + hh, I_M - I0 + i0:I_M - I0 + i0 + w],
-                                           i0=i0, j0=j0)
-                    m.assess_se2(1)
+                    # H1 + H2 + H9 in one call (se2m_step): recentre, fill the entered cells from the
+                    # device-resident world patch, INCREMENTAL assess
+                    m.step(*path[t], wh, I0, J0)
                     e1.record(stream)
                     if t > warm:
                         ts.append((e0, e1))

@@ -130,6 +130,17 @@ se2m_status se2m_shift_window(se2m_map* m, double robot_x, double robot_y, int32
  * SE2M_ERR_STATE if no elevation was ever written. */
 se2m_status se2m_assess_se2(se2m_map* m, int32_t mode);
 
+/* One rolling-window step against a larger device-resident source map, H1 + H2 + H9 in one call (two
+ * kernel launches): recentre on (x, y) as se2m_shift_window (Eq. 4), write the cells
+ * that entered the window from `world` — a device plane of heights covering world cells
+ * [world_I0, world_I0 + world_w) x [world_J0, world_J0 + world_h), leading dimension world_ld
+ * (elements), NaN = unknown; window cells outside it become unknown — and assess INCREMENTAL.
+ * mem must be SE2M_MEM_DEVICE.  Same results as shift_window + update_elevation(strips) +
+ * assess_se2(INCREMENTAL), bit for bit.  Optional out_di / out_dj as in se2m_shift_window. */
+se2m_status se2m_step(se2m_map* m, double x, double y, const float* world, int64_t world_ld,
+                      int64_t world_I0, int64_t world_J0, int32_t world_w, int32_t world_h, int32_t mem,
+                      int32_t* out_di, int32_t* out_dj);
+
 /* n world-frame queries xyt[3*q + {0,1,2}] = (x, y, theta): the state of the window cell
  * containing (x, y) at the nearest yaw bin (reading R3/R6).  Any output pointer may be NULL;
  * outputs are host memory of n entries.  Entries outside the window (or of yaw bins this

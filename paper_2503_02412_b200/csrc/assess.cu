@@ -1051,6 +1051,28 @@ cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt,
   return cudaGetLastError();
 }
 
+__global__ void fill_strips_kernel(const FillArgs f) {
+  const int4 rc = f.rect[blockIdx.z];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+  if (i >= rc.z || j >= rc.w) return;
+  const int li = rc.x + i, lj = rc.y + j;  // logical window cell
+  const long long wi = f.I_M + li - f.wI0, wj = f.J_M + lj - f.wJ0;
+  float v = __int_as_float(0x7fc00000);
+  if (wi >= 0 && wi < f.ww && wj >= 0 && wj < f.wh) v = __ldg(f.world + wj * f.world_ld + wi);
+  int px = f.pxM + li; if (px >= f.nx) px -= f.nx;
+  int py = f.pyM + lj; if (py >= f.ny) py -= f.ny;
+  f.h[(size_t)py * f.ldh + px] = v;
+  if (f.var) f.var[(size_t)py * f.ldh + px] = f.prior_var;
+}
+
+cudaError_t launch_fill_strips(const FillArgs& f, cudaStream_t s) {
+  int w = 0, hgt = 0;
+  for (int q = 0; q < f.n; ++q) { w = max(w, f.rect[q].z); hgt = max(hgt, f.rect[q].w); }
+  if (w <= 0 || hgt <= 0) return cudaSuccess;
+  fill_strips_kernel<<<dim3((w + 127) / 128, hgt, f.n), 128, 0, s>>>(f);
+  return cudaGetLastError();
+}
+
 __global__ void scatter_rect_kernel(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
                                     int w, int hgt, const float* __restrict__ src, long long ld,
                                     const uint8_t* __restrict__ known) {

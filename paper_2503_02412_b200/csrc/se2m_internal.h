@@ -86,6 +86,21 @@ cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUt
                           cudaStream_t stream);
 
 // Small helpers (same file as the kernels).
+// se2m_step: the window cells that entered (up to 2 logical rectangles (i0, j0, w, h)) from a device
+// plane of world heights covering [wI0, wI0 + ww) x [wJ0, wJ0 + wh) (NaN = unknown; outside: unknown)
+struct FillArgs {
+  float* h;
+  float* var;
+  float prior_var;
+  int ldh, nx, ny, pxM, pyM;
+  long long I_M, J_M;
+  const float* world;
+  long long world_ld, wI0, wJ0;
+  int ww, wh;
+  int n;
+  int4 rect[2];
+};
+cudaError_t launch_fill_strips(const FillArgs& f, cudaStream_t s);
 cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt, int nx, int ny,
                               cudaStream_t s);
 cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,

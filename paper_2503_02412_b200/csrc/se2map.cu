@@ -528,52 +528,98 @@ extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0
   return SE2M_OK;
 }
 
-extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_t* out_di, int32_t* out_dj) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
-  if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "shift_window: position not finite");
+// Eq. 4 recentre shared by se2m_shift_window and se2m_step: moves the origin, records the dirty strips
+// (H9) and returns the logical rectangles (i0, j0, w, h) of the window that entered (n_strips <= 2;
+// *all = the whole window was replaced).  Launches nothing.
+static void recentre(se2m_map* m, double x, double y, long long* pdi, long long* pdj, int4 strips[2],
+                     int* n_strips, bool* all) {
   const int nx = m->prm.nx, ny = m->prm.ny;
   // Eq. 4: p_M = l_res * floor(x / l_res); window origin = floor(x/r) - nx/2
   const long long I_M = (long long)floor(x / m->prm.resolution) - nx / 2;
   const long long J_M = (long long)floor(y / m->prm.resolution) - ny / 2;
   const long long di = I_M - m->I_M, dj = J_M - m->J_M;
-  if (out_di) *out_di = (int32_t)std::max<long long>(INT32_MIN, std::min<long long>(INT32_MAX, di));
-  if (out_dj) *out_dj = (int32_t)std::max<long long>(INT32_MIN, std::min<long long>(INT32_MAX, dj));
-  if (di == 0 && dj == 0) return SE2M_OK;
+  *pdi = di; *pdj = dj; *n_strips = 0; *all = false;
+  if (di == 0 && dj == 0) return;
   const Rect old_w{m->I_M, m->I_M + nx, m->J_M, m->J_M + ny};
   const Rect new_w{I_M, I_M + nx, J_M, J_M + ny};
   m->I_M = I_M;
   m->J_M = J_M;
-  const int pxM = pmod(I_M, nx), pyM = pmod(J_M, ny);
-  if (std::llabs(di) >= nx || std::llabs(dj) >= ny) {
-    // displacement >= side: every cell leaves the window
-    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, 0, 0, nx, ny, nx, ny, m->stream), "clear");
-    m->launches++;
+  m->inpaint_valid = false;
+  if (std::llabs(di) >= nx || std::llabs(dj) >= ny) {  // displacement >= side: every cell leaves
+    *all = true;
+    strips[0] = make_int4(0, 0, nx, ny);
+    *n_strips = 1;
     m->all_dirty = true;
     m->dirty.clear();
-    m->inpaint_valid = false;
-    return SE2M_OK;
+    return;
   }
-  // cells entering the window (their physical slots held cells that left): set unknown.
-  // Column strip: logical columns [nx - di, nx) if di > 0, [0, -di) if di < 0, all rows.
+  // column strip: logical columns [nx - di, nx) if di > 0, [0, -di) if di < 0, all rows; row strip alike
   if (di != 0) {
     const int w = (int)std::llabs(di);
-    const int l0 = di > 0 ? nx - w : 0;
-    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, (pxM + l0) % nx, pyM, w, ny, nx, ny, m->stream), "clear cols");
-    m->launches++;
+    strips[(*n_strips)++] = make_int4(di > 0 ? nx - w : 0, 0, w, ny);
   }
   if (dj != 0) {
     const int hgt = (int)std::llabs(dj);
-    const int l0 = dj > 0 ? ny - hgt : 0;
-    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, pxM, (pyM + l0) % ny, nx, hgt, nx, ny, m->stream), "clear rows");
-    m->launches++;
+    strips[(*n_strips)++] = make_int4(0, dj > 0 ? ny - hgt : 0, nx, hgt);
   }
-  m->inpaint_valid = false;
   // dirty: the entered strips of the new window and the vacated strips of the old one (H9)
   if (di > 0) { m->dirty.push_back(Rect{old_w.I1, new_w.I1, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{old_w.I0, new_w.I0, old_w.J0, old_w.J1}); }
   if (di < 0) { m->dirty.push_back(Rect{new_w.I0, old_w.I0, new_w.J0, new_w.J1}); m->dirty.push_back(Rect{new_w.I1, old_w.I1, old_w.J0, old_w.J1}); }
   if (dj > 0) { m->dirty.push_back(Rect{new_w.I0, new_w.I1, old_w.J1, new_w.J1}); m->dirty.push_back(Rect{old_w.I0, old_w.I1, old_w.J0, new_w.J0}); }
   if (dj < 0) { m->dirty.push_back(Rect{new_w.I0, new_w.I1, new_w.J0, old_w.J0}); m->dirty.push_back(Rect{old_w.I0, old_w.I1, new_w.J1, old_w.J1}); }
+}
+
+static void clamp_out(long long d, int32_t* out) {
+  if (out) *out = (int32_t)std::max<long long>(INT32_MIN, std::min<long long>(INT32_MAX, d));
+}
+
+extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_t* out_di, int32_t* out_dj) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "shift_window: position not finite");
+  long long di, dj;
+  int4 strips[2];
+  int ns;
+  bool all;
+  recentre(m, x, y, &di, &dj, strips, &ns, &all);
+  clamp_out(di, out_di);
+  clamp_out(dj, out_dj);
+  const int nx = m->prm.nx, ny = m->prm.ny, pxM = pmod(m->I_M, nx), pyM = pmod(m->J_M, ny);
+  for (int q = 0; q < ns; ++q) {  // cells entering the window (their slots held cells that left): unknown
+    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, (pxM + strips[q].x) % nx, (pyM + strips[q].y) % ny, strips[q].z,
+                                  strips[q].w, nx, ny, m->stream), "clear");
+    m->launches++;
+  }
   return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_step(se2m_map* m, double x, double y, const float* world, int64_t world_ld,
+                                 int64_t world_I0, int64_t world_J0, int32_t world_w, int32_t world_h,
+                                 int32_t mem, int32_t* out_di, int32_t* out_dj) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "step: position not finite");
+  if (!world || mem != SE2M_MEM_DEVICE || world_w < 0 || world_h < 0 || world_ld < world_w)
+    return fail(m, SE2M_ERR_INVALID_ARG, "step: world must be a device plane with ld >= w");
+  long long di, dj;
+  int4 strips[2];
+  int ns;
+  bool all;
+  recentre(m, x, y, &di, &dj, strips, &ns, &all);
+  clamp_out(di, out_di);
+  clamp_out(dj, out_dj);
+  if (ns > 0) {
+    FillArgs f;
+    f.h = m->d_h; f.var = m->d_var; f.prior_var = (float)m->prm.fe_prior_var; f.ldh = m->ldh;
+    f.nx = m->prm.nx; f.ny = m->prm.ny; f.pxM = pmod(m->I_M, f.nx); f.pyM = pmod(m->J_M, f.ny);
+    f.I_M = m->I_M; f.J_M = m->J_M;
+    f.world = world; f.world_ld = world_ld; f.wI0 = world_I0; f.wJ0 = world_J0; f.ww = world_w; f.wh = world_h;
+    f.n = ns;
+    for (int q = 0; q < ns; ++q) f.rect[q] = strips[q];
+    CUDA_TRY(m, launch_fill_strips(f, m->stream), "fill strips");
+    m->launches++;
+    m->have_data = true;
+  }
+  if (!m->have_data) return SE2M_OK;  // nothing to assess yet
+  return se2m_assess_se2(m, SE2M_INCREMENTAL);
 }
 
 

@@ -31,7 +31,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
-           "se2m_download_inpainted", "se2m_download_compact_rep"]
+           "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step"]
 
 
 class Params(ctypes.Structure):
@@ -87,6 +87,8 @@ _lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
 _lib.se2m_integrate_scan.argtypes = [_vp, _vp, _i64, ctypes.POINTER(Pose), _i32, _vp]
 _lib.se2m_download_elevation.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_inpaint.argtypes = [_vp]
+_lib.se2m_step.argtypes = [_vp, _f64, _f64, _vp, _i64, _i64, _i64, _i32, _i32, _i32, ctypes.POINTER(_i32),
+                           ctypes.POINTER(_i32)]
 _lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
@@ -233,6 +235,18 @@ class Se2Map:
     def shift_window(self, x: float, y: float):
         di, dj = _i32(), _i32()
         self._check(_lib.se2m_shift_window(self.h, x, y, ctypes.byref(di), ctypes.byref(dj)))
+        return di.value, dj.value
+
+    def step(self, x: float, y: float, world, world_I0: int, world_J0: int):
+        """H1 + H2 + H9 in one call: recentre on (x, y), fill the entered cells from `world` (a float32 CUDA
+        tensor of world heights whose element [0, 0] is world cell (world_I0, world_J0)), assess
+        INCREMENTAL.  Returns (di, dj)."""
+        if not (hasattr(world, "is_cuda") and world.is_cuda) or world.stride(1) != 1:
+            raise ValueError("world must be a CUDA tensor with unit column stride")
+        wh, ww = world.shape
+        di, dj = _i32(), _i32()
+        self._check(_lib.se2m_step(self.h, x, y, world.data_ptr(), world.stride(0), world_I0, world_J0, ww, wh,
+                                   SE2M_MEM_DEVICE, ctypes.byref(di), ctypes.byref(dj)))
         return di.value, dj.value
 
     def assess_se2(self, mode: int = SE2M_FULL):

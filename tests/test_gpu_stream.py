@@ -166,3 +166,38 @@ def test_chain_map_incremental_and_sharded(n_yaw):
     orc = oracle.assess_states(oracle_params(nx, ny, r, n_yaw), h, ijk.astype(np.int32))
     rep = compare({f: ref[f][ijk[:, 2], ijk[:, 1], ijk[:, 0]] for f in ref}, orc)
     assert rep["ok"], rep
+
+
+def test_step_equals_separate_calls():
+    """se2m_step (recentre + fill the entered cells from a device world plane + INCREMENTAL) gives the
+    same state records, bit for bit, as shift_window + update_elevation(strips) + assess(INCREMENTAL),
+    including cells outside the world plane (unknown) and a jump larger than the window."""
+    import torch
+    cfg = CONFIGS["stream"]
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    terrain = cfg["terrain"]
+    a = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    b = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    I0, J0 = a.origin()
+    WI0, WJ0, WW, WH = I0 - 40, J0 - 30, nx + 90, ny + 60          # world plane (partly smaller than the path)
+    world = world_heights(terrain, WI0, WJ0, WW, WH, r)
+    wt = torch.from_numpy(world).cuda()
+    h = world_heights(terrain, I0, J0, nx, ny, r)
+    for m in (a, b):
+        m.update_elevation(h)
+        m.assess_se2(0)
+    path = [(0.61, 0.77), (1.13, 0.52), (1.13, 0.52), (4.9, 2.3), (-0.4, -1.7), (30.0, 10.0), (0.5, 0.5)]
+    for (x, y) in path:
+        d = a.shift_window(x, y)
+        I_M, J_M = a.origin()
+        for (i0, j0, w, hh) in _exposed_strips(*d, nx, ny):
+            strip = np.full((hh, w), np.nan, np.float32)
+            ii = np.arange(I_M + i0, I_M + i0 + w) - WI0
+            jj = np.arange(J_M + j0, J_M + j0 + hh) - WJ0
+            oki, okj = (ii >= 0) & (ii < WW), (jj >= 0) & (jj < WH)
+            strip[np.ix_(okj, oki)] = world[np.ix_(jj[okj], ii[oki])]
+            a.update_elevation(strip, i0=i0, j0=j0)
+        a.assess_se2(1)
+        assert b.step(x, y, wt, WI0, WJ0) == d
+        assert b.origin() == (I_M, J_M)
+        assert _equal(a.download(), b.download()), (x, y)
