@@ -151,7 +151,8 @@ se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, f
 
 /* Whole output planes in LOGICAL window order, layout [k][j][i] (n_yaw * ny * nx entries per
  * non-NULL pointer; trav as bytes 0/1).  mem says whether the output pointers are host or
- * device memory.  States of yaw bins not owned by this rank are NaN / 0.  Synchronises. */
+ * device memory.  States this rank does not own (yaw bins or tile-row bands, see se2m_shard_plan) are
+ * NaN / 0 (compact downloads: 65535 / 0).  Synchronises. */
 se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z,
                           uint8_t* trav, int32_t mem);
 

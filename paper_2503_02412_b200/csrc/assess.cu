@@ -422,7 +422,10 @@ __device__ __noinline__ StateOut1 solve1_fp64(double C00, double C01, double C11
 // much there (a handful of cells out of a full halo row), so those moments are recomputed directly from
 // the tile's heights, shifted by the mean estimate m0 (a two-pass variance): exact up to FP32 rounding of
 // the small deviations.
-constexpr float kDirectN = 32.f;
+#ifndef SE2M_DIRECT_N
+#define SE2M_DIRECT_N 32.f
+#endif
+constexpr float kDirectN = SE2M_DIRECT_N;
 
 // ------------------------------------------------------------------------------------------
 // The assess kernel.
@@ -1098,6 +1101,13 @@ cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, 
 
 __device__ __forceinline__ long long floor_div32(long long a) { return a >= 0 ? a / 32 : -((-a + 31) / 32); }
 
+__device__ __forceinline__ bool row_owned(const AssessParams& p, int j) {
+  if (p.own_G <= 1) return true;
+  const long long J = p.J_M + j;
+  const long long TJ = J >= 0 ? J / p.own_ty : -((-J + p.own_ty - 1) / p.own_ty);
+  return (int)(((TJ - p.own_rank) % p.own_G + p.own_G) % p.own_G) == 0;
+}
+
 __global__ void gather_logical_kernel(const AssessParams p, int k_lo, int k_hi, float* risk, float* pitch,
                                       float* roll, float* z, uint8_t* trav) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1108,7 +1118,7 @@ __global__ void gather_logical_kernel(const AssessParams p, int k_lo, int k_hi, 
   int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
   const size_t src = ((size_t)k * p.ny + py) * p.nx + px;
   const size_t dst = ((size_t)k * p.ny + j) * p.nx + i;
-  const bool owned = k >= k_lo && k < k_hi;
+  const bool owned = k >= k_lo && k < k_hi && row_owned(p, j);
   const float qnan = __int_as_float(0x7fc00000);
   const float4 v = owned ? p.out[src] : make_float4(qnan, qnan, qnan, qnan);
   if (risk) risk[dst] = v.x;
@@ -1140,7 +1150,7 @@ __global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, 
   const int j = blockIdx.y;
   const int k = blockIdx.z;
   int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
-  const bool owned = k >= k_lo && k < k_hi;
+  const bool owned = k >= k_lo && k < k_hi && row_owned(p, j);
   if (risk_q && i < p.nx) {
     int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
     const float r = owned ? p.out[((size_t)k * p.ny + py) * p.nx + px].x : 1.f;

@@ -71,6 +71,9 @@ struct AssessParams {
   long long TI0, TJ0;
   int tiles_x;
   int row_first, row_mod;
+  // downloads: row-band ownership of this rank (SE2M_SHARD_ROWS): logical row j is owned iff
+  // (floor((J_M + j) / own_ty) - own_rank) mod own_G == 0 (own_G = 1: every row)
+  int own_G, own_rank, own_ty;
   int n_rects;
   int4 rects[kMaxRects];
   int k_begin, k_end;    // representative-bin range this launch covers

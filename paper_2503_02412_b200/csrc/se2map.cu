@@ -300,6 +300,10 @@ static AssessParams make_params(const se2m_map* m) {
   p.k_begin = m->k_lo; p.k_end = m->k_hi; p.k_chunk = 1;
   p.use_tma = m->tma_ok ? 1 : 0;
   p.force_general = m->force_general ? 1 : 0;
+  const bool rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  p.own_G = rows ? m->prm.world_size : 1;
+  p.own_rank = rows ? m->prm.rank : 0;
+  p.own_ty = tile_rows(m->R_T);
   return p;
 }
 

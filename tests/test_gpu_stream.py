@@ -107,6 +107,10 @@ def test_sharded_equals_single(mode, G):
             mask = np.broadcast_to(own_rows[None, :, None], ref["risk"].shape)
         for f in merged:
             merged[f][mask] = g[f][mask]
+        # states the rank does not own come back as NaN / 0 (downloads never expose stale records)
+        assert np.all(np.isnan(g["risk"][~mask])) and np.all(g["trav"][~mask] == 0)
+        c = m.download_compact()
+        assert np.all(c["risk_q"][~mask] == 65535)
     assert _equal(merged, ref)
 
 
