@@ -317,8 +317,9 @@ def main():
         # D2H completed (host wall clock around the loop, both streams synchronised).
         wpr = (nx + 31) // 32
         n_rep = n_yaw // 2 if n_yaw % 2 == 0 else n_yaw
-        comp = [{"risk_q": torch.empty((n_rep, ny, nx), dtype=torch.int16).pin_memory(),
-                 "trav_bits": torch.empty((n_rep, ny, wpr), dtype=torch.int32).pin_memory()} for _ in range(2)]
+        own = len(m.owned_rows())                   # row-band ranks download their own rows only
+        comp = [{"risk_q": torch.empty((n_rep, own, nx), dtype=torch.int16).pin_memory(),
+                 "trav_bits": torch.empty((n_rep, own, wpr), dtype=torch.int32).pin_memory()} for _ in range(2)]
         ke = max(3, min(K, 8))
         with torch.cuda.stream(stream):
             for t in range(2):                      # warm the staging buffers
@@ -342,7 +343,7 @@ def main():
             e2e_s = time.perf_counter() - t0
         e2e_s = max_over_ranks([e2e_s], world, dev)[0]
         e2e = {"value": n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
-               "d2h_bytes_per_step": n_rep * ny * nx * 2 + n_rep * ny * wpr * 4, "ms_per_step": e2e_s / ke * 1e3,
+               "d2h_bytes_per_step": n_rep * own * nx * 2 + n_rep * own * wpr * 4, "ms_per_step": e2e_s / ke * 1e3,
                "steps": ke,
                "note": "per step: H2D of the full window from pinned host memory, assess FULL, and D2H of the "
                        "risk map (u16, 1.5e-5 resolution) + traversable bits in logical order to pinned host "

@@ -172,6 +172,10 @@ se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_
  * overlaps the next update / assess; the buffers may be read after se2m_synchronize.  Device
  * destinations are written on the map's stream. */
 se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+/* (With row-band sharding, se2m_download_compact_rep writes only the rank's own logical rows, packed in
+ * increasing order: planes of n_rows rows.)  The rank's own logical rows of the current window
+ * (all ny rows unless row-band sharded): *n of them, listed in rows[] if rows is not NULL. */
+se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t* n);
 
 /* NEXT-1: integrate one LiDAR frame into the elevation window (§V.A, Fig. 3):
  * points (n x 3 float, sensor frame; host or device per mem) are transformed with the pose, points

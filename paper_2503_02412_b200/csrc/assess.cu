@@ -1144,17 +1144,36 @@ cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, flo
 // Compact download: risk quantised to u16 (q = rint(risk * 65535), unknown = 65535) and traversable bits
 // re-packed in logical order (word w of logical row j holds logical columns 32w .. 32w+31, bit = column
 // mod 32; bits beyond nx are 0).  Bins outside [k_lo, k_hi) (not owned) read as risk 65535, trav 0.
+// packed = 1 (row-band sharding): output row q is the rank's q-th own logical row (own rows only, in
+// increasing order; rows_out rows per plane)
+__device__ __forceinline__ int packed_row(const AssessParams& p, int q) {
+  const long long ty = p.own_ty, G = p.own_G;
+  const long long J_M = p.J_M;
+  const long long b0 = J_M >= 0 ? J_M / ty : -((-J_M + ty - 1) / ty);            // band of the first row
+  const long long bf = b0 + ((((p.own_rank - b0) % G) + G) % G);                  // first own band >= b0
+  const long long Js = bf * ty > J_M ? bf * ty : J_M;
+  const long long c0 = (bf + 1) * ty - Js;                                         // own rows in it
+  long long J;
+  if (q < c0) J = Js + q;
+  else {
+    const long long qq = q - c0;
+    J = (bf + G * (1 + qq / ty)) * ty + qq % ty;
+  }
+  return (int)(J - J_M);
+}
+
 __global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, uint16_t* __restrict__ risk_q,
-                                      uint32_t* __restrict__ bits, int wpr) {
+                                      uint32_t* __restrict__ bits, int wpr, int packed, int rows_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y;
+  const int q = blockIdx.y;  // output row
+  const int j = packed ? packed_row(p, q) : q;
   const int k = blockIdx.z;
   int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
   const bool owned = k >= k_lo && k < k_hi && row_owned(p, j);
   if (risk_q && i < p.nx) {
     int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
     const float r = owned ? p.out[((size_t)k * p.ny + py) * p.nx + px].x : 1.f;
-    risk_q[((size_t)k * p.ny + j) * p.nx + i] = (uint16_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 65535.f);
+    risk_q[((size_t)k * rows_out + q) * p.nx + i] = (uint16_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 65535.f);
   }
   if (bits && i < wpr) {
     uint32_t w = 0;
@@ -1170,14 +1189,17 @@ __global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, 
       const int valid = p.nx - 32 * i;                    // logical columns left in this word
       if (valid < 32) w &= (1u << valid) - 1u;
     }
-    bits[((size_t)k * p.ny + j) * wpr + i] = w;
+    bits[((size_t)k * rows_out + q) * wpr + i] = w;
   }
 }
 
 cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
-                                  int words_per_row, cudaStream_t s) {
-  dim3 grid((p.nx + 255) / 256, p.ny, p.n_yaw);
-  gather_compact_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk_q, bits, words_per_row);
+                                  int words_per_row, cudaStream_t s, int packed_rows) {
+  const int rows = packed_rows > 0 ? packed_rows : p.ny;
+  if (rows <= 0) return cudaSuccess;
+  dim3 grid((p.nx + 255) / 256, rows, p.n_yaw);
+  gather_compact_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk_q, bits, words_per_row, packed_rows > 0 ? 1 : 0,
+                                             rows);
   return cudaGetLastError();
 }
 

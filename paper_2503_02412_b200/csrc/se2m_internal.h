@@ -110,8 +110,9 @@ cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, 
                                 int w, int hgt, const float* src, long long ld, const uint8_t* known, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
+// packed_rows > 0: only the rank's own rows (row-band sharding), packed in increasing order
 cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
-                                  int words_per_row, cudaStream_t s);
+                                  int words_per_row, cudaStream_t s, int packed_rows = 0);
 // World (x, y, theta) -> ring indices, resolved on the device in FP64 exactly as readings R3/R6 state.
 struct QueryGeo {
   double r, dth;

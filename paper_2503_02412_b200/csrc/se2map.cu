@@ -913,19 +913,44 @@ extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint
   return SE2M_OK;
 }
 
+// logical rows of the window this rank owns under row-band sharding (all rows otherwise)
+static int owned_rows(const se2m_map* m, int32_t* rows) {
+  const bool sh = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  const int TY = tile_rows(m->R_T), G = m->prm.world_size;
+  int n = 0;
+  for (int j = 0; j < m->prm.ny; ++j) {
+    const long long J = m->J_M + j;
+    if (!sh || pmod(floor_div(J, TY) - m->prm.rank, G) == 0) {
+      if (rows) rows[n] = j;
+      ++n;
+    }
+  }
+  return n;
+}
+
+extern "C" se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t* n) {
+  if (!m || !n) return SE2M_ERR_INVALID_ARG;
+  *n = owned_rows(m, rows);
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
   if (!m) return SE2M_ERR_INVALID_ARG;
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact_rep: bad mem");
   const int wpr = (m->prm.nx + 31) / 32;
   const int n_rep = m->paired ? m->H : m->prm.n_yaw;
-  const size_t plane = (size_t)m->prm.nx * m->prm.ny;
-  const size_t rb = risk_q ? plane * n_rep * 2 : 0, bb = trav_bits ? (size_t)n_rep * m->prm.ny * wpr * 4 : 0;
+  // row-band sharding: only the rank's own rows, packed (se2m_owned_rows lists them)
+  const bool packed = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
+  const int rows = packed ? owned_rows(m, nullptr) : m->prm.ny;
+  const size_t plane = (size_t)m->prm.nx * rows;
+  const size_t rb = risk_q ? plane * n_rep * 2 : 0, bb = trav_bits ? (size_t)n_rep * rows * wpr * 4 : 0;
   if (!rb && !bb) return SE2M_OK;
   AssessParams p = make_params(m);
   p.n_yaw = n_rep;  // planes [0, n_rep): the representative bins (or all bins when n_yaw is odd)
   const int klo = m->k_lo, khi = m->k_hi;  // owned representative bins (others: 65535 / 0)
   if (mem == SE2M_MEM_DEVICE) {
-    CUDA_TRY(m, launch_gather_compact(p, klo, khi, risk_q, trav_bits, wpr, m->stream), "gather_compact");
+    CUDA_TRY(m, launch_gather_compact(p, klo, khi, risk_q, trav_bits, wpr, m->stream, packed ? rows : 0),
+             "gather_compact");
     m->launches++;
     return SE2M_OK;
   }
@@ -953,7 +978,7 @@ extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, 
   uint32_t* db = trav_bits ? reinterpret_cast<uint32_t*>(m->d_rep[b] + rb) : nullptr;
   // staging b is reused only after its previous D2H finished; the D2H waits for the gather
   CUDA_TRY(m, cudaStreamWaitEvent(m->stream, m->ev_copied[b], 0), "wait(copied)");
-  CUDA_TRY(m, launch_gather_compact(p, klo, khi, dr, db, wpr, m->stream), "gather_compact");
+  CUDA_TRY(m, launch_gather_compact(p, klo, khi, dr, db, wpr, m->stream, packed ? rows : 0), "gather_compact");
   m->launches++;
   CUDA_TRY(m, cudaEventRecord(m->ev_gathered[b], m->stream), "record(gathered)");
   CUDA_TRY(m, cudaStreamWaitEvent(m->copy_stream, m->ev_gathered[b], 0), "wait(gathered)");

@@ -31,7 +31,8 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_synchronize", "se2m_launch_count", "se2m_last_error", "se2m_tile_info", "se2m_shard_plan",
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
-           "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step"]
+           "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
+           "se2m_owned_rows"]
 
 
 class Params(ctypes.Structure):
@@ -87,6 +88,7 @@ _lib.se2m_query_trilinear.argtypes = [_vp, _i64, _vp, _i32, _vp, _vp]
 _lib.se2m_integrate_scan.argtypes = [_vp, _vp, _i64, ctypes.POINTER(Pose), _i32, _vp]
 _lib.se2m_download_elevation.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_inpaint.argtypes = [_vp]
+_lib.se2m_owned_rows.argtypes = [_vp, _vp, ctypes.POINTER(_i32)]
 _lib.se2m_step.argtypes = [_vp, _f64, _f64, _vp, _i64, _i64, _i64, _i32, _i32, _i32, ctypes.POINTER(_i32),
                            ctypes.POINTER(_i32)]
 _lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
@@ -300,6 +302,14 @@ class Se2Map:
         self._check(_lib.se2m_download_compact(self.h, rp, bp, mem))
         return out
 
+    def owned_rows(self):
+        """Logical rows of the window this rank owns (all rows unless row-band sharded)."""
+        n = _i32()
+        self._check(_lib.se2m_owned_rows(self.h, None, ctypes.byref(n)))
+        rows = np.empty(n.value, np.int32)
+        self._check(_lib.se2m_owned_rows(self.h, rows.ctypes.data, ctypes.byref(n)))
+        return rows
+
     def download_compact_rep(self, out=None):
         """Representative planes only (Risk and traversability are pi-periodic in theta: plane k serves bins k
         and k + n_yaw/2).  Host outputs (pinned, for overlap) are filled asynchronously: call synchronize()
@@ -308,8 +318,9 @@ class Se2Map:
         n_rep = P.n_yaw // 2 if P.n_yaw % 2 == 0 else P.n_yaw
         wpr = (P.nx + 31) // 32
         if out is None:
-            out = {"risk_q": np.empty((n_rep, P.ny, P.nx), np.uint16),
-                   "trav_bits": np.empty((n_rep, P.ny, wpr), np.uint32)}
+            rows = len(self.owned_rows())
+            out = {"risk_q": np.empty((n_rep, rows, P.nx), np.uint16),
+                   "trav_bits": np.empty((n_rep, rows, wpr), np.uint32)}
         rp, mem, k1 = _ptr_nocopy(out.get("risk_q"))
         bp, mem2, k2 = _ptr_nocopy(out.get("trav_bits"))
         if out.get("risk_q") is not None and out.get("trav_bits") is not None and mem != mem2:

@@ -111,6 +111,15 @@ def test_sharded_equals_single(mode, G):
         assert np.all(np.isnan(g["risk"][~mask])) and np.all(g["trav"][~mask] == 0)
         c = m.download_compact()
         assert np.all(c["risk_q"][~mask] == 65535)
+        if mode == 2:  # the planner copy of a row-band rank: its own rows only, packed
+            rows = m.owned_rows()
+            assert np.array_equal(rows, np.nonzero(own_rows)[0])
+            rep_ = m.download_compact_rep()
+            m.synchronize()
+            H2 = n_yaw // 2
+            assert rep_["risk_q"].shape == (H2, len(rows), nx)
+            assert np.array_equal(rep_["risk_q"], c["risk_q"][:H2][:, rows, :])
+            assert np.array_equal(rep_["trav_bits"], c["trav_bits"][:H2][:, rows, :])
     assert _equal(merged, ref)
 
 
