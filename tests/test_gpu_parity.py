@@ -19,6 +19,15 @@ def _show(name, rep):
     print(name, {k: rep[k] for k in sorted(rep)})
 
 
+@pytest.mark.parametrize("n_yaw", [9, 1, 72])
+def test_parity_paper_window_yaw_counts(n_yaw):
+    """Interior tiles (arrowhead solve) with odd n_yaw (no theta / theta + pi pairing), a single bin, and 5-degree
+    bins, on the paper-like window."""
+    m, h, gpu, orc, rep = run_config(cfg=dict(CONFIGS["paper"], n_yaw=n_yaw))
+    _show("paper n_yaw=%d" % n_yaw, rep)
+    assert rep["ok"], rep
+
+
 @pytest.mark.parametrize("name", ["tiny", "tiny_small_fp", "paper"])
 def test_parity_configs(name):
     m, h, gpu, orc, rep = run_config(name)
