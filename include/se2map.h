@@ -120,7 +120,8 @@ se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w
  * origin is floor(x/r) - nx/2 (IEEE double, reading R7); cells that leave the window become
  * unknown ("removed in parallel").  No data moves (ring buffer).  Returns the
  * origin displacement in cells through out_di / out_dj (either may be NULL).  Marks the
- * exposed and the vacated strips dirty. */
+ * exposed and the vacated strips dirty.  State records (se2m_query / se2m_download) of cells that
+ * entered the window are undefined until the next se2m_assess_se2; the SDF must be recomputed. */
 se2m_status se2m_shift_window(se2m_map* m, double robot_x, double robot_y, int32_t* out_di,
                               int32_t* out_dj);
 

@@ -549,6 +549,7 @@ static void recentre(se2m_map* m, double x, double y, long long* pdi, long long*
   m->I_M = I_M;
   m->J_M = J_M;
   m->inpaint_valid = false;
+  m->sdf_valid = false;  // the SDF layers are in ring order of the old window's risk map
   if (std::llabs(di) >= nx || std::llabs(dj) >= ny) {  // displacement >= side: every cell leaves
     *all = true;
     strips[0] = make_int4(0, 0, nx, ny);
