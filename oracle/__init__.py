@@ -20,7 +20,9 @@ Parity: pinned by ``tests/test_oracle_pins.py`` (pins Q1-Q12 of DESIGN.md) and t
 NumPy brute force in ``tests/bruteforce.py`` (Q5).  On non-planar terrain the per-state values
 are pinned only by the invariants Q3-Q8 and the brute force; readings R1, R2, R8 and R14 are
 readings of the paper, not confirmable from it ("parity unpinned" for those readings only;
-see DESIGN.md §oracle).
+see DESIGN.md §oracle).  ``sdf`` (NEXT-2) is pinned by tests/test_oracle_sdf.py (SPEC examples, scipy's
+exact EDT, the 1-Lipschitz property); its reading R24 (centre-to-centre distance, unknown = obstacle) is
+parity unpinned as a reading.
 """
 from __future__ import annotations
 

@@ -19,6 +19,12 @@ Mahalanobis gate is |z - h| / sqrt(s2 + s2_m) <= 2 and on failure the higher of 
 (SPEC S:163); points are fused sequentially in input order; cells store float32 height and variance.
 
 Everything is plain Python / NumPy in float64 with no FMA contraction.
+
+Pinned by tests/test_oracle_frontend.py: the SPEC's worked variance and KF examples, a Monte-Carlo
+check of sigma^2, the ray-cast examples, dense sampling of the slab traversal, KF order-insensitivity
+and variance monotonicity.  The readings R26-R30 themselves (sign of p_B, band frame, ray geometry,
+sequential fusion order, float32 storage) are parity unpinned as readings (not confirmable from the
+paper's text).
 """
 from __future__ import annotations
 

@@ -11,6 +11,9 @@ unchanged; a window without any known cell is an error.
 Written as the definition: for each unknown cell, the squared distance to every known cell, the first
 minimum in row-major order (np.nonzero enumerates in row-major order, np.argmin returns the first
 minimum).  Integer arithmetic only; heights are copied, never computed.
+
+Pinned by tests/test_oracle_inpaint.py (SPEC examples, tie cases, an independent exact EDT, a pure-Python
+brute force); the tie rule of R31 is a reading (the paper is silent): parity unpinned as a reading.
 """
 from __future__ import annotations
 

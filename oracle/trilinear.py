@@ -8,6 +8,10 @@ SPEC S:261-269 (query_trilinear): trilinear over (x, y, theta), theta wrapped cy
 Lattice (readings R3/R6): node (i, j, k) of the window sits at x = (I_M + i + 1/2) r,
 y = (J_M + j + 1/2) r, theta_k = -pi + 2 pi k / n.  A query needs its 4 spatial corner nodes inside
 the window; otherwise it is out of range.
+
+Pinned by tests/test_oracle_trilinear.py (interpolation of linear fields is exact, node values are
+reproduced, the gradient matches finite differences, theta wraps); the lattice placement (R25) is a
+reading: parity unpinned as a reading.
 """
 from __future__ import annotations
 
