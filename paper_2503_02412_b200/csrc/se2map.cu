@@ -500,6 +500,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
 extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w, int32_t h,
                                              const float* heights, int64_t ld, const uint8_t* known, int32_t mem) {
   if (!m) return SE2M_ERR_INVALID_ARG;
+  if (w == 0 || h == 0) return SE2M_OK;  // nothing to write (the pointer of an empty array may be NULL)
   if (!heights || w < 0 || h < 0 || ld < w || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
     return fail(m, SE2M_ERR_INVALID_ARG, "update_elevation: bad pointer / size / mem");
   if (i0 < 0 || j0 < 0 || (long long)i0 + w > m->prm.nx || (long long)j0 + h > m->prm.ny)
