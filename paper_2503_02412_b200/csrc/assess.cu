@@ -994,7 +994,11 @@ template <int R_T>
 static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {
   using G = Geom<R_T>;
   const size_t smem = G::bytes(p.tab_cap);
-  static int configured_bytes = 0;
+  // the attribute is per device: remember the configured size per device ordinal
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& configured_bytes = configured[dev & 63];
   if ((int)smem > configured_bytes) {
     cudaError_t e = cudaFuncSetAttribute(assess_kernel<R_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
