@@ -815,8 +815,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   // interior moments (prefix entries with validity prefixes, then single cells: h^ or NaN = unknown)
 #pragma unroll 1
   for (int sp = 0; sp < RPW; sp += 2) {
-    float2 S02g[2];
-    float SXHg[2], SYHg[2], N[2], Sx[2], Sy[2], Sxx[2], Sxy[2], Syy[2];
+    // accumulators packed across the state pair (lo = state sp, hi = state sp + 1): one FFMA2 per moment
+    F2 S0g, S2g, SXHg, SYHg, Nv, Sxv, Syv, Sxxv, Sxyv, Syyv;
     const int so8 = sp * RS8, so4 = sp * RS4;
     int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
 #pragma unroll
@@ -836,64 +836,63 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const float2 csk = __ldg(p.cs + k);
       const bool restart = k == kb || kc == 0 || !G::CB;
       if (++kc == p.period) kc = 0;
-      if (restart) {
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          S02g[s] = make_float2(0.f, 0.f);
-          SXHg[s] = SYHg[s] = N[s] = Sx[s] = Sy[s] = Sxx[s] = Sxy[s] = Syy[s] = 0.f;
-        }
-      }
+      if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
 #pragma unroll 1
       for (int d = 0; d < npre; ++d) {
         const int4 o = rk[d];
         const float dj = __int_as_float(o.w);
         const int ob4 = o.z + ((o.y - o.x) >> 1);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const float2 A = *reinterpret_cast<const float2*>(b8 + so8 + o.x + s * RS8);
-          const float2 B = *reinterpret_cast<const float2*>(b8 + so8 + o.y + s * RS8);
-          const float ax = *reinterpret_cast<const float*>(b4 + so4 + o.z + s * RS4);
-          const float bxv = *reinterpret_cast<const float*>(b4 + so4 + ob4 + s * RS4);
-          const float2 VA = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + s * RS8);
-          const float2 VB = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + s * RS8);
-          const float wa = *reinterpret_cast<const float*>(bv4 + so4 + o.z + s * RS4);
-          const float wb = *reinterpret_cast<const float*>(bv4 + so4 + ob4 + s * RS4);
-          const float2 dd = sub2(B, A);
-          const float cnt = VB.x - VA.x, sxv = VB.y - VA.y, sxxv = wb - wa;  // exact integers
-          const float sdi = fmaf(-xs, cnt, sxv);                              // sum di over the run
-          S02g[s] = add2(S02g[s], dd);
-          SXHg[s] += fmaf(-xs, dd.x, bxv - ax);
-          SYHg[s] = fmaf(dj, dd.x, SYHg[s]);
-          N[s] += cnt;
-          Sx[s] += sdi;
-          Sxx[s] += fmaf(xs * xs, cnt, fmaf(-2.f * xs, sxv, sxxv));
-          Sy[s] = fmaf(dj, cnt, Sy[s]);
-          Syy[s] = fmaf(dj * dj, cnt, Syy[s]);
-          Sxy[s] = fmaf(dj, sdi, Sxy[s]);
-        }
+        const float2 A0 = *reinterpret_cast<const float2*>(b8 + so8 + o.x);
+        const float2 B0 = *reinterpret_cast<const float2*>(b8 + so8 + o.y);
+        const float2 A1 = *reinterpret_cast<const float2*>(b8 + so8 + o.x + RS8);
+        const float2 B1 = *reinterpret_cast<const float2*>(b8 + so8 + o.y + RS8);
+        const F2 ax = pk(*reinterpret_cast<const float*>(b4 + so4 + o.z),
+                         *reinterpret_cast<const float*>(b4 + so4 + o.z + RS4));
+        const F2 bx = pk(*reinterpret_cast<const float*>(b4 + so4 + ob4),
+                         *reinterpret_cast<const float*>(b4 + so4 + ob4 + RS4));
+        const float2 VA0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x);
+        const float2 VB0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y);
+        const float2 VA1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + RS8);
+        const float2 VB1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + RS8);
+        const F2 wa = pk(*reinterpret_cast<const float*>(bv4 + so4 + o.z),
+                         *reinterpret_cast<const float*>(bv4 + so4 + o.z + RS4));
+        const F2 wb = pk(*reinterpret_cast<const float*>(bv4 + so4 + ob4),
+                         *reinterpret_cast<const float*>(bv4 + so4 + ob4 + RS4));
+        const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x), d2 = pk(B0.y, B1.y) - pk(A0.y, A1.y);
+        const F2 cnt = pk(VB0.x, VB1.x) - pk(VA0.x, VA1.x), sxv = pk(VB0.y, VB1.y) - pk(VA0.y, VA1.y);
+        const F2 sxxv = wb - wa;                                  // exact integers
+        const F2 sdi = fma2(bc(-xs), cnt, sxv);                   // sum di over the run
+        S0g = S0g + d0;
+        S2g = S2g + d2;
+        SXHg = SXHg + fma2(bc(-xs), d0, bx - ax);
+        SYHg = fma2(bc(dj), d0, SYHg);
+        Nv = Nv + cnt;
+        Sxv = Sxv + sdi;
+        Sxxv = Sxxv + fma2(bc(xs * xs), cnt, fma2(bc(-2.f * xs), sxv, sxxv));
+        Syv = fma2(bc(dj), cnt, Syv);
+        Syyv = fma2(bc(dj * dj), cnt, Syyv);
+        Sxyv = fma2(bc(dj), sdi, Sxyv);
       }
 #pragma unroll 1
       for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
         const int4 o = rk[d];
         const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
         const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const float h = *reinterpret_cast<const float*>(bh + so4 + o.x + s * RS4);
-          const bool ok = !isnan(h);
-          const float v = ok ? 1.f : 0.f, hv = ok ? h : 0.f;
-          const float sh = sg * hv;
-          S02g[s].x += sh;
-          S02g[s].y = fmaf(sh, hv, S02g[s].y);
-          SXHg[s] = fmaf(sdi, hv, SXHg[s]);
-          SYHg[s] = fmaf(sdj, hv, SYHg[s]);
-          N[s] = fmaf(sg, v, N[s]);
-          Sx[s] = fmaf(sdi, v, Sx[s]);
-          Sy[s] = fmaf(sdj, v, Sy[s]);
-          Sxx[s] = fmaf(cxx, v, Sxx[s]);
-          Sxy[s] = fmaf(cxy, v, Sxy[s]);
-          Syy[s] = fmaf(cyy, v, Syy[s]);
-        }
+        const float h0 = *reinterpret_cast<const float*>(bh + so4 + o.x);
+        const float h1 = *reinterpret_cast<const float*>(bh + so4 + o.x + RS4);
+        const bool k0 = !isnan(h0), k1 = !isnan(h1);
+        const F2 v = pk(k0 ? 1.f : 0.f, k1 ? 1.f : 0.f), hv = pk(k0 ? h0 : 0.f, k1 ? h1 : 0.f);
+        const F2 sh = bc(sg) * hv;
+        S0g = S0g + sh;
+        S2g = fma2(sh, hv, S2g);
+        SXHg = fma2(bc(sdi), hv, SXHg);
+        SYHg = fma2(bc(sdj), hv, SYHg);
+        Nv = fma2(bc(sg), v, Nv);
+        Sxv = fma2(bc(sdi), v, Sxv);
+        Syv = fma2(bc(sdj), v, Syv);
+        Sxxv = fma2(bc(cxx), v, Sxxv);
+        Sxyv = fma2(bc(cxy), v, Sxyv);
+        Syyv = fma2(bc(cyy), v, Syyv);
       }
       float4* outk = p.out + (size_t)k * plane;
       float4* outk2 = p.out + (size_t)(k + p.H) * plane;
@@ -910,10 +909,11 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           if (p.paired) travk2[toff] = tmask;
         }
       };
+          const float N[2] = {lo(Nv), hi(Nv)}, Sx[2] = {lo(Sxv), hi(Sxv)}, Sy[2] = {lo(Syv), hi(Syv)};
+          const float Sxx[2] = {lo(Sxxv), hi(Sxxv)}, Sxy[2] = {lo(Sxyv), hi(Sxyv)}, Syy[2] = {lo(Syyv), hi(Syyv)};
           const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
           const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
-          Cov2 cv = cov_general(pk(N[0], N[1]), pk(Sx[0], Sx[1]), pk(Sy[0], Sy[1]), shl, shh, pk(S02g[0].x, S02g[1].x),
-                                pk(S02g[0].y, S02g[1].y), pk(SXHg[0], SXHg[1]), pk(SYHg[0], SYHg[1]),
+          Cov2 cv = cov_general(Nv, Sxv, Syv, shl, shh, S0g, S2g, SXHg, SYHg,
                                 pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
           // (states outside the window are not stored: they never take the direct path)
           const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
