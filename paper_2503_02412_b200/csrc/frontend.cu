@@ -3,9 +3,10 @@
 //   fe_points_kernel   one thread per LiDAR point: sensor -> body -> world, map-range and
 //                      body-frame height-band filters, sigma^2 = J_S^T S_S J_S + J_R^T S_R J_R
 //                      + J_B^T S_B J_B;
-//   fe_raycast_kernel  one thread per used point: the cells its ray crosses (2-D DDA, each candidate
-//                      confirmed by an exact slab test) are reset to unknown when their height exceeds
-//                      the ray's highest height over the cell + eps;
+//   fe_raycast_kernel  one warp per used point: the cells its ray crosses (lanes over the columns of the
+//                      ray's major axis, each candidate confirmed by an exact slab test) are reset to
+//                      unknown when their height exceeds the ray's highest height over the cell + eps
+//                      (P:103);
 //   (CUB stable radix sort of (cell, point index))
 //   fe_fuse_kernel     one thread per cell run: the cell's points in input order through the 1-D Kalman
 //                      filter with the Mahalanobis gate / higher-wins rule (readings R29-R30).
@@ -59,7 +60,7 @@ __global__ void fe_points_kernel(const FrontendArgs a, int n, const float* __res
   s2 = fmax(s2, 0.0);
   const long long I = (long long)floor(dd(x, a.r)), J = (long long)floor(dd(y, a.r));
   const long long i = I - a.I_M, j = J - a.J_M;
-  int k = -1, st = 0;
+  int k = a.key_none, st = 0;
   if (!(i >= 0 && i < a.nx && j >= 0 && j < a.ny)) st = 1;            // outside the map
   else if (!(q2 >= a.z_min && q2 <= a.z_max)) st = 2;                   // height band in B
   else if (!(s2 > 0.0)) st = 3;                                         // unusable variance
@@ -71,7 +72,14 @@ __global__ void fe_points_kernel(const FrontendArgs a, int n, const float* __res
   key[t] = k;
   idx[t] = t;
   meas[t] = make_double4(x, y, z, s2);
-  atomicAdd(counts + st, 1);
+  // status counters aggregated per warp (four words shared by the whole grid)
+  const unsigned act = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int m = __popc(__ballot_sync(act, st == c));
+    if (lane == leader && m) atomicAdd(counts + c, m);
+  }
 }
 
 // Slab method (reading R28): parameter interval (t0, t1) of s + t d, t in (0, 1), inside the open square.
@@ -93,78 +101,130 @@ __device__ __forceinline__ bool cell_interval(double sx, double sy, double dx, d
   return t0 < t1;
 }
 
+// One warp per ray: the lanes take the columns (x-major rays) or rows (y-major rays) of the ray's span;
+// in its column a lane tests the (padded) range of rows the segment can cross there with the exact slab
+// test of the oracle (reading R28), so the cells tested are a superset of the cells crossed and every
+// decision is the oracle's.  All rays read the pre-frame heights; a cell reset by another ray reads
+// NaN (unknown) and is left as it is, so the outcome does not depend on the order.
 __global__ void fe_raycast_kernel(const FrontendArgs a, int n, const int* __restrict__ key,
                                   const double4* __restrict__ meas, float* h, int* bbox, int* n_reset) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n || key[t] < 0) return;
+  const int t = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (t >= n || key[t] == a.key_none) return;  // warp-uniform
   const double4 e = meas[t];
   const double sx = a.sx, sy = a.sy, sz = a.sz;
   const double dx = ds(e.x, sx), dy = ds(e.y, sy), dz = ds(e.z, sz);
   const long long Ie = (long long)floor(dd(e.x, a.r)), Je = (long long)floor(dd(e.y, a.r));
-  long long I = (long long)floor(dd(sx, a.r)), J = (long long)floor(dd(sy, a.r));
-  // 2-D DDA from the sensor's cell to the point's cell; every visited cell is confirmed by the slab test
-  const int stepI = dx > 0 ? 1 : (dx < 0 ? -1 : 0), stepJ = dy > 0 ? 1 : (dy < 0 ? -1 : 0);
-  const double inf = 1e300;
-  double tMaxX = stepI > 0 ? dd(ds((double)(I + 1) * a.r, sx), dx) : (stepI < 0 ? dd(ds((double)I * a.r, sx), dx) : inf);
-  double tMaxY = stepJ > 0 ? dd(ds((double)(J + 1) * a.r, sy), dy) : (stepJ < 0 ? dd(ds((double)J * a.r, sy), dy) : inf);
-  const double tDX = stepI ? fabs(dd(a.r, dx)) : inf, tDY = stepJ ? fabs(dd(a.r, dy)) : inf;
-  const int max_steps = (int)(llabs(Ie - I) + llabs(Je - J)) + 2;
-  for (int s = 0; s <= max_steps; ++s) {
-    if (!(I == Ie && J == Je)) {
-      const long long i = I - a.I_M, j = J - a.J_M;
-      double t0, t1;
-      if (i >= 0 && i < a.nx && j >= 0 && j < a.ny &&
-          cell_interval(sx, sy, dx, dy, (double)I * a.r, (double)(I + 1) * a.r, (double)J * a.r, (double)(J + 1) * a.r, t0, t1)) {
-        int px = a.pxM + (int)i; if (px >= a.nx) px -= a.nx;
-        int py = a.pyM + (int)j; if (py >= a.ny) py -= a.ny;
-        float* cell = h + (size_t)py * a.ldh + px;
-        const float hc = *cell;
-        const double zr = fmax(da(sz, dm(t0, dz)), da(sz, dm(t1, dz)));  // highest ray height over the cell
-        if (!isnan(hc) && (double)hc > da(zr, a.ray_eps)) {              // P:103, margin reading R28
-          *cell = __int_as_float(0x7fc00000);
-          atomicAdd(n_reset, 1);
-          atomicMin(bbox + 0, (int)i); atomicMax(bbox + 1, (int)i);
-          atomicMin(bbox + 2, (int)j); atomicMax(bbox + 3, (int)j);
-        }
-      }
-    } else {
-      break;
+  const long long Is = (long long)floor(dd(sx, a.r)), Js = (long long)floor(dd(sy, a.r));
+  const bool xmaj = llabs(Ie - Is) >= llabs(Je - Js);
+  // major axis (u) spans [u0, u1] cells; along the minor axis (w) the crossed cells lie between the
+  // segment's w at the column's two faces (clipped to the segment), padded by one cell for rounding
+  const long long u0 = xmaj ? min(Is, Ie) : min(Js, Je), u1 = xmaj ? max(Is, Ie) : max(Js, Je);
+  const double su = xmaj ? sx : sy, sw = xmaj ? sy : sx, du = xmaj ? dx : dy, dw = xmaj ? dy : dx;
+  int resets = 0, bi0 = 0x7fffffff, bi1 = -1, bj0 = 0x7fffffff, bj1 = -1;
+  for (long long U = u0 + lane; U <= u1; U += 32) {
+    double tlo = 0.0, thi = 1.0;
+    if (du != 0.0) {
+      double ta = dd(ds((double)U * a.r, su), du), tb = dd(ds((double)(U + 1) * a.r, su), du);
+      if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+      tlo = fmax(0.0, ta);
+      thi = fmin(1.0, tb);
     }
-    if (tMaxX < tMaxY) { tMaxX = da(tMaxX, tDX); I += stepI; }
-    else if (tMaxY < tMaxX) { tMaxY = da(tMaxY, tDY); J += stepJ; }
-    else { tMaxX = da(tMaxX, tDX); tMaxY = da(tMaxY, tDY); I += stepI; J += stepJ; }  // exact corner
+    const double wa = da(sw, dm(tlo, dw)), wb = da(sw, dm(thi, dw));
+    const long long W0 = (long long)floor(dd(fmin(wa, wb), a.r)) - 1, W1 = (long long)floor(dd(fmax(wa, wb), a.r)) + 1;
+    for (long long Wc = W0; Wc <= W1; ++Wc) {
+      const long long I = xmaj ? U : Wc, J = xmaj ? Wc : U;
+      if (I == Ie && J == Je) continue;  // the point's own cell is measured, not cleared (R28)
+      const long long i = I - a.I_M, j = J - a.J_M;
+      if (!(i >= 0 && i < a.nx && j >= 0 && j < a.ny)) continue;
+      double t0, t1;
+      if (!cell_interval(sx, sy, dx, dy, (double)I * a.r, (double)(I + 1) * a.r, (double)J * a.r,
+                         (double)(J + 1) * a.r, t0, t1))
+        continue;
+      int px = a.pxM + (int)i; if (px >= a.nx) px -= a.nx;
+      int py = a.pyM + (int)j; if (py >= a.ny) py -= a.ny;
+      float* cell = h + (size_t)py * a.ldh + px;
+      const float hc = *cell;
+      const double zr = fmax(da(sz, dm(t0, dz)), da(sz, dm(t1, dz)));  // highest ray height over the cell
+      if (!isnan(hc) && (double)hc > da(zr, a.ray_eps)) {              // P:103, margin reading R28
+        *cell = __int_as_float(0x7fc00000);
+        ++resets;
+        bi0 = min(bi0, (int)i); bi1 = max(bi1, (int)i);
+        bj0 = min(bj0, (int)j); bj1 = max(bj1, (int)j);
+      }
+    }
+  }
+  // one set of atomics per ray (warp): reset count and touched box
+  resets = __reduce_add_sync(0xffffffffu, resets);
+  bi0 = __reduce_min_sync(0xffffffffu, bi0); bi1 = __reduce_max_sync(0xffffffffu, bi1);
+  bj0 = __reduce_min_sync(0xffffffffu, bj0); bj1 = __reduce_max_sync(0xffffffffu, bj1);
+  if (lane == 0 && resets) {
+    atomicAdd(n_reset, resets);
+    atomicMin(bbox + 0, bi0); atomicMax(bbox + 1, bi1);
+    atomicMin(bbox + 2, bj0); atomicMax(bbox + 3, bj1);
   }
 }
 
 __global__ void fe_fuse_kernel(const FrontendArgs a, int n, const int* __restrict__ skey, const int* __restrict__ sidx,
                                const double4* __restrict__ meas, float* h, float* var, int* bbox) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const int k = skey[t];
-  if (k < 0 || (t > 0 && skey[t - 1] == k)) return;  // one thread per run of equal cells
-  float* hp = h + k;
-  float* vp = var + k;
-  float hc = *hp, vc = *vp;
-  for (int u = t; u < n && skey[u] == k; ++u) {
-    const double4 e = meas[sidx[u]];
-    const double z = e.z, s2 = e.w;
-    if (isnan(hc)) { hc = (float)z; vc = (float)s2; continue; }  // unknown: initialise
-    const double hh = hc, sc = vc;
-    const double d = dd(fabs(ds(z, hh)), __dsqrt_rn(da(sc, s2)));
-    if (d <= a.gate) {                                              // 1-D Kalman update
-      const double den = da(sc, s2);
-      hc = (float)dd(da(dm(s2, hh), dm(sc, z)), den);
-      vc = (float)dd(dm(sc, s2), den);
-    } else if (z > hh) {                                            // Mahalanobis gate: higher wins
-      hc = (float)z; vc = (float)s2;
+  const int k = t < n ? skey[t] : a.key_none;
+  // one thread per run of equal cells; the touched-cell box is reduced per warp (one atomic per bound
+  // and warp instead of per cell: the four bound words are shared by the whole grid)
+  const bool lead = t < n && k != a.key_none && !(t > 0 && skey[t - 1] == k);
+  int i = 0x7fffffff, j = 0x7fffffff, i1 = -1, j1 = -1;
+  if (lead) {
+    float* hp = h + k;
+    float* vp = var + k;
+    float hc = *hp, vc = *vp;
+    // the run's measurements are gathered 8 at a time (independent loads in flight together) and
+    // then fused in input order
+    constexpr int CH = 8;
+    for (int u0 = t; u0 < n && skey[u0] == k; u0 += CH) {
+      double4 ech[CH];
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int u = u0 + q;
+        const bool in = u < n && skey[u] == k;
+        if (in) { ech[q] = meas[sidx[u]]; cnt = q + 1; }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+      if (q >= cnt) break;
+      const double4 e = ech[q];
+      const double z = e.z, s2 = e.w;
+      if (isnan(hc)) { hc = (float)z; vc = (float)s2; continue; }  // unknown: initialise
+      const double hh = hc, sc = vc;
+      const double diff = fabs(ds(z, hh)), den = da(sc, s2);
+      // Mahalanobis gate d = diff / sqrt(den) <= gate (reading R29), decided without the sqrt / division
+      // chain unless d is within 1e-12 of the gate (then the exact formula, as in the oracle)
+      const double l2 = dm(diff, diff), r2 = dm(dm(a.gate, a.gate), den);
+      bool pass;
+      if (l2 < r2 * (1.0 - 1e-12)) pass = true;
+      else if (l2 > r2 * (1.0 + 1e-12)) pass = false;
+      else pass = dd(diff, __dsqrt_rn(den)) <= a.gate;
+      if (pass) {                                                     // 1-D Kalman update
+        hc = (float)dd(da(dm(s2, hh), dm(sc, z)), den);
+        vc = (float)dd(dm(sc, s2), den);
+      } else if (z > hh) {                                            // Mahalanobis gate: higher wins
+        hc = (float)z; vc = (float)s2;
+      }
+      }
+      if (cnt < CH) break;
     }
+    *hp = hc;
+    *vp = vc;
+    const int px = k % a.ldh, py = k / a.ldh;
+    i = px >= a.pxM ? px - a.pxM : px + a.nx - a.pxM;
+    j = py >= a.pyM ? py - a.pyM : py + a.ny - a.pyM;
+    i1 = i; j1 = j;
   }
-  *hp = hc;
-  *vp = vc;
-  const int px = k % a.ldh, py = k / a.ldh;
-  const int i = px >= a.pxM ? px - a.pxM : px + a.nx - a.pxM, j = py >= a.pyM ? py - a.pyM : py + a.ny - a.pyM;
-  atomicMin(bbox + 0, i); atomicMax(bbox + 1, i);
-  atomicMin(bbox + 2, j); atomicMax(bbox + 3, j);
+  i = __reduce_min_sync(0xffffffffu, i); i1 = __reduce_max_sync(0xffffffffu, i1);
+  j = __reduce_min_sync(0xffffffffu, j); j1 = __reduce_max_sync(0xffffffffu, j1);
+  if ((threadIdx.x & 31) == 0 && i1 >= 0) {
+    atomicMin(bbox + 0, i); atomicMax(bbox + 1, i1);
+    atomicMin(bbox + 2, j); atomicMax(bbox + 3, j1);
+  }
 }
 
 cudaError_t frontend_run(const FrontendArgs& a, int n, const float* pts, FrontendScratch& s, float* h, float* var,
@@ -174,12 +234,15 @@ cudaError_t frontend_run(const FrontendArgs& a, int n, const float* pts, Fronten
   const int B = 256, G = (n + B - 1) / B;
   fe_points_kernel<<<G, B, 0, st>>>(a, n, pts, s.key, s.idx, s.meas, s.counts);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  fe_raycast_kernel<<<G, B, 0, st>>>(a, n, s.key, s.meas, h, s.bbox, s.counts + 4);
+  fe_raycast_kernel<<<(unsigned)(((size_t)n * 32 + B - 1) / B), B, 0, st>>>(a, n, s.key, s.meas, h, s.bbox,
+                                                                           s.counts + 4);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   size_t need = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, need, s.key, s.skey, s.idx, s.sidx, n, 0, 32, st);
+  // stable sort by cell over the key bits that occur (ring indices): the points of a cell keep their
+  // input order (reading R29)
+  cub::DeviceRadixSort::SortPairs(nullptr, need, s.key, s.skey, s.idx, s.sidx, n, 0, a.key_bits, st);
   if (need > s.temp_bytes) return cudaErrorMemoryAllocation;  // caller sizes the scratch (frontend_temp_bytes)
-  e = cub::DeviceRadixSort::SortPairs(s.temp, need, s.key, s.skey, s.idx, s.sidx, n, 0, 32, st);
+  e = cub::DeviceRadixSort::SortPairs(s.temp, need, s.key, s.skey, s.idx, s.sidx, n, 0, a.key_bits, st);
   if (e != cudaSuccess) return e;
   fe_fuse_kernel<<<G, B, 0, st>>>(a, n, s.skey, s.sidx, s.meas, h, var, s.bbox);
   return cudaGetLastError();

@@ -136,6 +136,8 @@ struct FrontendArgs {
   double sx, sy, sz;     // LiDAR position in the world, R_B p_BS + p_B (host, fixed order)
   long long I_M, J_M;
   int nx, ny, ldh, pxM, pyM;
+  int key_bits;          // radix-sort key width: ring cell indices < 2^key_bits - 1
+  int key_none;          // 2^key_bits - 1: the key of a filtered point (sorts last)
 };
 struct FrontendScratch {
   int *key, *idx, *skey, *sidx;

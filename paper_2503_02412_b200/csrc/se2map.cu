@@ -1041,6 +1041,9 @@ extern "C" se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int
   a.sz = (RB[6] * pbs[0] + RB[7] * pbs[1] + RB[8] * pbs[2]) + pose->p_B[2];
   a.I_M = m->I_M; a.J_M = m->J_M;
   a.nx = m->prm.nx; a.ny = m->prm.ny; a.ldh = m->ldh;
+  a.key_bits = 1;
+  while ((1ll << a.key_bits) - 1 <= (long long)m->ldh * m->prm.ny) ++a.key_bits;  // indices < 2^bits - 1
+  a.key_none = (int)((1ll << a.key_bits) - 1);
   a.pxM = pmod(m->I_M, m->prm.nx); a.pyM = pmod(m->J_M, m->prm.ny);
   CUDA_TRY(m, frontend_run(a, (int)n, pts, s, m->d_h, m->d_var, m->stream), "front-end kernels");
   m->launches += 3;
