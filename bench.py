@@ -190,7 +190,8 @@ def run_reference(args, cfg):
     import oracle
     I_M, J_M = oracle.window_origin(x, y, cfg["r"], cfg["nx"], cfg["ny"])
     h = world_heights(cfg["terrain"], I_M, J_M, cfg["nx"], cfg["ny"], cfg["r"])
-    per_step = float(os.environ.get("BENCH_REF_STEP_S", "6"))
+    # each step a bounded sample: ~6 s, shrunk so that the whole run stays within ~2.5 minutes
+    per_step = float(os.environ.get("BENCH_REF_STEP_S", str(max(0.5, min(6.0, 150.0 / max(1, args.steps))))))
     for _ in range(args.warmup):
         cpu_oracle_rate(cfg, h, budget_s=min(1.0, per_step / 4))
     rates, states, secs = [], 0, 0.0
