@@ -7,8 +7,10 @@ A step = one pass of the whole hot path over the 
 map: shift_window (Eq. 4, the robot moves along a path), update_elevation (the full window,
 from an HBM-resident world buffer for `value`, from pinned host memory for `e2e`), assess_se2
 FULL (Alg. 1 for every SE(2) state), and a batch query of planner states.  Prints ONE JSON line
-on rank 0.  Under torchrun (N > 1) the states are sharded by interleaved tile rows
-(SE2M_SHARD_ROWS), no data-path collective; value = all ranks' states / max-over-ranks time.
+on rank 0.  Under torchrun (N > 1) every GPU runs its own map of the configuration's size (a batch
+of independent maps, one per GPU: weak scaling — the path has no exchange step, so no data-path
+collective); value = all ranks' states / the max-over-ranks time.  (Splitting ONE map across GPUs —
+yaw slices or interleaved tile-row bands — is in the library, se2m_params.shard_mode, and tested.)
 
 `--impl reference`: the FP64 CPU oracle (oracle/, the test reference) timed as it stands on this
 host's cores on a bounded random sample of the same workload per step (rank 0 only).
@@ -204,7 +206,7 @@ def run_reference(args, cfg):
     value = states / secs
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (T_hills seed 5, SURVEY.md §8(d)); random-init-free: no weights",
             "config": {"workload": args.config, "nx": cfg["nx"], "ny": cfg["ny"], "n_yaw": cfg["n_yaw"],
                        "resolution_m": cfg["r"], "footprint_m": [cfg["ex"], cfg["ey"]]},
@@ -237,9 +239,14 @@ def main():
     n_states = nx * ny * n_yaw
     K, W = args.steps, max(args.warmup, 3)
     positions, margin = robot_positions(cfg, K + W + 2)
+    # multi-GPU: a batch of independent maps, one per GPU (weak scaling: the path needs no exchange,
+    # SURVEY.md §8(e) "batches of maps"); rank g's robot drives the same path 1 km further east
+    off_x = 1000.0 * rank
+    positions = [(x + off_x, y) for (x, y) in positions]
+    robot0 = (cfg["robot"][0] + off_x, cfg["robot"][1])
 
     import oracle  # window arithmetic only (Eq. 4 origin) and the cpu_baseline leg
-    I_M0, J_M0 = oracle.window_origin(*cfg["robot"], r, nx, ny)
+    I_M0, J_M0 = oracle.window_origin(*robot0, r, nx, ny)
     # world buffer covering every window of the path, resident in HBM (inputs of `value`)
     WX, WY = nx + 2 * margin, ny + 2 * margin
     WI0, WJ0 = I_M0 - margin, J_M0 - margin
@@ -249,10 +256,8 @@ def main():
     world_d = torch.from_numpy(world_h).to(dev)
     world_pinned = torch.from_numpy(world_h).pin_memory()
 
-    shard = S.SE2M_SHARD_ROWS if world > 1 else S.SE2M_SHARD_NONE
     m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
-                 robot_x=cfg["robot"][0], robot_y=cfg["robot"][1], device=local, shard_mode=shard,
-                 rank=rank, world_size=world, cuda_stream=stream.cuda_stream)
+                 robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream)
     rng = np.random.default_rng(1)
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -306,7 +311,7 @@ def main():
     tot_s = sum(step_ms) / 1e3
     kern_s = sum(kern_ms) / 1e3
     tot_s, kern_s = max_over_ranks([tot_s, kern_s], world, dev)
-    value = n_states * K / tot_s
+    value = world * n_states * K / tot_s           # all ranks' states / the slowest rank's time
 
     # ---- e2e: public API with host buffers (H2D of the step's map from pinned memory, D2H of the
     #      risk map to pinned memory: the paper sends the risk map back to the CPU) -----
@@ -343,7 +348,7 @@ def main():
             m.synchronize()
             e2e_s = time.perf_counter() - t0
         e2e_s = max_over_ranks([e2e_s], world, dev)[0]
-        e2e = {"value": n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
+        e2e = {"value": world * n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
                "d2h_bytes_per_step": n_rep * own * nx * 2 + n_rep * own * wpr * 4, "ms_per_step": e2e_s / ke * 1e3,
                "steps": ke,
                "note": "per step: H2D of the full window from pinned host memory, assess FULL, and D2H of the "
@@ -366,7 +371,7 @@ def main():
     alu_peak = n_sm * 128 * sm_max * 1e6 / 1e12      # FP32-pipe lane-ops/s (FMA = 1 op), Tops/s
     Pk = stencil_cells(cfg)
     W_state = 4 * Pk + 200                           # SURVEY.md §8(d) algorithmic ops per state
-    states_per_launch = n_states / world
+    states_per_launch = n_states                     # per rank (one map per GPU)
     t_kernel = kern_s / K                            # per launch (update scatter included: < 1%)
     achieved = states_per_launch * W_state / t_kernel / 1e12
     bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
@@ -412,13 +417,14 @@ def main():
         extras.update(highres_update(S, stream, torch))
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: T_hills seed 5 (sinusoid hills, slope_rms 0.5, rocks, 1 cm noise; SURVEY.md §8(d)); "
                     "no weights",
             "config": {"workload": args.config, "nx": nx, "ny": ny, "n_yaw": n_yaw, "resolution_m": r,
-                       "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": n_states,
-                       "parallelism": "rows%d" % world if world > 1 else "single",
+                       "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": world * n_states,
+                       "states_per_gpu_per_step": n_states,
+                       "parallelism": "batch%d (one independent map per GPU)" % world if world > 1 else "single",
                        "l2": "256 MB buffer written between timed steps (outside the step events); "
                              "each step also writes %.2f GB of outputs" % (n_states * 16.125 / 1e9),
                        "step": "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
