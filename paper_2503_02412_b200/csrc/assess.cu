@@ -687,24 +687,27 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const bool col_any = __any_sync(0xffffffffu, col_in);
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
   const float Gx = pgx / p.r, Gy = pgy / p.r;
+  // warp w owns the RPW consecutive tile rows row0 .. row0 + RPW - 1 (state s = tile row row0 + s), so
+  // that on a border tile the warps whose footprints stay clear of the border take the interior path
+  const int row0 = warp * RPW;
   // tile-plane height at state s: zref0 + s * zstep (absolute, metres)
-  const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)warp - (float)(TY / 2), pc));
-  const float zstep = pgy * (float)NWARPS;
+  const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)row0 - (float)(TY / 2), pc));
+  const float zstep = pgy;
   // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, column lane)
-  const char* b8 = reinterpret_cast<const char*>(p02) + (size_t)(warp * PW + lane) * 8;
-  const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(warp * PW + lane) * 4;
-  const char* bv8 = reinterpret_cast<const char*>(pv) + (size_t)(warp * PW + lane) * 8;
-  const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(warp * PW + lane) * 4;
-  const char* bh = reinterpret_cast<const char*>(hh_s) + (size_t)(warp * PW + lane) * 4;
-  constexpr int RS8 = NWARPS * PW * 8, RS4 = NWARPS * PW * 4;  // state s -> s * NWARPS halo rows lower
+  const char* b8 = reinterpret_cast<const char*>(p02) + (size_t)(row0 * PW + lane) * 8;
+  const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(row0 * PW + lane) * 4;
+  const char* bv8 = reinterpret_cast<const char*>(pv) + (size_t)(row0 * PW + lane) * 8;
+  const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(row0 * PW + lane) * 4;
+  const char* bh = reinterpret_cast<const char*>(hh_s) + (size_t)(row0 * PW + lane) * 4;
+  constexpr int RS8 = PW * 8, RS4 = PW * 4;  // state s -> s halo rows lower
 
-  // per state s (tile row warp + s NWARPS): record index in a bin plane, traversable-word index (-1: the
+  // per state s (tile row row0 + s): record index in a bin plane, traversable-word index (-1: the
   // state's row is outside the window)
   int tmy = -1;  // interior tiles: lane s < RPW writes the traversable word of state s
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
-    const long long lj = TJ * TY + warp + s * NWARPS - p.J_M;
+    const long long lj = TJ * TY + row0 + s - p.J_M;
     int py = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
     soff[s] = (py >= 0 && col_in) ? py * p.nx + pxs : -1;
@@ -721,7 +724,15 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   uint32_t* travk = p.trav + (size_t)kb * twplane;
   uint32_t* travk2 = travk + (size_t)p.H * twplane;
   int kc = kb % p.period;     // position in the yaw chain (restart at 0)
-  if (fast) {
+  // border tile: this warp takes the interior path when every halo row its footprints reach (halo rows
+  // row0 .. row0 + RPW - 1 + 2 R_T) is fully known and inside the window (validity row totals)
+  bool wfast = fast;
+  if (!fast && G::CB) {
+    bool full = true;
+    for (int hr = row0 + lane; hr < row0 + RPW + 2 * R_T; hr += 32) full &= pv[hr * PW + HX].x == (float)HX;
+    wfast = __all_sync(0xffffffffu, full);
+  }
+  if (wfast) {
     for (int k = kb; k < ke; ++k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
       const int e0 = __ldg(tab_off + k);
       const int4* rk = runs_s + (e0 - tab_base);
@@ -931,7 +942,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
                 const int src = __ffs(msk) - 1;
                 msk &= msk - 1;
                 const float mu = __shfl_sync(0xffffffffu, m0[s], src);
-                const float* rb = raw + (warp + (sp + s) * NWARPS) * HX + src;  // state's halo row, column src
+                const float* rb = raw + (row0 + sp + s) * HX + src;  // state's halo row, column src
                 float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
   #pragma unroll 1
                 for (int d = 0; d < nf; ++d) {
