@@ -191,6 +191,10 @@ static bool build_stencils(se2m_map* m, std::vector<int4>& runs, std::vector<int
 
 // Run-entry tables (AssessParams::full / chain) from the per-bin row runs: element offsets into a
 // halo prefix row of pitch PW = TX + 2 R_T + 1, relative to the state's own column.
+#ifndef SE2M_CELL_MAX
+#define SE2M_CELL_MAX 2  // endpoint moves of up to this many cells become single-cell chain entries
+#endif
+
 static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows,
                          std::vector<int4>& full, std::vector<int4>& chain) {
   const int RT = m->R_T, NR = 2 * RT + 1, PW = TX + 2 * RT + 1;
@@ -231,7 +235,7 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
       // cell entries, longer spans a prefix entry P[eb(hi)] - P[ea(lo)] (sign by endpoint order)
       auto span = [&](int d, int lo, int hi, int sg) {
         if (hi < lo) return;
-        if (hi - lo + 1 <= 2) {
+        if (hi - lo + 1 <= SE2M_CELL_MAX) {
           for (int di = lo; di <= hi; ++di) cells.push_back(cent(d, di, sg));
         } else if (sg > 0) {
           chain.push_back(pent(ea(d, lo), eb(d, hi), d));
