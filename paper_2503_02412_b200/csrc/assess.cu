@@ -715,8 +715,9 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     if (lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
   }
 
-  float2 S02[RPW];            // interior tiles: moments carried along the yaw chain
-  float SXH[RPW], SYH[RPW];
+  // interior tiles: moments carried along the yaw chain, packed across the state pairs (2q, 2q + 1)
+  // so that one FFMA2 / FADD2 updates a moment of two states
+  F2 S0p[RPW / 2], S2p[RPW / 2], SXp[RPW / 2], SYp[RPW / 2];
   // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
   const size_t twplane = (size_t)p.ny * p.trav_words;
   float4* outk = p.out + (size_t)kb * plane;
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
         if (restart) {
   #pragma unroll
-          for (int s = 0; s < RPW; ++s) { S02[s] = make_float2(0.f, 0.f); SXH[s] = SYH[s] = 0.f; }
+          for (int q = 0; q < RPW / 2; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
         }
         const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
 #pragma unroll kUnrollPre
@@ -769,15 +770,21 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           const char* pa4 = b4 + o.z;
           const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
   #pragma unroll
-          for (int s = 0; s < RPW; ++s) {
-            const float2 A = *reinterpret_cast<const float2*>(pa8 + s * RS8);
-            const float2 B = *reinterpret_cast<const float2*>(pb8 + s * RS8);
-            const float ax = *reinterpret_cast<const float*>(pa4 + s * RS4);
-            const float bxv = *reinterpret_cast<const float*>(pb4 + s * RS4);
-            const float2 dd = sub2(B, A);  // (run sum of h^, run sum of h^2)
-            S02[s] = add2(S02[s], dd);
-            SXH[s] += bxv - ax;  // sum of x' h^ (x' from the tile centre); -xs S0 is applied once below
-            SYH[s] = fmaf(dj, dd.x, SYH[s]);
+          for (int q = 0; q < RPW / 2; ++q) {
+            const int s = 2 * q;
+            const float2 A0 = *reinterpret_cast<const float2*>(pa8 + s * RS8);
+            const float2 B0 = *reinterpret_cast<const float2*>(pb8 + s * RS8);
+            const float2 A1 = *reinterpret_cast<const float2*>(pa8 + (s + 1) * RS8);
+            const float2 B1 = *reinterpret_cast<const float2*>(pb8 + (s + 1) * RS8);
+            const F2 ax = pk(*reinterpret_cast<const float*>(pa4 + s * RS4),
+                             *reinterpret_cast<const float*>(pa4 + (s + 1) * RS4));
+            const F2 bx = pk(*reinterpret_cast<const float*>(pb4 + s * RS4),
+                             *reinterpret_cast<const float*>(pb4 + (s + 1) * RS4));
+            const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x);  // run sums of h^ of the two states
+            S0p[q] = S0p[q] + d0;
+            S2p[q] = S2p[q] + (pk(B0.y, B1.y) - pk(A0.y, A1.y));
+            SXp[q] = SXp[q] + (bx - ax);  // sum of x' h^ (x' from the tile centre); -xs S0 applied below
+            SYp[q] = fma2(bc(dj), d0, SYp[q]);
           }
         }
         // single cells entering / leaving the footprint since bin k-1: one h^ load per state
@@ -788,13 +795,14 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
           const char* ph = bh + o.x;
   #pragma unroll
-          for (int s = 0; s < RPW; ++s) {
-            const float h = *reinterpret_cast<const float*>(ph + s * RS4);
-            const float sh = sg * h;
-            S02[s].x += sh;
-            S02[s].y = fmaf(sh, h, S02[s].y);
-            SXH[s] = fmaf(cx, h, SXH[s]);
-            SYH[s] = fmaf(sdj, h, SYH[s]);
+          for (int q = 0; q < RPW / 2; ++q) {
+            const F2 h = pk(*reinterpret_cast<const float*>(ph + 2 * q * RS4),
+                            *reinterpret_cast<const float*>(ph + (2 * q + 1) * RS4));
+            const F2 sh = bc(sg) * h;
+            S0p[q] = S0p[q] + sh;
+            S2p[q] = fma2(sh, h, S2p[q]);
+            SXp[q] = fma2(bc(cx), h, SXp[q]);
+            SYp[q] = fma2(bc(sdj), h, SYp[q]);
           }
         }
         const float4 gc = __ldg(p.geoc + 4 * k), gd = __ldg(p.geoc + 4 * k + 1);
@@ -804,9 +812,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         unsigned tmine = 0;
   #pragma unroll
         for (int s = 0; s < RPW; s += 2) {
-          const F2 S0p = pk(S02[s].x, S02[s + 1].x);
-          const StateOut2 o = arrow2(S0p, pk(S02[s].y, S02[s + 1].y), fma2(bc(-xs), S0p, pk(SXH[s], SXH[s + 1])),
-                                     pk(SYH[s], SYH[s + 1]),
+          const int q = s / 2;
+          const StateOut2 o = arrow2(S0p[q], S2p[q], fma2(bc(-xs), S0p[q], SXp[q]), SYp[q],
                                      pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
                                      aG1, aG2, gc, gd, ge, gf, p);
           store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
