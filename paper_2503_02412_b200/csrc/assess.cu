@@ -5,16 +5,21 @@
 //   1. the tile + an R_T-cell footprint halo of the ring-buffered elevation map lands in shared
 //      memory, by one TMA box (cp.async.bulk.tensor.2d) when the halo lies inside the window and
 //      does not straddle the ring seam, by coalesced LDG otherwise;
-//   2. per halo row, exclusive prefix sums of h^ = h - h_ref, h^2, x' h^ (and, for tiles with
-//      unknown / out-of-window cells, of the indicator v, x' v, x'^2 v) are built with warp scans;
+//   2. a least-squares tile plane is removed (h^ = h - h_ref - plane), and per halo row exclusive prefix
+//      sums of h^, h^2, x' h^ (and, for tiles with unknown / out-of-window cells, of the indicator v,
+//      x' v, x'^2 v) are built with warp scans, plus the h^ plane itself (NaN = unknown);
 //   3. for each representative yaw bin k < n_yaw/2 (reading R5: the ellipse depends on theta mod
 //      pi), every state's footprint moments (FindEllipticalPoints + the covariance sums of Alg. 1
-//      lines 1-8) are sums over the <= 2R+1 stencil rows of prefix differences: O(rows) per
-//      state instead of O(cells) — an exact re-association of the sums of Alg. 1 lines 2-8;
-//   4. register epilogue: covariance, closed-form smallest eigenpair + one inverse-iteration
-//      refinement (GetMinEigenVecWithCurv, line 9), kappa, Eqs. 2-3 frame, pitch/roll (lines
-//      12-13), thresholds and weighted risk (lines 10-18), written for bin k AND bin k + n/2
-//      (x_yaw negated: pitch/roll negated, everything else identical — pin Q3);
+//      lines 1-8) are carried along the yaw chain: at a restart, sums over the <= 2R+1 stencil rows
+//      of prefix differences; between bins, the cells that enter or leave the footprint (single-cell
+//      entries) — an exact re-association of the sums of Alg. 1 lines 2-8;
+//   4. register epilogue, two states per packed FP32x2 instruction: covariance; for interior tiles
+//      the arrowhead form in the footprint's eigenbasis (trigonometric seed + one secular Newton
+//      step), for border tiles the general 3x3 solve (trigonometric lambda0 + adj(M) eigenvector
+//      refined once; FP64 for footprints with < 32 known cells) (GetMinEigenVecWithCurv, line 9),
+//      kappa, Eqs. 2-3 frame, pitch/roll (lines 12-13), thresholds and weighted risk (lines 10-18),
+//      written for bin k AND bin k + n/2 (x_yaw negated: pitch/roll negated, everything else
+//      identical — pin Q3);
 //   5. coalesced 16-B stores of (risk, pitch, roll, z) state records + ballot-packed traversable bits.
 // No tensor cores: the path is not a dense contraction.
 #include <math.h>
