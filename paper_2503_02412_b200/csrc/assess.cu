@@ -435,6 +435,15 @@ constexpr float kDirectN = SE2M_DIRECT_N;
 // ------------------------------------------------------------------------------------------
 // The assess kernel.
 // ------------------------------------------------------------------------------------------
+// per-bin constants of a CTA's chunk in shared memory (interior path)
+struct BinC {
+  int e0, npre, nr, restart;  // chain entries [e0, e0 + nr) relative to the CTA's table, prefix entries first
+  int f0, nf, pad0, pad1;     // full rows [f0, f0 + nf) relative to the CTA's table (border / unknown tiles)
+  float4 cs;                  // (cos, sin) theta_k, -, -
+  float4 gc, gd, ge, gf;      // geoc[4k .. 4k + 3]
+  float4 gq;                  // (Gq1, Gq2, aG1, aG2): the tile plane's gradient in the bin's eigenbasis
+};
+
 template <int R_T>
 struct Geom {
   static constexpr int TY = tile_rows(R_T);
@@ -454,7 +463,9 @@ struct Geom {
   static constexpr size_t hh_off = CB ? pvxx_off + 4 * E : pv_off;
   static constexpr size_t misc_off = ((CB ? hh_off : pvxx_off) + 4 * E + 15) / 16 * 16;
   static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
-  static size_t bytes(int tab_cap) { return runs_off + (size_t)tab_cap * 16; }
+  // then the per-bin constants of the CTA's chunk (BinC: table offsets + interior geometry), so the
+  // bin loop reads them with broadcast LDS instead of waiting on global loads at every bin
+  static size_t bytes(int tab_cap, int k_chunk) { return runs_off + (size_t)tab_cap * 16 + (size_t)k_chunk * sizeof(BinC); }
 };
 
 template <int R_T>
@@ -472,6 +483,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
   float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
+  BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (size_t)p.tab_cap * 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx_rel = (int)(blockIdx.x % (unsigned)p.tiles_x);
@@ -624,6 +636,28 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     }
   }
 
+  {  // per-bin constants of the chunk
+    const float Gx = pgx / p.r, Gy = pgy / p.r;
+    for (int b = tid; b < ke - kb; b += NTHREADS) {
+      const int k = kb + b;
+      BinC c;
+      c.e0 = __ldg(tab_off + k) - tab_base;
+      c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
+      c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
+      c.restart = (b == 0 || k % p.period == 0) ? 1 : 0;
+      c.f0 = n_chain + __ldg(p.full_off + k) - full_base;
+      c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
+      c.pad0 = c.pad1 = 0;
+      const float2 csk = __ldg(p.cs + k);
+      c.cs = make_float4(csk.x, csk.y, 0.f, 0.f);
+      c.gc = __ldg(p.geoc + 4 * k); c.gd = __ldg(p.geoc + 4 * k + 1);
+      c.ge = __ldg(p.geoc + 4 * k + 2); c.gf = __ldg(p.geoc + 4 * k + 3);
+      const float Gq1 = fmaf(Gx, c.ge.x, Gy * c.ge.y), Gq2 = fmaf(Gy, c.ge.x, -Gx * c.ge.y);
+      c.gq = make_float4(Gq1, Gq2, c.gd.y * Gq1, c.gd.z * Gq2);
+      bins_s[b] = c;
+    }
+  }
+
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
     float hh[CPL], xp[CPL], vv[CPL];
@@ -691,7 +725,6 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   if (col_in) { pxs = p.pxM + (int)li; if (pxs >= p.nx) pxs -= p.nx; }
   const bool col_any = __any_sync(0xffffffffu, col_in);
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
-  const float Gx = pgx / p.r, Gy = pgy / p.r;
   // warp w owns the RPW consecutive tile rows row0 .. row0 + RPW - 1 (state s = tile row row0 + s), so
   // that on a border tile the warps whose footprints stay clear of the border take the interior path
   const int row0 = warp * RPW;
@@ -729,7 +762,6 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   float4* outk2 = outk + (size_t)p.H * plane;
   uint32_t* travk = p.trav + (size_t)kb * twplane;
   uint32_t* travk2 = travk + (size_t)p.H * twplane;
-  int kc = kb % p.period;     // position in the yaw chain (restart at 0)
   // border tile: this warp takes the interior path when every halo row its footprints reach (halo rows
   // row0 .. row0 + RPW - 1 + 2 R_T) is fully known and inside the window (validity row totals)
   bool wfast = fast;
@@ -739,13 +771,12 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     wfast = __all_sync(0xffffffffu, full);
   }
   if (wfast) {
-    for (int k = kb; k < ke; ++k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
-      const int e0 = __ldg(tab_off + k);
-      const int4* rk = runs_s + (e0 - tab_base);
-      const int nr = __ldg(tab_off + k + 1) - e0;
-      const float2 csk = __ldg(p.cs + k);
-      const bool restart = k == kb || kc == 0;
-      if (++kc == p.period) kc = 0;
+    const BinC* bc_k = bins_s;
+    for (int k = kb; k < ke; ++k, ++bc_k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
+      const int4 meta = *reinterpret_cast<const int4*>(bc_k);  // (e0, npre, nr, restart)
+      const int4* rk = runs_s + meta.x;
+      const int nr = meta.z;
+      const bool restart = meta.w != 0;
       // interior tiles lie inside the window (their whole halo does), so every state is stored
       auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
         __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
@@ -765,7 +796,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   #pragma unroll
           for (int q = 0; q < RPW / 2; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
         }
-        const int npre = __ldg(p.chain_mid + k) - e0;  // prefix entries first, then cell entries
+        const int npre = meta.y;  // prefix entries first, then cell entries
 #pragma unroll kUnrollPre
         for (int d = 0; d < npre; ++d) {
           const int4 o = rk[d];
@@ -810,10 +841,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
             SYp[q] = fma2(bc(sdj), h, SYp[q]);
           }
         }
-        const float4 gc = __ldg(p.geoc + 4 * k), gd = __ldg(p.geoc + 4 * k + 1);
-        const float4 ge = __ldg(p.geoc + 4 * k + 2), gf = __ldg(p.geoc + 4 * k + 3);
-        const float Gq1 = fmaf(Gx, ge.x, Gy * ge.y), Gq2 = fmaf(Gy, ge.x, -Gx * ge.y);
-        const float aG1 = gd.y * Gq1, aG2 = gd.z * Gq2;
+        const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
+        const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
         unsigned tmine = 0;
   #pragma unroll
         for (int s = 0; s < RPW; s += 2) {
@@ -845,20 +874,19 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 #pragma unroll
     for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
       if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
-    int kc = kb % p.period;
 #pragma unroll 1
     for (int k = kb; k < ke; ++k) {
-      const int f0 = __ldg(p.full_off + k);
-      const int4* rkf = runs_s + n_chain + (f0 - full_base);
-      const int nf = __ldg(p.full_off + k + 1) - f0;
+      const BinC* bk = bins_s + (k - kb);
+      const int4 meta = *reinterpret_cast<const int4*>(&bk->e0);
+      const int4 metaf = *reinterpret_cast<const int4*>(&bk->f0);
+      const int4* rkf = runs_s + metaf.x;
+      const int nf = metaf.y;
       // the yaw chain, or (R_T = 32) the full rows of every bin as prefix entries
-      const int e0 = G::CB ? __ldg(tab_off + k) : 0;
-      const int4* rk = G::CB ? runs_s + (e0 - tab_base) : rkf;
-      const int nr = G::CB ? __ldg(tab_off + k + 1) - e0 : nf;
-      const int npre = G::CB ? __ldg(p.chain_mid + k) - e0 : nf;
-      const float2 csk = __ldg(p.cs + k);
-      const bool restart = k == kb || kc == 0 || !G::CB;
-      if (++kc == p.period) kc = 0;
+      const int4* rk = G::CB ? runs_s + meta.x : rkf;
+      const int nr = G::CB ? meta.z : nf;
+      const int npre = G::CB ? meta.y : nf;
+      const float2 csk = make_float2(bk->cs.x, bk->cs.y);
+      const bool restart = meta.w != 0 || !G::CB;
       if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
 #pragma unroll 1
       for (int d = 0; d < npre; ++d) {
@@ -1016,7 +1044,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 template <int R_T>
 static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {
   using G = Geom<R_T>;
-  const size_t smem = G::bytes(p.tab_cap);
+  const size_t smem = G::bytes(p.tab_cap, p.k_chunk);
   // the attribute is per device: remember the configured size per device ordinal
   static int configured[64] = {0};
   int dev = 0;
@@ -1036,14 +1064,14 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
   return cudaGetLastError();
 }
 
-size_t assess_smem_bytes(int R_T, int tab_cap) {
+size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
   switch (R_T) {
-    case 4: return Geom<4>::bytes(tab_cap);
-    case 8: return Geom<8>::bytes(tab_cap);
-    case 12: return Geom<12>::bytes(tab_cap);
-    case 16: return Geom<16>::bytes(tab_cap);
-    case 24: return Geom<24>::bytes(tab_cap);
-    case 32: return Geom<32>::bytes(tab_cap);
+    case 4: return Geom<4>::bytes(tab_cap, k_chunk);
+    case 8: return Geom<8>::bytes(tab_cap, k_chunk);
+    case 12: return Geom<12>::bytes(tab_cap, k_chunk);
+    case 16: return Geom<16>::bytes(tab_cap, k_chunk);
+    case 24: return Geom<24>::bytes(tab_cap, k_chunk);
+    case 32: return Geom<32>::bytes(tab_cap, k_chunk);
     default: return 0;
   }
 }

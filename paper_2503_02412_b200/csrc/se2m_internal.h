@@ -84,7 +84,7 @@ struct AssessParams {
 
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.
 // dynamic shared memory of one assess CTA (halo, prefix planes, h^ plane, run tables of tab_cap entries)
-size_t assess_smem_bytes(int R_T, int tab_cap);
+size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk);
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
                           cudaStream_t stream);
 

@@ -742,10 +742,10 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
       cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
     }
     const int step = m->period > 1 ? m->period : 1;
-    if (assess_smem_bytes(m->R_T, cap) <= (size_t)m->smem_optin || chunk <= step) break;
+    if (assess_smem_bytes(m->R_T, cap, chunk) <= (size_t)m->smem_optin || chunk <= step) break;
     chunk = std::max(step, (chunk / 2 + step - 1) / step * step);
   }
-  if (assess_smem_bytes(m->R_T, cap) > (size_t)m->smem_optin)
+  if (assess_smem_bytes(m->R_T, cap, chunk) > (size_t)m->smem_optin)
     return fail(m, SE2M_ERR_UNSUPPORTED, "assess: footprint tables exceed the shared memory of a CTA");
   p.k_chunk = chunk;
   p.tab_cap = cap;
