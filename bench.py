@@ -9,8 +9,10 @@ from an HBM-resident world buffer for `value`, from pinned host memory for `e2e`
 FULL (Alg. 1 for every SE(2) state), and a batch query of planner states.  Prints ONE JSON line
 on rank 0.  Under torchrun (N > 1) every GPU runs its own map of the configuration's size (a batch
 of independent maps, one per GPU: weak scaling — the path has no exchange step, so no data-path
-collective); value = all ranks' states / the max-over-ranks time.  (Splitting ONE map across GPUs —
-yaw slices or interleaved tile-row bands — is in the library, se2m_params.shard_mode, and tested.)
+collective); value = all ranks' states / the max-over-ranks time.  `--shard rows` instead splits ONE
+map across the GPUs in interleaved tile-row bands: each rank is fed only its own rows, the halo rows
+its tiles read are exchanged with NCCL send/recv every step (Se2Map.exchange_halo), and it assesses
+its own tile rows (strong scaling; SURVEY.md §8(e) "row bands + halo").
 
 `--impl reference`: the FP64 CPU oracle (oracle/, the test reference) timed as it stands on this
 host's cores on a bounded random sample of the same workload per step (rank 0 only).
@@ -48,6 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--queries", type=int, default=4096)
+    ap.add_argument("--shard", default="maps", choices=["maps", "rows"],
+                    help="N > 1: 'maps' = one independent map per GPU (weak scaling, default); 'rows' = ONE map "
+                         "split into interleaved tile-row bands, each rank fed only its own rows, halo rows "
+                         "exchanged by NCCL send/recv every step (strong scaling, SURVEY.md §8(e))")
     return ap.parse_args()
 
 
@@ -240,8 +246,10 @@ def main():
     K, W = args.steps, max(args.warmup, 3)
     positions, margin = robot_positions(cfg, K + W + 2)
     # multi-GPU: a batch of independent maps, one per GPU (weak scaling: the path needs no exchange,
-    # SURVEY.md §8(e) "batches of maps"); rank g's robot drives the same path 1 km further east
-    off_x = 1000.0 * rank
+    # SURVEY.md §8(e) "batches of maps"); rank g's robot drives the same path 1 km further east.
+    # --shard rows: one map, every rank on the same path, row bands + NCCL halo exchange (strong scaling)
+    rows_mode = args.shard == "rows" and world > 1
+    off_x = 0.0 if rows_mode else 1000.0 * rank
     positions = [(x + off_x, y) for (x, y) in positions]
     robot0 = (cfg["robot"][0] + off_x, cfg["robot"][1])
 
@@ -256,8 +264,9 @@ def main():
     world_d = torch.from_numpy(world_h).to(dev)
     world_pinned = torch.from_numpy(world_h).pin_memory()
 
+    shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS, rank=rank, world_size=world) if rows_mode else {}
     m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
-                 robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream)
+                 robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream, **shard_kw)
     rng = np.random.default_rng(1)
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -270,10 +279,30 @@ def main():
         return np.stack([rng.uniform(I_M * r, (I_M + nx) * r, nq), rng.uniform(J_M * r, (J_M + ny) * r, nq),
                          rng.uniform(-math.pi, math.pi, nq)], axis=1)
 
+    def own_row_runs():
+        """(j0, n) runs of the window rows this rank owns (all rows unless --shard rows)."""
+        runs = []
+        for j in m.owned_rows():
+            if runs and runs[-1][0] + runs[-1][1] == j:
+                runs[-1][1] += 1
+            else:
+                runs.append([int(j), 1])
+        return runs
+
+    def update(src, I_M, J_M, host=False):
+        """H2: the whole window, or (--shard rows) the rank's own rows only, then the halo exchange."""
+        v = window_view(src, I_M, J_M)
+        if not rows_mode:
+            m.update_elevation(v.numpy() if host else v)
+            return
+        for j0, n in own_row_runs():
+            m.update_elevation(v[j0:j0 + n].numpy() if host else v[j0:j0 + n], j0=j0)
+        m.exchange_halo()
+
     def step(t, src):
         m.shift_window(*positions[t])
         I_M, J_M = m.origin()
-        m.update_elevation(window_view(src, I_M, J_M))
+        update(src, I_M, J_M)
         m.assess_se2(S.SE2M_FULL)
         return I_M, J_M
 
@@ -297,7 +326,7 @@ def main():
                 ev[t][0].record(stream)
                 m.shift_window(*positions[tt])
                 I_M, J_M = m.origin()
-                m.update_elevation(window_view(world_d, I_M, J_M))
+                update(world_d, I_M, J_M)
                 evk[t][0].record(stream)
                 m.assess_se2(S.SE2M_FULL)
                 evk[t][1].record(stream)
@@ -311,7 +340,9 @@ def main():
     tot_s = sum(step_ms) / 1e3
     kern_s = sum(kern_ms) / 1e3
     tot_s, kern_s = max_over_ranks([tot_s, kern_s], world, dev)
-    value = world * n_states * K / tot_s           # all ranks' states / the slowest rank's time
+    n_jobs = 1 if rows_mode else world             # maps assessed per step (rows: one map split in bands)
+    own_states = len(m.owned_rows()) * nx * n_yaw  # this rank's states of the last window
+    value = n_jobs * n_states * K / tot_s          # all ranks' states / the slowest rank's time
 
     # ---- e2e: public API with host buffers (H2D of the step's map from pinned memory, D2H of the
     #      risk map to pinned memory: the paper sends the risk map back to the CPU) -----
@@ -331,7 +362,7 @@ def main():
             for t in range(2):                      # warm the staging buffers
                 m.shift_window(*positions[t])
                 I_M, J_M = m.origin()
-                m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
+                update(world_pinned, I_M, J_M, host=True)
                 m.assess_se2(S.SE2M_FULL)
                 m.download_compact_rep(out=comp[t % 2])
             m.synchronize()
@@ -342,16 +373,17 @@ def main():
             for t in range(ke):
                 m.shift_window(*positions[W + t])
                 I_M, J_M = m.origin()
-                m.update_elevation(window_view(world_pinned, I_M, J_M).numpy())
+                update(world_pinned, I_M, J_M, host=True)
                 m.assess_se2(S.SE2M_FULL)
                 m.download_compact_rep(out=comp[t % 2])
             m.synchronize()
             e2e_s = time.perf_counter() - t0
         e2e_s = max_over_ranks([e2e_s], world, dev)[0]
-        e2e = {"value": world * n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nx * ny * 4,
+        e2e = {"value": n_jobs * n_states * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": own * nx * 4,
                "d2h_bytes_per_step": n_rep * own * nx * 2 + n_rep * own * wpr * 4, "ms_per_step": e2e_s / ke * 1e3,
                "steps": ke,
-               "note": "per step: H2D of the full window from pinned host memory, assess FULL, and D2H of the "
+               "note": "per step: H2D of the full window (--shard rows: the rank's own rows, then the NCCL halo "
+                       "exchange) from pinned host memory, assess FULL, and D2H of the "
                        "risk map (u16, 1.5e-5 resolution) + traversable bits in logical order to pinned host "
                        "memory (se2m_download_compact_rep: the n_yaw/2 representative planes, Risk being "
                        "pi-periodic in theta; the paper sends the risk map to the CPU, PAPER.md:95); D2H of step "
@@ -371,7 +403,7 @@ def main():
     alu_peak = n_sm * 128 * sm_max * 1e6 / 1e12      # FP32-pipe lane-ops/s (FMA = 1 op), Tops/s
     Pk = stencil_cells(cfg)
     W_state = 4 * Pk + 200                           # SURVEY.md §8(d) algorithmic ops per state
-    states_per_launch = n_states                     # per rank (one map per GPU)
+    states_per_launch = own_states if rows_mode else n_states   # per rank
     t_kernel = kern_s / K                            # per launch (update scatter included: < 1%)
     achieved = states_per_launch * W_state / t_kernel / 1e12
     bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
@@ -417,18 +449,22 @@ def main():
         extras.update(highres_update(S, stream, torch))
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong" if rows_mode else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: T_hills seed 5 (sinusoid hills, slope_rms 0.5, rocks, 1 cm noise; SURVEY.md §8(d)); "
                     "no weights",
             "config": {"workload": args.config, "nx": nx, "ny": ny, "n_yaw": n_yaw, "resolution_m": r,
-                       "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": world * n_states,
-                       "states_per_gpu_per_step": n_states,
-                       "parallelism": "batch%d (one independent map per GPU)" % world if world > 1 else "single",
+                       "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": n_jobs * n_states,
+                       "states_per_gpu_per_step": own_states if rows_mode else n_states,
+                       "parallelism": ("rows%d (one map, interleaved tile-row bands, NCCL halo exchange)" % world
+                                       if rows_mode else "batch%d (one independent map per GPU)" % world)
+                                      if world > 1 else "single",
                        "l2": "256 MB buffer written between timed steps (outside the step events); "
                              "each step also writes %.2f GB of outputs" % (n_states * 16.125 / 1e9),
-                       "step": "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
-                               "query(%d states)" % args.queries},
+                       "step": ("shift_window + update_elevation(own rows, D2D from HBM) + exchange_halo (NCCL) + "
+                                "assess_se2(FULL, own tile rows) + query(%d states)" if rows_mode else
+                                "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
+                                "query(%d states)") % args.queries},
             "ms_per_full_update": kern_s / K * 1e3,
             "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
             "ms_per_full_update_p10_p50_p90": [float(np.percentile(kern_ms, q)) for q in (10, 50, 90)],

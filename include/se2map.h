@@ -178,6 +178,31 @@ se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* t
  * (all ny rows unless row-band sharded): *n of them, listed in rows[] if rows is not NULL. */
 se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t* n);
 
+/* Row-band halo exchange (SE2M_SHARD_ROWS, world_size G > 1; SURVEY.md §8(e) "row bands + halo";
+ * a state's risk reads the elevation under its footprint, up to R cells away).  Rank g owns
+ * the world tile rows TJ = g (mod G) (se2m_shard_plan).  A rank whose update_elevation wrote only its own
+ * rows (se2m_owned_rows) lacks the R_T rows on either side of each owned tile row, which rank g - 1 and
+ * rank g + 1 own.  Exchange, per step, before se2m_assess_se2:
+ *   se2m_halo_pack(m, -1, a)  -> send a to rank g - 1;   se2m_halo_pack(m, +1, b) -> send b to rank g + 1;
+ *   receive c from rank g + 1 -> se2m_halo_unpack(m, +1, c);  d from rank g - 1 -> se2m_halo_unpack(m, -1, d).
+ * The transfer (NCCL send/recv over NVLink) is the caller's; the Python binding's Se2Map.exchange_halo
+ * does it with torch.distributed on the map's stream.  Buffers: device memory of cap x slab_rows x nx
+ * floats (se2m_halo_size), slab q = slab_rows window-width rows in logical column order; rows outside the
+ * window are NaN in a packed buffer and ignored on unpack.  Slab lists are derived from the window origin,
+ * which every rank shares, so sender and receiver agree without metadata.  pack only reads the ring;
+ * unpack writes the received rows and marks them dirty (INCREMENTAL).  Both are asynchronous on the map's
+ * stream.  SE2M_ERR_INVALID_ARG unless row-sharded with world_size > 1 (or dir / pointers bad);
+ * SE2M_ERR_UNSUPPORTED when R_T exceeds the tile height (the halo would reach tile rows TJ +- 2). */
+se2m_status se2m_halo_size(const se2m_map* m, int32_t* cap, int32_t* slab_rows);
+se2m_status se2m_halo_pack(se2m_map* m, int32_t dir, float* dst);
+se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* src);
+/* Host-only (no device): the slab list of rank `sender` for window origin row J_M: first_rows[q] = first
+ * world row of slab q (slab_rows rows), or INT64_MIN past the end of the list; last = 0: the first rows of
+ * the sender's tile rows (the slabs it sends to rank sender - 1), 1: the last rows (to sender + 1).
+ * first_rows (cap entries) may be NULL to query cap / slab_rows. */
+se2m_status se2m_halo_plan(const se2m_params* p, int64_t J_M, int32_t sender, int32_t last, int32_t* cap,
+                           int32_t* slab_rows, int64_t* first_rows);
+
 /* NEXT-1: integrate one LiDAR frame into the elevation window (§V.A, Fig. 3):
  * points (n x 3 float, sensor frame; host or device per mem) are transformed with the pose, points
  * outside the window or outside the body-frame height band are ignored, each point gets the

@@ -1154,6 +1154,34 @@ cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, 
   return cudaGetLastError();
 }
 
+// row-band halo exchange: pack this rank's outgoing slabs into a contiguous device buffer, or write the
+// slabs received from a neighbour into the ring (one thread per cell; coalesced along the row)
+__global__ void halo_kernel(const HaloArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y, q = blockIdx.z;
+  if (i >= a.nx) return;
+  const long long TJ = a.TJ0 + (long long)q * a.G;
+  const long long W = TJ * a.TY + (a.last ? a.TY - a.R_T : 0) + r;
+  const long long j = W - a.J_M;
+  const bool in = TJ <= a.TJb && j >= 0 && j < a.ny;
+  float* b = a.buf + ((size_t)q * a.R_T + r) * a.nx + i;
+  if (!in) {
+    if (!a.unpack) *b = __int_as_float(0x7fc00000);
+    return;
+  }
+  int px = a.pxM + i; if (px >= a.nx) px -= a.nx;
+  int py = a.pyM + (int)j; if (py >= a.ny) py -= a.ny;
+  float* c = a.h + (size_t)py * a.ldh + px;
+  if (a.unpack) *c = *b;
+  else *b = *c;
+}
+
+cudaError_t launch_halo(const HaloArgs& a, int cap, cudaStream_t s) {
+  if (cap <= 0 || a.R_T <= 0) return cudaSuccess;
+  halo_kernel<<<dim3((a.nx + 127) / 128, a.R_T, cap), 128, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 __device__ __forceinline__ long long floor_div32(long long a) { return a >= 0 ? a / 32 : -((-a + 31) / 32); }
 
 __device__ __forceinline__ bool row_owned(const AssessParams& p, int j) {

@@ -108,6 +108,20 @@ cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt,
                               cudaStream_t s);
 cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
                                 int w, int hgt, const float* src, long long ld, const uint8_t* known, cudaStream_t s);
+// Row-band halo slabs (SE2M_SHARD_ROWS; enumeration in se2map.cu): slab q holds world rows
+// [W_q, W_q + R_T), W_q = TJ_q TY (the first rows of tile row TJ_q) or TJ_q TY + TY - R_T (the last rows),
+// TJ_q = TJ0 + q G while TJ_q <= TJb; buffer layout [q][r][i], i = logical column.  Rows outside the
+// window: NaN in a packed buffer, untouched in the ring on unpack.
+struct HaloArgs {
+  float* h;                // ring heights [ny][ldh]
+  float* buf;              // device slabs [cap][R_T][nx]
+  int ldh, nx, ny, pxM, pyM;
+  long long J_M;           // window origin row (world)
+  long long TJ0, TJb;      // first tile row of the list, last tile row of the range
+  int G, TY, R_T, last;    // last = 1: the last R_T rows of each tile row, 0: the first R_T rows
+  int unpack;              // 0: ring -> buf, 1: buf -> ring
+};
+cudaError_t launch_halo(const HaloArgs& a, int cap, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
 // packed_rows > 0: only the rank's own rows (row-band sharding), packed in increasing order

@@ -379,6 +379,57 @@ extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int
   return SE2M_OK;
 }
 
+// ---- row-band halo exchange (SE2M_SHARD_ROWS) --------------------
+// Rank g owns the world tile rows TJ = g (mod G).  Assessing tile row TJ reads R_T rows on either side
+// (the CTA's halo), which lie in tile rows TJ - 1 (rank g - 1) and TJ + 1 (rank g + 1) when R_T <= TY.
+// A rank that received only its own rows sends, for every owned tile row, its first R_T rows to rank
+// g - 1 and its last R_T rows to rank g + 1.  Both sides enumerate the slabs from the common window
+// origin (every rank shifts the same window), so no metadata is exchanged; the list has a fixed
+// capacity per window size so the buffers are allocated once.
+static int halo_cap(int ny, int TY, int G) { return ((ny + TY - 1) / TY + 3 + G - 1) / G; }
+// tile rows sent by `sender`: TJ0, TJ0 + G, ... <= TJb (the tile rows meeting the window, +-1)
+static void halo_list(long long J_M, int ny, int TY, int G, int sender, long long* TJ0, long long* TJb) {
+  const long long TJa = floor_div(J_M, TY) - 1;
+  *TJb = floor_div(J_M + ny - 1, TY) + 1;
+  *TJ0 = TJa + pmod((long long)sender - TJa, G);
+}
+static se2m_status halo_check(const se2m_params* p, int R_T) {
+  if (p->shard_mode != SE2M_SHARD_ROWS || p->world_size < 2)
+    return SE2M_ERR_INVALID_ARG;
+  if (R_T > tile_rows(R_T)) return SE2M_ERR_UNSUPPORTED;  // the halo would reach tile rows TJ +- 2
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_halo_plan(const se2m_params* p, int64_t J_M, int32_t sender, int32_t last, int32_t* cap,
+                                      int32_t* slab_rows, int64_t* first_rows) {
+  se2m_status st = validate(p);
+  if (st != SE2M_OK) return st;
+  se2m_map m;  // host-only: the footprint radius decides R_T and the tile height
+  m.prm = *p;
+  m.paired = (p->n_yaw % 2 == 0) ? 1 : 0;
+  m.H = m.paired ? p->n_yaw / 2 : p->n_yaw;
+  std::vector<int4> runs;
+  std::vector<int> nrows;
+  std::vector<float4> geo, geoc;
+  std::vector<float2> cs;
+  if (!build_stencils(&m, runs, nrows, geo, geoc, cs)) return fail(nullptr, SE2M_ERR_UNSUPPORTED, "stencil");
+  st = halo_check(p, m.R_T);
+  if (st != SE2M_OK) return fail(nullptr, st, "halo_plan: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
+  if (sender < 0 || sender >= p->world_size) return fail(nullptr, SE2M_ERR_INVALID_ARG, "halo_plan: bad sender");
+  const int TY = tile_rows(m.R_T), G = p->world_size, n = halo_cap(p->ny, TY, G);
+  if (cap) *cap = n;
+  if (slab_rows) *slab_rows = m.R_T;
+  if (first_rows) {
+    long long TJ0, TJb;
+    halo_list(J_M, p->ny, TY, G, sender, &TJ0, &TJb);
+    for (int q = 0; q < n; ++q) {
+      const long long TJ = TJ0 + (long long)q * G;
+      first_rows[q] = TJ <= TJb ? TJ * TY + (last ? TY - m.R_T : 0) : INT64_MIN;
+    }
+  }
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   if (!out) return fail(nullptr, SE2M_ERR_INVALID_ARG, "out is NULL");
   se2m_status st = validate(p);
@@ -757,6 +808,59 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   m->dirty.clear();
   m->all_dirty = false;
   m->sdf_valid = false;  // the SDF follows the risk map: recompute with se2m_compute_sdf
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_halo_size(const se2m_map* m, int32_t* cap, int32_t* slab_rows) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  const se2m_status st = halo_check(&m->prm, m->R_T);
+  if (st != SE2M_OK) return st;
+  if (cap) *cap = halo_cap(m->prm.ny, tile_rows(m->R_T), m->prm.world_size);
+  if (slab_rows) *slab_rows = m->R_T;
+  return SE2M_OK;
+}
+
+static HaloArgs halo_args(se2m_map* m, int sender, int last, float* buf, int unpack) {
+  HaloArgs a;
+  a.h = m->d_h; a.buf = buf; a.ldh = m->ldh; a.nx = m->prm.nx; a.ny = m->prm.ny;
+  a.pxM = pmod(m->I_M, a.nx); a.pyM = pmod(m->J_M, a.ny); a.J_M = m->J_M;
+  a.G = m->prm.world_size; a.TY = tile_rows(m->R_T); a.R_T = m->R_T; a.last = last; a.unpack = unpack;
+  halo_list(m->J_M, a.ny, a.TY, a.G, sender, &a.TJ0, &a.TJb);
+  return a;
+}
+
+extern "C" se2m_status se2m_halo_pack(se2m_map* m, int32_t dir, float* dst) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  se2m_status st = halo_check(&m->prm, m->R_T);
+  if (st != SE2M_OK) return fail(m, st, "halo_pack: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
+  if (!dst || (dir != -1 && dir != 1)) return fail(m, SE2M_ERR_INVALID_ARG, "halo_pack: dir must be -1 or +1, dst non-NULL");
+  // to rank g - 1: the first R_T rows of each owned tile row; to rank g + 1: the last R_T rows
+  const HaloArgs a = halo_args(m, m->prm.rank, dir > 0 ? 1 : 0, dst, 0);
+  CUDA_TRY(m, launch_halo(a, halo_cap(a.ny, a.TY, a.G), m->stream), "halo pack");
+  m->launches++;
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* src) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  se2m_status st = halo_check(&m->prm, m->R_T);
+  if (st != SE2M_OK) return fail(m, st, "halo_unpack: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
+  if (!src || (from != -1 && from != 1)) return fail(m, SE2M_ERR_INVALID_ARG, "halo_unpack: from must be -1 or +1, src non-NULL");
+  // slabs from rank g + 1 are the first rows of its tile rows (it packed toward g - 1 = us), from g - 1 the last
+  const int G = m->prm.world_size, sender = pmod((long long)m->prm.rank + from, G), last = from < 0 ? 1 : 0;
+  const HaloArgs a = halo_args(m, sender, last, const_cast<float*>(src), 1);
+  const int cap = halo_cap(a.ny, a.TY, G);
+  CUDA_TRY(m, launch_halo(a, cap, m->stream), "halo unpack");
+  m->launches++;
+  m->have_data = true;
+  m->inpaint_valid = false;
+  for (int q = 0; q < cap; ++q) {  // written rows are dirty (H9)
+    const long long TJ = a.TJ0 + (long long)q * G;
+    if (TJ > a.TJb) break;
+    const long long W0 = std::max(TJ * a.TY + (last ? a.TY - a.R_T : 0), m->J_M);
+    const long long W1 = std::min(TJ * a.TY + (last ? a.TY : a.R_T), m->J_M + a.ny);
+    if (W0 < W1) m->dirty.push_back(Rect{m->I_M, m->I_M + a.nx, W0, W1});
+  }
   return SE2M_OK;
 }
 

@@ -32,7 +32,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
-           "se2m_owned_rows"]
+           "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan"]
 
 
 class Params(ctypes.Structure):
@@ -95,6 +95,11 @@ _lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
+_lib.se2m_halo_size.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
+_lib.se2m_halo_pack.argtypes = [_vp, _i32, _vp]
+_lib.se2m_halo_unpack.argtypes = [_vp, _i32, _vp]
+_lib.se2m_halo_plan.argtypes = [ctypes.POINTER(Params), _i64, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                _vp]
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
 _lib.se2m_last_error.argtypes = [_vp]
@@ -103,7 +108,8 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_download", "se2m_get_origin", "se2m_stencil_info", "se2m_synchronize", "se2m_tile_info",
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
-              "se2m_download_elevation"):
+              "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
+              "se2m_halo_plan"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -138,6 +144,12 @@ def _ptr(a):
     return a.ctypes.data, SE2M_MEM_HOST, a
 
 
+def _cuda_ptr(t):
+    if not (hasattr(t, "is_cuda") and t.is_cuda and t.is_contiguous()):
+        raise ValueError("expected a contiguous CUDA tensor")
+    return t.data_ptr()
+
+
 def _ptr_nocopy(a):
     if a is None:
         return None, SE2M_MEM_HOST, None
@@ -154,6 +166,23 @@ def shard_plan(params: Params) -> dict:
         raise Se2mError(st, _lib.se2m_last_error(None).decode())
     keys = ("n_rep", "k_lo", "k_hi", "tile_y", "row_mod", "row_rank")
     return {k: x.value for k, x in zip(keys, v)}
+
+
+def halo_plan(params: Params, J_M: int, sender: int, last: int) -> dict:
+    """Host-only (no GPU): the row-band halo slabs rank `sender` sends for window origin row J_M — the
+    first world row of each slab (None past the end of the list); last = 0: the first rows of its tile rows
+    (sent to rank sender - 1), 1: the last rows (sent to rank sender + 1).  See se2m_halo_plan."""
+    cap, rows = _i32(), _i32()
+    st = _lib.se2m_halo_plan(ctypes.byref(params), J_M, sender, last, ctypes.byref(cap), ctypes.byref(rows), None)
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    first = np.empty(cap.value, np.int64)
+    st = _lib.se2m_halo_plan(ctypes.byref(params), J_M, sender, last, ctypes.byref(cap), ctypes.byref(rows),
+                             first.ctypes.data)
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    return {"cap": cap.value, "slab_rows": rows.value,
+            "first_rows": [int(v) if v != np.iinfo(np.int64).min else None for v in first]}
 
 
 def sdf_from_mask(mask, resolution: float, d_max: float, device: int = 0):
@@ -397,5 +426,65 @@ class Se2Map:
     def synchronize(self):
         return self._check(_lib.se2m_synchronize(self.h))
 
+    # -- row-band halo exchange (SE2M_SHARD_ROWS, world_size > 1) ----------------------------------
+    def halo_size(self):
+        """(cap, slab_rows): a halo buffer holds cap x slab_rows x nx float32."""
+        cap, rows = _i32(), _i32()
+        self._check(_lib.se2m_halo_size(self.h, ctypes.byref(cap), ctypes.byref(rows)))
+        return cap.value, rows.value
+
+    def halo_pack(self, dir: int, dst):
+        """Outgoing slabs toward rank g + dir (dir = -1 / +1) into the CUDA tensor dst (asynchronous)."""
+        return self._check(_lib.se2m_halo_pack(self.h, dir, _cuda_ptr(dst)))
+
+    def halo_unpack(self, src, frm: int):
+        """Write the slabs received from rank g + frm (frm = -1 / +1) into the map (asynchronous)."""
+        return self._check(_lib.se2m_halo_unpack(self.h, frm, _cuda_ptr(src)))
+
+    def exchange_halo(self, group=None):
+        """One halo exchange over torch.distributed (NCCL on the GPU): pack both directions, send to the
+        neighbouring ranks g - 1 and g + 1 and receive from them, unpack — all ordered on the map's stream
+        (the NCCL transfers run on that stream too).  Call after update_elevation of the rank's own rows and
+        before assess_se2."""
+        import torch
+        import torch.distributed as dist
+        G, g = self.params.world_size, self.params.rank
+        if G < 2:
+            return
+        bufs = getattr(self, "_halo_bufs", None)
+        if bufs is None:
+            cap, rows = self.halo_size()
+            dev = torch.device("cuda", self.params.device)
+            bufs = [torch.empty((cap, rows, self.params.nx), dtype=torch.float32, device=dev) for _ in range(4)]
+            self._halo_bufs = bufs
+        send_dn, send_up, recv_up, recv_dn = bufs          # to g - 1, to g + 1, from g + 1, from g - 1
+        stream = torch.cuda.ExternalStream(self.params.cuda_stream) if self.params.cuda_stream \
+            else torch.cuda.current_stream()
+        own_stream = not self.params.cuda_stream            # the library made its own stream
+        with torch.cuda.stream(stream):
+            self.halo_pack(-1, send_dn)
+            self.halo_pack(+1, send_up)
+            if own_stream:
+                self.synchronize()
+            halo_transfer(send_dn, send_up, recv_up, recv_dn, g, G, group)
+            if own_stream:
+                stream.synchronize()
+            self.halo_unpack(recv_up, +1)
+            self.halo_unpack(recv_dn, -1)
+
     def launch_count(self) -> int:
         return int(_lib.se2m_launch_count(self.h))
+
+
+def halo_transfer(send_dn, send_up, recv_up, recv_dn, rank: int, world: int, group=None):
+    """The exchange step of the row-band halo (torch.distributed P2P: NCCL on device tensors, gloo on host
+    tensors in the CPU tests): send_dn -> rank - 1, send_up -> rank + 1; recv_up <- rank + 1 (its send_dn),
+    recv_dn <- rank - 1 (its send_up).  With two ranks both neighbours are the same peer: point-to-point
+    messages between a pair match in issue order, and every rank issues (send_dn, recv_up, send_up, recv_dn),
+    so each receive still gets the right slab set.  NCCL waits are stream-ordered (no host sync)."""
+    import torch.distributed as dist
+    lo, hi = (rank - 1) % world, (rank + 1) % world
+    ops = [dist.P2POp(dist.isend, send_dn, lo, group), dist.P2POp(dist.irecv, recv_up, hi, group),
+           dist.P2POp(dist.isend, send_up, hi, group), dist.P2POp(dist.irecv, recv_dn, lo, group)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()

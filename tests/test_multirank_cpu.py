@@ -73,3 +73,74 @@ def test_shard_plan_partitions_and_max_reduce(world):
                 for TJ in range(-7, 40):
                     owners = [r for r, pl in enumerate(ps) if TJ % pl["row_mod"] == pl["row_rank"]]
                     assert len(owners) == 1
+
+
+def _halo_worker(rank, world, port, q):
+    """Each rank holds only its own rows of a random map; slabs are cut by the library's host-only slab
+    plan (se2m_halo_plan), exchanged with se2map.halo_transfer over gloo, and written back by the plan of
+    the sending rank — then every row the rank's tiles read (owned tile rows +- R_T) must be present."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        import torch
+        from paper_2503_02412_b200 import se2map as S
+        checked = 0
+        for nx, ny, r, J_M in ((96, 200, 0.1, 12345), (64, 131, 0.1, -77), (48, 100, 0.05, 3)):
+            p = S.default_params(nx=nx, ny=ny, n_yaw=8, resolution=r, shard_mode=S.SE2M_SHARD_ROWS, rank=rank,
+                                 world_size=world)
+            TY = S.shard_plan(p)["tile_y"]
+            truth = np.random.default_rng(J_M & 0xffff).standard_normal((ny, nx)).astype(np.float32)
+            J = np.arange(J_M, J_M + ny)
+            own = (np.floor_divide(J, TY) % world) == rank
+            local = np.full_like(truth, np.nan)
+            local[own] = truth[own]
+
+            def pack(sender, last):
+                pl = S.halo_plan(p, J_M, sender, last)
+                buf = np.full((pl["cap"], pl["slab_rows"], nx), np.nan, np.float32)
+                for qi, w0 in enumerate(pl["first_rows"]):
+                    for rr in range(pl["slab_rows"]):
+                        if w0 is not None and 0 <= w0 + rr - J_M < ny:
+                            buf[qi, rr] = local[w0 + rr - J_M]
+                return torch.from_numpy(buf)
+
+            def unpack(buf, sender, last):
+                pl = S.halo_plan(p, J_M, sender, last)
+                for qi, w0 in enumerate(pl["first_rows"]):
+                    for rr in range(pl["slab_rows"]):
+                        if w0 is not None and 0 <= w0 + rr - J_M < ny:
+                            local[w0 + rr - J_M] = buf[qi, rr].numpy()
+
+            send_dn, send_up = pack(rank, 0), pack(rank, 1)
+            recv_up, recv_dn = torch.empty_like(send_dn), torch.empty_like(send_up)
+            S.halo_transfer(send_dn, send_up, recv_up, recv_dn, rank, world)
+            unpack(recv_up, (rank + 1) % world, 0)
+            unpack(recv_dn, (rank - 1) % world, 1)
+            R_T = S.halo_plan(p, J_M, rank, 0)["slab_rows"]
+            for TJ in np.unique(np.floor_divide(J, TY)):
+                if TJ % world != rank:
+                    continue
+                j0, j1 = max(0, TJ * TY - R_T - J_M), min(ny, TJ * TY + TY + R_T - J_M)
+                assert np.array_equal(local[j0:j1], truth[j0:j1]), (nx, ny, J_M, TJ)
+                checked += 1
+        q.put((rank, checked))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p_ in procs:
+        p_.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert all(n > 0 for _, n in res)
