@@ -874,6 +874,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 #pragma unroll
     for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
       if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
+    // both rows outside the window (tile rows beyond a window edge): nothing to store, nothing to compute
+    if (!__any_sync(0xffffffffu, so0 >= 0 || so1 >= 0)) continue;
 #pragma unroll 1
     for (int k = kb; k < ke; ++k) {
       const BinC* bk = bins_s + (k - kb);
