@@ -25,6 +25,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "se2m_internal.h"
 
 #ifndef SE2M_UNROLL_PRE
@@ -468,7 +470,10 @@ struct Geom {
   static size_t bytes(int tab_cap, int k_chunk) { return runs_off + (size_t)tab_cap * 16 + (size_t)k_chunk * sizeof(BinC); }
 };
 
-template <int R_T>
+// MODE 0: every tile of the grid (except, with p.tsplit, the vertical-window-edge tiles); MODE 1: only
+// the vertical-window-edge tiles, in the column-major thread layout (T-mode; see below), launched
+// concurrently on a second stream so the two register allocations stay separate.
+template <int R_T, int MODE>
 __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
@@ -486,11 +491,13 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (size_t)p.tab_cap * 16);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tx_rel = (int)(blockIdx.x % (unsigned)p.tiles_x);
+  // MODE 1 runs the tile columns p.tcols[0 .. n_tcols) of every grid row
+  const int gx = MODE == 1 ? p.n_tcols : p.tiles_x;
+  const int tx_rel = MODE == 1 ? p.tcols[blockIdx.x % (unsigned)gx] : (int)(blockIdx.x % (unsigned)gx);
   // grid rows in the order [last, 0, 1, ..., last - 1]: the window's bottom and top tile rows (border
   // tiles: the slower general path) are scheduled in the first wave instead of forming the tail
-  const int n_gr = (int)(gridDim.x / (unsigned)p.tiles_x);
-  int gr = (int)(blockIdx.x / (unsigned)p.tiles_x) - 1;
+  const int n_gr = (int)(gridDim.x / (unsigned)gx);
+  int gr = (int)(blockIdx.x / (unsigned)gx) - 1;
   if (gr < 0) gr = n_gr - 1;
   const int ty_rel = p.row_first + gr * p.row_mod;
   if (p.n_rects) {  // INCREMENTAL: only tiles that hold a state within R of a changed cell (CTA-uniform exit)
@@ -506,6 +513,16 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const int kb = p.k_begin + blockIdx.y * p.k_chunk;
   const int ke = min(kb + p.k_chunk, p.k_end);
   if (kb >= ke) return;
+  // Vertical-window-edge tiles (the halo crosses the window's left or right edge only; they are never
+  // "fast"): in MODE 1, warps own RPW tile COLUMNS each (lane = tile row), so the warps whose column band
+  // (+- R_T) lies inside the window take the interior path, the ones wholly outside the window skip, and
+  // only the band at the edge runs the general path.  Their traversable words are assembled with atomic
+  // ORs from zeroed words.
+  constexpr bool TMODE_OK = G::TY == 32 && TX == 32 && G::CB;
+  const bool tedge = TMODE_OK && (li0 < 0 || li0 + HX > p.nx) && lj0 >= 0 && lj0 + HY <= p.ny;
+  if (MODE == 0 && p.tsplit && tedge) return;
+  if (MODE == 1 && !tedge) return;
+  constexpr bool tmode = MODE == 1 && TMODE_OK;
 
   // ---- 1. halo -> shared memory ----------------------------------------------------------
   const bool box_in = li0 >= 0 && li0 + HX <= p.nx && lj0 >= 0 && lj0 + HY <= p.ny;
@@ -658,6 +675,19 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     }
   }
 
+  // T-mode: zero the tile's traversable words of the chunk (warps OR their bits in)
+  if (tmode) {
+    const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
+    const size_t twplane = (size_t)p.ny * p.trav_words;
+    for (int idx = tid; idx < (ke - kb) * TY; idx += NTHREADS) {
+      const int b = idx / TY, row = idx - b * TY;
+      int py = p.pyM + (int)(lj0 + R_T + row); if (py >= p.ny) py -= p.ny;  // rows are inside the window
+      const size_t w = (size_t)(kb + b) * twplane + (size_t)py * p.trav_words + gword;
+      p.trav[w] = 0u;
+      if (p.paired) p.trav[w + (size_t)p.H * twplane] = 0u;
+    }
+  }
+
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
     float hh[CPL], xp[CPL], vv[CPL];
@@ -717,334 +747,375 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   __syncthreads();
 
   // ---- 4./5. states ------------------------------------------------------------------------
+  // Thread layout: warp w owns the RPW consecutive tile rows row0 .. row0 + RPW - 1, lane = column, state
+  // s = tile row row0 + s (so that on a border tile the warps whose footprints stay clear of the border
+  // take the interior path); T-mode: warp w owns the tile columns tc0 .. tc0 + RPW - 1, lane = row, state
+  // s = column tc0 + s.  State s of a thread sits at tile (trow0 + s drow, tcol0 + s dcol).
   const size_t plane = (size_t)p.nx * p.ny;
-  const float xs = (float)(lane - TX / 2);
+  const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
+  const size_t twplane = (size_t)p.ny * p.trav_words;
+  const int row0 = warp * RPW, tc0 = warp * RPW;
+  const int trow0 = tmode ? lane : row0, tcol0 = tmode ? tc0 : lane;
+  const float xs = (float)(tcol0 - TX / 2);  // x' of state 0 (T-mode: state s at xs + s)
   const long long li = TI * TX + lane - p.I_M;
   const bool col_in = li >= 0 && li < p.nx;
-  int pxs = 0;
-  if (col_in) { pxs = p.pxM + (int)li; if (pxs >= p.nx) pxs -= p.nx; }
   const bool col_any = __any_sync(0xffffffffu, col_in);
-  const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
-  // warp w owns the RPW consecutive tile rows row0 .. row0 + RPW - 1 (state s = tile row row0 + s), so
-  // that on a border tile the warps whose footprints stay clear of the border take the interior path
-  const int row0 = warp * RPW;
   // tile-plane height at state s: zref0 + s * zstep (absolute, metres)
-  const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)row0 - (float)(TY / 2), pc));
-  const float zstep = pgy;
-  // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, column lane)
-  const char* b8 = reinterpret_cast<const char*>(p02) + (size_t)(row0 * PW + lane) * 8;
-  const char* b4 = reinterpret_cast<const char*>(pxh) + (size_t)(row0 * PW + lane) * 4;
-  const char* bv8 = reinterpret_cast<const char*>(pv) + (size_t)(row0 * PW + lane) * 8;
-  const char* bv4 = reinterpret_cast<const char*>(pvxx) + (size_t)(row0 * PW + lane) * 4;
-  const char* bh = reinterpret_cast<const char*>(hh_s) + (size_t)(row0 * PW + lane) * 4;
-  constexpr int RS8 = PW * 8, RS4 = PW * 4;  // state s -> s halo rows lower
+  const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)trow0 - (float)(TY / 2), pc));
+  const float zstep = tmode ? pgx : pgy;
+  // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, halo column = its column)
+  const size_t base = (size_t)trow0 * PW + tcol0;
+  const char* b8 = reinterpret_cast<const char*>(p02) + base * 8;
+  const char* b4 = reinterpret_cast<const char*>(pxh) + base * 4;
+  const char* bv8 = reinterpret_cast<const char*>(pv) + base * 8;
+  const char* bv4 = reinterpret_cast<const char*>(pvxx) + base * 4;
+  const char* bh = reinterpret_cast<const char*>(hh_s) + base * 4;
+  constexpr int RS8 = PW * 8, RS4 = PW * 4;  // state s -> s halo rows lower (T-mode: s columns right)
 
-  // per state s (tile row row0 + s): record index in a bin plane, traversable-word index (-1: the
-  // state's row is outside the window)
-  int tmy = -1;  // interior tiles: lane s < RPW writes the traversable word of state s
+  // per state s: record index in a bin plane (-1: outside the window), traversable-word index
+  int tmy = -1;  // interior tiles: lane s < RPW writes the traversable word of state s; T-mode: lane's row word
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
-    const long long lj = TJ * TY + row0 + s - p.J_M;
-    int py = -1;
+    const int trow = tmode ? lane : row0 + s, tcol = tmode ? tc0 + s : lane;
+    const long long lj = TJ * TY + trow - p.J_M, lis = TI * TX + tcol - p.I_M;
+    int py = -1, px = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
-    soff[s] = (py >= 0 && col_in) ? py * p.nx + pxs : -1;
-    stoff[s] = (py >= 0 && col_any && lane == 0) ? py * p.trav_words + gword : -1;
-    if (lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
+    if (lis >= 0 && lis < p.nx) { px = p.pxM + (int)lis; if (px >= p.nx) px -= p.nx; }
+    soff[s] = (py >= 0 && px >= 0) ? py * p.nx + px : -1;
+    stoff[s] = (!tmode && py >= 0 && col_any && lane == 0) ? py * p.trav_words + gword : -1;
+    if (tmode) tmy = py >= 0 ? py * p.trav_words + gword : -1;
+    else if (lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
   }
 
   // interior tiles: moments carried along the yaw chain, packed across the state pairs (2q, 2q + 1)
   // so that one FFMA2 / FADD2 updates a moment of two states
   F2 S0p[RPW / 2], S2p[RPW / 2], SXp[RPW / 2], SYp[RPW / 2];
   // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
-  const size_t twplane = (size_t)p.ny * p.trav_words;
   float4* outk = p.out + (size_t)kb * plane;
   float4* outk2 = outk + (size_t)p.H * plane;
   uint32_t* travk = p.trav + (size_t)kb * twplane;
   uint32_t* travk2 = travk + (size_t)p.H * twplane;
   // border tile: this warp takes the interior path when every halo row its footprints reach (halo rows
   // row0 .. row0 + RPW - 1 + 2 R_T) is fully known and inside the window (validity row totals)
+  // (T-mode: every halo row's columns tc0 .. tc0 + RPW - 1 + 2 R_T)
   bool wfast = fast;
   if (!fast && G::CB) {
     bool full = true;
-    for (int hr = row0 + lane; hr < row0 + RPW + 2 * R_T; hr += 32) full &= pv[hr * PW + HX].x == (float)HX;
+    if (tmode) {
+      for (int hr = lane; hr < HY; hr += 32)
+        full &= pv[hr * PW + tc0 + RPW + 2 * R_T].x - pv[hr * PW + tc0].x == (float)(RPW + 2 * R_T);
+    } else {
+      for (int hr = row0 + lane; hr < row0 + RPW + 2 * R_T; hr += 32) full &= pv[hr * PW + HX].x == (float)HX;
+    }
     wfast = __all_sync(0xffffffffu, full);
   }
-  if (wfast) {
+  // the interior path, for both thread layouts (T: the T-mode one; compile-time state strides)
+  auto interior = [&](auto tm) {
+    constexpr bool T = decltype(tm)::value;
+    constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
     const BinC* bc_k = bins_s;
     for (int k = kb; k < ke; ++k, ++bc_k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
       const int4 meta = *reinterpret_cast<const int4*>(bc_k);  // (e0, npre, nr, restart)
       const int4* rk = runs_s + meta.x;
       const int nr = meta.z;
       const bool restart = meta.w != 0;
-      // interior tiles lie inside the window (their whole halo does), so every state is stored
+      // interior warps' states all lie inside the window (their whole halo band does), so every one is stored
       auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
         __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
         if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
       };
-      // traversable bits: the warp's 32 lanes are one world-aligned 32-group = one word
-      auto store_trav = [&](int toff, unsigned tmask) {
-        if (toff >= 0) {
-          travk[toff] = tmask;
-          if (p.paired) travk2[toff] = tmask;
-        }
-      };
-      {
-        // ---- interior tile: 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.
-        // At a chain restart the entries are the full rows of bin k, otherwise the corrections from k-1.
-        if (restart) {
-  #pragma unroll
-          for (int q = 0; q < RPW / 2; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
-        }
-        const int npre = meta.y;  // prefix entries first, then cell entries
+      // ---- 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.  At a chain restart
+      // the entries are the full rows of bin k, otherwise the corrections from k-1.
+      if (restart) {
+#pragma unroll
+        for (int q = 0; q < RPW / 2; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
+      }
+      const int npre = meta.y;  // prefix entries first, then cell entries
 #pragma unroll kUnrollPre
-        for (int d = 0; d < npre; ++d) {
-          const int4 o = rk[d];
-          const float dj = __int_as_float(o.w);
-          const char* pa8 = b8 + o.x;
-          const char* pb8 = b8 + o.y;
-          const char* pa4 = b4 + o.z;
-          const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
-  #pragma unroll
-          for (int q = 0; q < RPW / 2; ++q) {
-            const int s = 2 * q;
-            const float2 A0 = *reinterpret_cast<const float2*>(pa8 + s * RS8);
-            const float2 B0 = *reinterpret_cast<const float2*>(pb8 + s * RS8);
-            const float2 A1 = *reinterpret_cast<const float2*>(pa8 + (s + 1) * RS8);
-            const float2 B1 = *reinterpret_cast<const float2*>(pb8 + (s + 1) * RS8);
-            const F2 ax = pk(*reinterpret_cast<const float*>(pa4 + s * RS4),
-                             *reinterpret_cast<const float*>(pa4 + (s + 1) * RS4));
-            const F2 bx = pk(*reinterpret_cast<const float*>(pb4 + s * RS4),
-                             *reinterpret_cast<const float*>(pb4 + (s + 1) * RS4));
-            const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x);  // run sums of h^ of the two states
-            S0p[q] = S0p[q] + d0;
-            S2p[q] = S2p[q] + (pk(B0.y, B1.y) - pk(A0.y, A1.y));
-            SXp[q] = SXp[q] + (bx - ax);  // sum of x' h^ (x' from the tile centre); -xs S0 applied below
-            SYp[q] = fma2(bc(dj), d0, SYp[q]);
-          }
+      for (int d = 0; d < npre; ++d) {
+        const int4 o = rk[d];
+        const float dj = __int_as_float(o.w);
+        const char* pa8 = b8 + o.x;
+        const char* pb8 = b8 + o.y;
+        const char* pa4 = b4 + o.z;
+        const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
+#pragma unroll
+        for (int q = 0; q < RPW / 2; ++q) {
+          const int s = 2 * q;
+          const float2 A0 = *reinterpret_cast<const float2*>(pa8 + s * S8);
+          const float2 B0 = *reinterpret_cast<const float2*>(pb8 + s * S8);
+          const float2 A1 = *reinterpret_cast<const float2*>(pa8 + (s + 1) * S8);
+          const float2 B1 = *reinterpret_cast<const float2*>(pb8 + (s + 1) * S8);
+          const F2 ax = pk(*reinterpret_cast<const float*>(pa4 + s * S4),
+                           *reinterpret_cast<const float*>(pa4 + (s + 1) * S4));
+          const F2 bx = pk(*reinterpret_cast<const float*>(pb4 + s * S4),
+                           *reinterpret_cast<const float*>(pb4 + (s + 1) * S4));
+          const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x);  // run sums of h^ of the two states
+          S0p[q] = S0p[q] + d0;
+          S2p[q] = S2p[q] + (pk(B0.y, B1.y) - pk(A0.y, A1.y));
+          SXp[q] = SXp[q] + (bx - ax);  // sum of x' h^ (x' from the tile centre); -xs S0 applied below
+          SYp[q] = fma2(bc(dj), d0, SYp[q]);
         }
-        // single cells entering / leaving the footprint since bin k-1: one h^ load per state
+      }
+      // single cells entering / leaving the footprint since bin k-1: one h^ load per state
 #pragma unroll kUnrollCell
-        for (int d = npre; d < nr; ++d) {
-          const int4 o = rk[d];
-          const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
-          const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
-          const char* ph = bh + o.x;
-  #pragma unroll
-          for (int q = 0; q < RPW / 2; ++q) {
-            const F2 h = pk(*reinterpret_cast<const float*>(ph + 2 * q * RS4),
-                            *reinterpret_cast<const float*>(ph + (2 * q + 1) * RS4));
-            const F2 sh = bc(sg) * h;
-            S0p[q] = S0p[q] + sh;
-            S2p[q] = fma2(sh, h, S2p[q]);
-            SXp[q] = fma2(bc(cx), h, SXp[q]);
-            SYp[q] = fma2(bc(sdj), h, SYp[q]);
-          }
+      for (int d = npre; d < nr; ++d) {
+        const int4 o = rk[d];
+        const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
+        const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
+        const char* ph = bh + o.x;
+#pragma unroll
+        for (int q = 0; q < RPW / 2; ++q) {
+          const F2 h = pk(*reinterpret_cast<const float*>(ph + 2 * q * S4),
+                          *reinterpret_cast<const float*>(ph + (2 * q + 1) * S4));
+          const F2 sh = bc(sg) * h;
+          // (T-mode: state s sits s columns right of state 0, so its x' is xs + s)
+          const F2 cxq = T ? pk(fmaf(sg, (float)(2 * q), cx), fmaf(sg, (float)(2 * q + 1), cx)) : bc(cx);
+          S0p[q] = S0p[q] + sh;
+          S2p[q] = fma2(sh, h, S2p[q]);
+          SXp[q] = fma2(cxq, h, SXp[q]);
+          SYp[q] = fma2(bc(sdj), h, SYp[q]);
         }
-        const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
-        const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
-        unsigned tmine = 0;
-  #pragma unroll
-        for (int s = 0; s < RPW; s += 2) {
-          const int q = s / 2;
-          const StateOut2 o = arrow2(S0p[q], S2p[q], fma2(bc(-xs), S0p[q], SXp[q]), SYp[q],
-                                     pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
-                                     aG1, aG2, gc, gd, ge, gf, p);
-          store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
-          store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
+      }
+      const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
+      const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
+      unsigned tmine = 0;
+#pragma unroll
+      for (int s = 0; s < RPW; s += 2) {
+        const int q = s / 2;
+        const F2 xsq = T ? pk(xs + (float)s, xs + (float)(s + 1)) : bc(xs);
+        const StateOut2 o = arrow2(S0p[q], S2p[q], fma2(neg2(xsq), S0p[q], SXp[q]), SYp[q],
+                                   pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
+                                   aG1, aG2, gc, gd, ge, gf, p);
+        store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
+        store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
+        if (T) {  // this lane's row: bits tc0 + s, tc0 + s + 1 of its word
+          tmine |= (o.trav_a ? 1u : 0u) << s;
+          tmine |= (o.trav_b ? 1u : 0u) << (s + 1);
+        } else {  // the warp's 32 lanes are one world-aligned 32-group = one word
           const unsigned ma = __ballot_sync(0xffffffffu, o.trav_a);
           const unsigned mb = __ballot_sync(0xffffffffu, o.trav_b);
           if (lane == s) tmine = ma;
           if (lane == s + 1) tmine = mb;
         }
-        store_trav(tmy, tmine);  // lane s writes state s's word
+      }
+      if (tmy >= 0) {
+        if (T) {  // the words were zeroed before the prefix build
+          if (tmine) {
+            atomicOr(travk + tmy, tmine << tc0);
+            if (p.paired) atomicOr(travk2 + tmy, tmine << tc0);
+          }
+        } else {  // lane s writes state s's word
+          travk[tmy] = tmine;
+          if (p.paired) travk2[tmy] = tmine;
+        }
       }
     }
+  };
+  if (wfast) {
+    interior(std::integral_constant<bool, tmode>{});
     return;
   }
   // ---- border / unknown tile: two states at a time along the whole yaw chunk; per state also the validity
   // moments (N, sum di, sum dj, sum di^2, sum di dj, sum dj^2), all carried along the yaw chain like the
   // interior moments (prefix entries with validity prefixes, then single cells: h^ or NaN = unknown)
-#pragma unroll 1
-  for (int sp = 0; sp < RPW; sp += 2) {
-    // accumulators packed across the state pair (lo = state sp, hi = state sp + 1): one FFMA2 per moment
-    F2 S0g, S2g, SXHg, SYHg, Nv, Sxv, Syv, Sxxv, Sxyv, Syyv;
-    const int so8 = sp * RS8, so4 = sp * RS4;
-    int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
-#pragma unroll
-    for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
-      if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
-    // both rows outside the window (tile rows beyond a window edge): nothing to store, nothing to compute
-    if (!__any_sync(0xffffffffu, so0 >= 0 || so1 >= 0)) continue;
-#pragma unroll 1
-    for (int k = kb; k < ke; ++k) {
-      const BinC* bk = bins_s + (k - kb);
-      const int4 meta = *reinterpret_cast<const int4*>(&bk->e0);
-      const int4 metaf = *reinterpret_cast<const int4*>(&bk->f0);
-      const int4* rkf = runs_s + metaf.x;
-      const int nf = metaf.y;
-      // the yaw chain, or (R_T = 32) the full rows of every bin as prefix entries
-      const int4* rk = G::CB ? runs_s + meta.x : rkf;
-      const int nr = G::CB ? meta.z : nf;
-      const int npre = G::CB ? meta.y : nf;
-      const float2 csk = make_float2(bk->cs.x, bk->cs.y);
-      const bool restart = meta.w != 0 || !G::CB;
-      if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
-#pragma unroll 1
-      for (int d = 0; d < npre; ++d) {
-        const int4 o = rk[d];
-        const float dj = __int_as_float(o.w);
-        const int ob4 = o.z + ((o.y - o.x) >> 1);
-        const float2 A0 = *reinterpret_cast<const float2*>(b8 + so8 + o.x);
-        const float2 B0 = *reinterpret_cast<const float2*>(b8 + so8 + o.y);
-        const float2 A1 = *reinterpret_cast<const float2*>(b8 + so8 + o.x + RS8);
-        const float2 B1 = *reinterpret_cast<const float2*>(b8 + so8 + o.y + RS8);
-        const F2 ax = pk(*reinterpret_cast<const float*>(b4 + so4 + o.z),
-                         *reinterpret_cast<const float*>(b4 + so4 + o.z + RS4));
-        const F2 bx = pk(*reinterpret_cast<const float*>(b4 + so4 + ob4),
-                         *reinterpret_cast<const float*>(b4 + so4 + ob4 + RS4));
-        const float2 VA0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x);
-        const float2 VB0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y);
-        const float2 VA1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + RS8);
-        const float2 VB1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + RS8);
-        const F2 wa = pk(*reinterpret_cast<const float*>(bv4 + so4 + o.z),
-                         *reinterpret_cast<const float*>(bv4 + so4 + o.z + RS4));
-        const F2 wb = pk(*reinterpret_cast<const float*>(bv4 + so4 + ob4),
-                         *reinterpret_cast<const float*>(bv4 + so4 + ob4 + RS4));
-        const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x), d2 = pk(B0.y, B1.y) - pk(A0.y, A1.y);
-        const F2 cnt = pk(VB0.x, VB1.x) - pk(VA0.x, VA1.x), sxv = pk(VB0.y, VB1.y) - pk(VA0.y, VA1.y);
-        const F2 sxxv = wb - wa;                                  // exact integers
-        const F2 sdi = fma2(bc(-xs), cnt, sxv);                   // sum di over the run
-        S0g = S0g + d0;
-        S2g = S2g + d2;
-        SXHg = SXHg + fma2(bc(-xs), d0, bx - ax);
-        SYHg = fma2(bc(dj), d0, SYHg);
-        Nv = Nv + cnt;
-        Sxv = Sxv + sdi;
-        Sxxv = Sxxv + fma2(bc(xs * xs), cnt, fma2(bc(-2.f * xs), sxv, sxxv));
-        Syv = fma2(bc(dj), cnt, Syv);
-        Syyv = fma2(bc(dj * dj), cnt, Syyv);
-        Sxyv = fma2(bc(dj), sdi, Sxyv);
-      }
-#pragma unroll 1
-      for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
-        const int4 o = rk[d];
-        const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
-        const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
-        const float h0 = *reinterpret_cast<const float*>(bh + so4 + o.x);
-        const float h1 = *reinterpret_cast<const float*>(bh + so4 + o.x + RS4);
-        const bool k0 = !isnan(h0), k1 = !isnan(h1);
-        const F2 v = pk(k0 ? 1.f : 0.f, k1 ? 1.f : 0.f), hv = pk(k0 ? h0 : 0.f, k1 ? h1 : 0.f);
-        const F2 sh = bc(sg) * hv;
-        S0g = S0g + sh;
-        S2g = fma2(sh, hv, S2g);
-        SXHg = fma2(bc(sdi), hv, SXHg);
-        SYHg = fma2(bc(sdj), hv, SYHg);
-        Nv = fma2(bc(sg), v, Nv);
-        Sxv = fma2(bc(sdi), v, Sxv);
-        Syv = fma2(bc(sdj), v, Syv);
-        Sxxv = fma2(bc(cxx), v, Sxxv);
-        Sxyv = fma2(bc(cxy), v, Sxyv);
-        Syyv = fma2(bc(cyy), v, Syyv);
-      }
-      float4* outk = p.out + (size_t)k * plane;
-      float4* outk2 = p.out + (size_t)(k + p.H) * plane;
-      uint32_t* travk = p.trav + (size_t)k * twplane;
-      uint32_t* travk2 = p.trav + (size_t)(k + p.H) * twplane;
-      auto store = [&](int off, int toff, float risk, float pitch, float roll, float z, unsigned trav) {
-        if (off >= 0) {
-          __stcs(outk + off, make_float4(risk, pitch, roll, z));
-          if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
-        }
-        const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
-        if (lane == 0 && toff >= 0) {
-          travk[toff] = tmask;
-          if (p.paired) travk2[toff] = tmask;
-        }
-      };
-          const float N[2] = {lo(Nv), hi(Nv)}, Sx[2] = {lo(Sxv), hi(Sxv)}, Sy[2] = {lo(Syv), hi(Syv)};
-          const float Sxx[2] = {lo(Sxxv), hi(Sxxv)}, Sxy[2] = {lo(Sxyv), hi(Sxyv)}, Syy[2] = {lo(Syyv), hi(Syyv)};
-          const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
-          const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
-          Cov2 cv = cov_general(Nv, Sxv, Syv, shl, shh, S0g, S2g, SXHg, SYHg,
-                                pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
-          // (states outside the window are not stored: they never take the direct path)
-          const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
-          const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
-          StateOut1 dres[2];
-          if (need0 | need1) {
-            // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
-            // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
-            const float m0[2] = {lo(cv.zz), hi(cv.zz)};
-            float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
-  #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              unsigned msk = s ? need1 : need0;
-              while (msk) {
-                const int src = __ffs(msk) - 1;
-                msk &= msk - 1;
-                const float mu = __shfl_sync(0xffffffffu, m0[s], src);
-                const float* rb = raw + (row0 + sp + s) * HX + src;  // state's halo row, column src
-                float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
+  auto border = [&](auto tm) {
+    constexpr bool T = decltype(tm)::value;
+    constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
   #pragma unroll 1
-                for (int d = 0; d < nf; ++d) {
-                  const int4 o = rkf[d];
-                  const float dj = __int_as_float(o.w);
-                  const int dr = (int)dj + R_T;  // stencil row -> halo row offset
-                  const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
-                  for (int c = c0 + lane; c < c1; c += 32) {
-                    const float hv = rb[dr * HX + c];
-                    if (!isnan(hv)) {
-                      const float dv = hv - mu;
-                      a0 += dv;
-                      a2 = fmaf(dv, dv, a2);
-                      ax = fmaf((float)(c - R_T), dv, ax);
-                      ay = fmaf(dj, dv, ay);
+    for (int sp = 0; sp < RPW; sp += 2) {
+      // accumulators packed across the state pair (lo = state sp, hi = state sp + 1): one FFMA2 per moment
+      F2 S0g, S2g, SXHg, SYHg, Nv, Sxv, Syv, Sxxv, Sxyv, Syyv;
+      const int so8 = sp * S8, so4 = sp * S4;
+      // x' of the pair's states (from the tile centre): T-mode columns xs + sp, xs + sp + 1
+      const F2 xsp = T ? pk(xs + (float)sp, xs + (float)(sp + 1)) : bc(xs);
+      const F2 xsp2 = T ? xsp * xsp : bc(xs * xs), xspm2 = T ? bc(-2.f) * xsp : bc(-2.f * xs);
+      int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
+  #pragma unroll
+      for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
+        if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
+      // both rows outside the window (tile rows beyond a window edge): nothing to store, nothing to compute
+      if (!__any_sync(0xffffffffu, so0 >= 0 || so1 >= 0)) continue;
+  #pragma unroll 1
+      for (int k = kb; k < ke; ++k) {
+        const BinC* bk = bins_s + (k - kb);
+        const int4 meta = *reinterpret_cast<const int4*>(&bk->e0);
+        const int4 metaf = *reinterpret_cast<const int4*>(&bk->f0);
+        const int4* rkf = runs_s + metaf.x;
+        const int nf = metaf.y;
+        // the yaw chain, or (R_T = 32) the full rows of every bin as prefix entries
+        const int4* rk = G::CB ? runs_s + meta.x : rkf;
+        const int nr = G::CB ? meta.z : nf;
+        const int npre = G::CB ? meta.y : nf;
+        const float2 csk = make_float2(bk->cs.x, bk->cs.y);
+        const bool restart = meta.w != 0 || !G::CB;
+        if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
+  #pragma unroll 1
+        for (int d = 0; d < npre; ++d) {
+          const int4 o = rk[d];
+          const float dj = __int_as_float(o.w);
+          const int ob4 = o.z + ((o.y - o.x) >> 1);
+          const float2 A0 = *reinterpret_cast<const float2*>(b8 + so8 + o.x);
+          const float2 B0 = *reinterpret_cast<const float2*>(b8 + so8 + o.y);
+          const float2 A1 = *reinterpret_cast<const float2*>(b8 + so8 + o.x + S8);
+          const float2 B1 = *reinterpret_cast<const float2*>(b8 + so8 + o.y + S8);
+          const F2 ax = pk(*reinterpret_cast<const float*>(b4 + so4 + o.z),
+                           *reinterpret_cast<const float*>(b4 + so4 + o.z + S4));
+          const F2 bx = pk(*reinterpret_cast<const float*>(b4 + so4 + ob4),
+                           *reinterpret_cast<const float*>(b4 + so4 + ob4 + S4));
+          const float2 VA0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x);
+          const float2 VB0 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y);
+          const float2 VA1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.x + S8);
+          const float2 VB1 = *reinterpret_cast<const float2*>(bv8 + so8 + o.y + S8);
+          const F2 wa = pk(*reinterpret_cast<const float*>(bv4 + so4 + o.z),
+                           *reinterpret_cast<const float*>(bv4 + so4 + o.z + S4));
+          const F2 wb = pk(*reinterpret_cast<const float*>(bv4 + so4 + ob4),
+                           *reinterpret_cast<const float*>(bv4 + so4 + ob4 + S4));
+          const F2 d0 = pk(B0.x, B1.x) - pk(A0.x, A1.x), d2 = pk(B0.y, B1.y) - pk(A0.y, A1.y);
+          const F2 cnt = pk(VB0.x, VB1.x) - pk(VA0.x, VA1.x), sxv = pk(VB0.y, VB1.y) - pk(VA0.y, VA1.y);
+          const F2 sxxv = wb - wa;                                  // exact integers
+          const F2 sdi = fma2(neg2(xsp), cnt, sxv);                 // sum di over the run
+          S0g = S0g + d0;
+          S2g = S2g + d2;
+          SXHg = SXHg + fma2(neg2(xsp), d0, bx - ax);
+          SYHg = fma2(bc(dj), d0, SYHg);
+          Nv = Nv + cnt;
+          Sxv = Sxv + sdi;
+          Sxxv = Sxxv + fma2(xsp2, cnt, fma2(xspm2, sxv, sxxv));
+          Syv = fma2(bc(dj), cnt, Syv);
+          Syyv = fma2(bc(dj * dj), cnt, Syyv);
+          Sxyv = fma2(bc(dj), sdi, Sxyv);
+        }
+  #pragma unroll 1
+        for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
+          const int4 o = rk[d];
+          const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
+          const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
+          const float h0 = *reinterpret_cast<const float*>(bh + so4 + o.x);
+          const float h1 = *reinterpret_cast<const float*>(bh + so4 + o.x + S4);
+          const bool k0 = !isnan(h0), k1 = !isnan(h1);
+          const F2 v = pk(k0 ? 1.f : 0.f, k1 ? 1.f : 0.f), hv = pk(k0 ? h0 : 0.f, k1 ? h1 : 0.f);
+          const F2 sh = bc(sg) * hv;
+          S0g = S0g + sh;
+          S2g = fma2(sh, hv, S2g);
+          SXHg = fma2(bc(sdi), hv, SXHg);
+          SYHg = fma2(bc(sdj), hv, SYHg);
+          Nv = fma2(bc(sg), v, Nv);
+          Sxv = fma2(bc(sdi), v, Sxv);
+          Syv = fma2(bc(sdj), v, Syv);
+          Sxxv = fma2(bc(cxx), v, Sxxv);
+          Sxyv = fma2(bc(cxy), v, Sxyv);
+          Syyv = fma2(bc(cyy), v, Syyv);
+        }
+        float4* outk = p.out + (size_t)k * plane;
+        float4* outk2 = p.out + (size_t)(k + p.H) * plane;
+        uint32_t* travk = p.trav + (size_t)k * twplane;
+        uint32_t* travk2 = p.trav + (size_t)(k + p.H) * twplane;
+        auto store = [&](int off, int toff, int bit, float risk, float pitch, float roll, float z, unsigned trav) {
+          if (off >= 0) {
+            __stcs(outk + off, make_float4(risk, pitch, roll, z));
+            if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
+          }
+          if (T) {  // T-mode: bit `bit` of this lane's row word (zeroed before the prefix build)
+            if (off >= 0 && trav && tmy >= 0) {
+              atomicOr(travk + tmy, 1u << bit);
+              if (p.paired) atomicOr(travk2 + tmy, 1u << bit);
+            }
+            return;
+          }
+          const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
+          if (lane == 0 && toff >= 0) {
+            travk[toff] = tmask;
+            if (p.paired) travk2[toff] = tmask;
+          }
+        };
+            const float N[2] = {lo(Nv), hi(Nv)}, Sx[2] = {lo(Sxv), hi(Sxv)}, Sy[2] = {lo(Syv), hi(Syv)};
+            const float Sxx[2] = {lo(Sxxv), hi(Sxxv)}, Sxy[2] = {lo(Sxyv), hi(Sxyv)}, Syy[2] = {lo(Syyv), hi(Syyv)};
+            const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
+            const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
+            Cov2 cv = cov_general(Nv, Sxv, Syv, shl, shh, S0g, S2g, SXHg, SYHg,
+                                  pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
+            // (states outside the window are not stored: they never take the direct path)
+            const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
+            const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
+            StateOut1 dres[2];
+            if (need0 | need1) {
+              // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
+              // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
+              const float m0[2] = {lo(cv.zz), hi(cv.zz)};
+              float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
+    #pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                unsigned msk = s ? need1 : need0;
+                while (msk) {
+                  const int src = __ffs(msk) - 1;
+                  msk &= msk - 1;
+                  const float mu = __shfl_sync(0xffffffffu, m0[s], src);
+                  // the state's top-left footprint-box cell: halo (row, column) = its tile (row, column)
+                  const float* rb = T ? raw + src * HX + tc0 + sp + s : raw + (row0 + sp + s) * HX + src;
+                  float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
+    #pragma unroll 1
+                  for (int d = 0; d < nf; ++d) {
+                    const int4 o = rkf[d];
+                    const float dj = __int_as_float(o.w);
+                    const int dr = (int)dj + R_T;  // stencil row -> halo row offset
+                    const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
+                    for (int c = c0 + lane; c < c1; c += 32) {
+                      const float hv = rb[dr * HX + c];
+                      if (!isnan(hv)) {
+                        const float dv = hv - mu;
+                        a0 += dv;
+                        a2 = fmaf(dv, dv, a2);
+                        ax = fmaf((float)(c - R_T), dv, ax);
+                        ay = fmaf(dj, dv, ay);
+                      }
                     }
                   }
+    #pragma unroll
+                  for (int w = 16; w >= 1; w >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, w);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, w);
+                    ax += __shfl_xor_sync(0xffffffffu, ax, w);
+                    ay += __shfl_xor_sync(0xffffffffu, ay, w);
+                  }
+                  if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
                 }
-  #pragma unroll
-                for (int w = 16; w >= 1; w >>= 1) {
-                  a0 += __shfl_xor_sync(0xffffffffu, a0, w);
-                  a2 += __shfl_xor_sync(0xffffffffu, a2, w);
-                  ax += __shfl_xor_sync(0xffffffffu, ax, w);
-                  ay += __shfl_xor_sync(0xffffffffu, ay, w);
+              }
+              // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
+    #pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                if (s ? dh : dl) {
+                  const double dN = N[s], iN = 1.0 / dN, r = p.r;
+                  const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
+                  const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
+                               c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
+                  const double r2n = r * r * iN * iN;
+                  dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
+                                        r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
+                                        (double)m0[s] + md, csk,
+                                        make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
+                                        make_float3(p.wk, p.wx, p.wy));
                 }
-                if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
               }
             }
-            // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
-  #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              if (s ? dh : dl) {
-                const double dN = N[s], iN = 1.0 / dN, r = p.r;
-                const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
-                const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
-                             c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
-                const double r2n = r * r * iN * iN;
-                dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
-                                      r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
-                                      (double)m0[s] + md, csk,
-                                      make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
-                                      make_float3(p.wk, p.wx, p.wy));
-              }
-            }
-          }
-          const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
-                                           shh.ok, 0.f, 0.f, csk, p);
-          // (store() holds a warp ballot: select first, store uniformly)
-          StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
-          StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
-          if (dl) ra = dres[0];
-          if (dh) rb = dres[1];
-          store(so0, st0, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
-          store(so1, st1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
+            const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
+                                             shh.ok, 0.f, 0.f, csk, p);
+            // (store() holds a warp ballot: select first, store uniformly)
+            StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
+            StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
+            if (dl) ra = dres[0];
+            if (dh) rb = dres[1];
+            store(so0, st0, tc0 + sp, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
+            store(so1, st1, tc0 + sp + 1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
+      }
     }
-  }
+  };
+  border(std::integral_constant<bool, tmode>{});
 }
 
-template <int R_T>
-static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {
+template <int R_T, int MODE>
+static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensorMap* tmap, cudaStream_t stream) {
   using G = Geom<R_T>;
   const size_t smem = G::bytes(p.tab_cap, p.k_chunk);
   // the attribute is per device: remember the configured size per device ordinal
@@ -1053,7 +1124,7 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
   cudaGetDevice(&dev);
   int& configured_bytes = configured[dev & 63];
   if ((int)smem > configured_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(assess_kernel<R_T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(assess_kernel<R_T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       cudaGetLastError();  // not sticky: leave no stale error for the next call
       return e;
@@ -1061,9 +1132,31 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
     configured_bytes = (int)smem;
   }
   const int nk = p.k_end - p.k_begin;
-  dim3 grid(n_tiles, (nk + p.k_chunk - 1) / p.k_chunk);
-  assess_kernel<R_T><<<grid, NTHREADS, smem, stream>>>(p, *tmap);
+  dim3 grid(grid_x, (nk + p.k_chunk - 1) / p.k_chunk);
+  assess_kernel<R_T, MODE><<<grid, NTHREADS, smem, stream>>>(p, *tmap);
   return cudaGetLastError();
+}
+
+// MODE 1 (edge stream) first, so its CTAs are scheduled early, then MODE 0 on the map's stream
+template <int R_T>
+static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream,
+                            cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+  cudaError_t e;
+  const int grid_rows = n_tiles / p.tiles_x;
+  *n_launch = 0;
+  if (p.tsplit) {
+    if ((e = cudaEventRecord(fork, stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(edge, fork, 0)) != cudaSuccess) return e;
+    if ((e = launch_mode<R_T, 1>(p, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
+    ++*n_launch;
+  }
+  if ((e = launch_mode<R_T, 0>(p, n_tiles, tmap, stream)) != cudaSuccess) return e;
+  ++*n_launch;
+  if (p.tsplit) {
+    if ((e = cudaEventRecord(join, edge)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(stream, join, 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
@@ -1078,15 +1171,17 @@ size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
   }
 }
 
-cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream) {
+cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream,
+                          cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+  *n_launch = 0;
   if (n_tiles <= 0 || p.k_end <= p.k_begin) return cudaSuccess;
   switch (R_T) {
-    case 4: return launch_t<4>(p, n_tiles, tmap, stream);
-    case 8: return launch_t<8>(p, n_tiles, tmap, stream);
-    case 12: return launch_t<12>(p, n_tiles, tmap, stream);
-    case 16: return launch_t<16>(p, n_tiles, tmap, stream);
-    case 24: return launch_t<24>(p, n_tiles, tmap, stream);
-    case 32: return launch_t<32>(p, n_tiles, tmap, stream);
+    case 4: return launch_t<4>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 8: return launch_t<8>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 12: return launch_t<12>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 16: return launch_t<16>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 24: return launch_t<24>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 32: return launch_t<32>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -78,6 +78,10 @@ struct AssessParams {
   int4 rects[kMaxRects];
   int k_begin, k_end;    // representative-bin range this launch covers
   int k_chunk;           // rep bins per CTA (grid.y = ceil((k_end-k_begin)/k_chunk))
+  // vertical-window-edge tiles (tile columns tcols[0 .. n_tcols) of the launch) run in a second kernel,
+  // assess_kernel<R_T, 1>, on the edge stream (tsplit = 1); the main launch skips them
+  int tsplit, n_tcols;
+  int tcols[4];
   int use_tma;           // tensor map valid
   int force_general;     // some full stencil is degenerate (< 3 cells or collinear): no interior fast path
 };
@@ -85,8 +89,11 @@ struct AssessParams {
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.
 // dynamic shared memory of one assess CTA (halo, prefix planes, h^ plane, run tables of tab_cap entries)
 size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk);
+// With p.tsplit the edge-tile kernel runs on `edge` (forked from / joined into `stream` with the two
+// events); *n_launch = kernels launched.
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
-                          cudaStream_t stream);
+                          cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join,
+                          int* n_launch);
 
 // Small helpers (same file as the kernels).
 // se2m_step: the window cells that entered (up to 2 logical rectangles (i0, j0, w, h)) from a device

@@ -15,6 +15,10 @@
 #include "../../include/se2map.h"
 #include "se2m_internal.h"
 
+#ifndef SE2M_TSPLIT
+#define SE2M_TSPLIT 1        // vertical-window-edge tiles in their own concurrent kernel (A/B knob)
+#endif
+
 using namespace se2m;
 
 namespace {
@@ -85,6 +89,9 @@ struct se2m_map {
   bool inpaint_valid = false;
   // se2m_download_compact_rep: copy stream, double-buffered staging, events (created on first use)
   cudaStream_t copy_stream = nullptr;
+  // assess: the vertical-window-edge tiles' kernel runs on this stream, forked from / joined into `stream`
+  cudaStream_t edge_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_gathered[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   char* d_rep[2] = {nullptr, nullptr};
   size_t rep_bytes = 0;
@@ -548,6 +555,12 @@ extern "C" void se2m_destroy(se2m_map* m) {
     if (m->ev_gathered[b]) cudaEventDestroy(m->ev_gathered[b]);
     if (m->ev_copied[b]) cudaEventDestroy(m->ev_copied[b]);
   }
+  if (m->edge_stream) {
+    cudaStreamSynchronize(m->edge_stream);
+    cudaStreamDestroy(m->edge_stream);
+  }
+  if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  if (m->ev_join) cudaEventDestroy(m->ev_join);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -800,10 +813,34 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
     return fail(m, SE2M_ERR_UNSUPPORTED, "assess: footprint tables exceed the shared memory of a CTA");
   p.k_chunk = chunk;
   p.tab_cap = cap;
+  // vertical-window-edge tile columns (the halo crosses the window's left / right edge): their tiles run
+  // in the column-major layout kernel on the edge stream, concurrently (tile_rows == 32 footprints only)
+  p.tsplit = 0; p.n_tcols = 0;
+  if (tile_rows(m->R_T) == 32 && chain_border(m->R_T) && SE2M_TSPLIT) {
+    const int HX = TX + 2 * m->R_T;
+    for (int tx = 0; tx < p.tiles_x; ++tx) {
+      const long long li0 = (p.TI0 + tx) * TX - m->R_T - m->I_M;
+      if (li0 < 0 || li0 + HX > nx) {
+        if (p.n_tcols == 4) { p.n_tcols = -1; break; }
+        p.tcols[p.n_tcols++] = tx;
+      }
+    }
+    if (p.n_tcols > 0) {
+      if (!m->edge_stream) {
+        CUDA_TRY(m, cudaStreamCreateWithFlags(&m->edge_stream, cudaStreamNonBlocking), "cudaStreamCreate(edge)");
+        CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+        CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+      }
+      p.tsplit = 1;
+    } else {
+      p.n_tcols = 0;
+    }
+  }
   if (n_tiles > 0 && nk > 0) {
-    cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream);
+    int nl = 0;
+    cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
-    m->launches++;
+    m->launches += nl;
   }
   m->dirty.clear();
   m->all_dirty = false;
