@@ -50,10 +50,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--queries", type=int, default=4096)
-    ap.add_argument("--shard", default="maps", choices=["maps", "rows"],
+    ap.add_argument("--shard", default="maps", choices=["maps", "rows", "yaw"],
                     help="N > 1: 'maps' = one independent map per GPU (weak scaling, default); 'rows' = ONE map "
                          "split into interleaved tile-row bands, each rank fed only its own rows, halo rows "
-                         "exchanged by NCCL send/recv every step (strong scaling, SURVEY.md §8(e))")
+                         "exchanged by NCCL send/recv every step; 'yaw' = ONE map, every rank fed the whole "
+                         "window, each assessing its slice of yaw bins (both strong scaling, SURVEY.md §8(e))")
     return ap.parse_args()
 
 
@@ -249,7 +250,9 @@ def main():
     # SURVEY.md §8(e) "batches of maps"); rank g's robot drives the same path 1 km further east.
     # --shard rows: one map, every rank on the same path, row bands + NCCL halo exchange (strong scaling)
     rows_mode = args.shard == "rows" and world > 1
-    off_x = 0.0 if rows_mode else 1000.0 * rank
+    yaw_mode = args.shard == "yaw" and world > 1
+    one_map = rows_mode or yaw_mode
+    off_x = 0.0 if one_map else 1000.0 * rank
     positions = [(x + off_x, y) for (x, y) in positions]
     robot0 = (cfg["robot"][0] + off_x, cfg["robot"][1])
 
@@ -264,7 +267,8 @@ def main():
     world_d = torch.from_numpy(world_h).to(dev)
     world_pinned = torch.from_numpy(world_h).pin_memory()
 
-    shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS, rank=rank, world_size=world) if rows_mode else {}
+    shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS if rows_mode else S.SE2M_SHARD_YAW, rank=rank,
+                    world_size=world) if one_map else {}
     m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
                  robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream, **shard_kw)
     rng = np.random.default_rng(1)
@@ -340,8 +344,11 @@ def main():
     tot_s = sum(step_ms) / 1e3
     kern_s = sum(kern_ms) / 1e3
     tot_s, kern_s = max_over_ranks([tot_s, kern_s], world, dev)
-    n_jobs = 1 if rows_mode else world             # maps assessed per step (rows: one map split in bands)
+    n_jobs = 1 if one_map else world               # maps assessed per step (rows / yaw: one map split)
     own_states = len(m.owned_rows()) * nx * n_yaw  # this rank's states of the last window
+    if yaw_mode:
+        pl = S.shard_plan(m.params)
+        own_states = (pl["k_hi"] - pl["k_lo"]) * (2 if n_yaw % 2 == 0 else 1) * nx * ny
     value = n_jobs * n_states * K / tot_s          # all ranks' states / the slowest rank's time
 
     # ---- e2e: public API with host buffers (H2D of the step's map from pinned memory, D2H of the
@@ -403,7 +410,7 @@ def main():
     alu_peak = n_sm * 128 * sm_max * 1e6 / 1e12      # FP32-pipe lane-ops/s (FMA = 1 op), Tops/s
     Pk = stencil_cells(cfg)
     W_state = 4 * Pk + 200                           # SURVEY.md §8(d) algorithmic ops per state
-    states_per_launch = own_states if rows_mode else n_states   # per rank
+    states_per_launch = own_states if one_map else n_states   # per rank
     t_kernel = kern_s / K                            # per launch (update scatter included: < 1%)
     achieved = states_per_launch * W_state / t_kernel / 1e12
     bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
@@ -455,15 +462,16 @@ def main():
         extras.update(highres_update(S, stream, torch))
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong" if rows_mode else "weak",
+            "ms_per_step": tot_s / K * 1e3, "higher_is_better": True, "scaling": "strong" if one_map else "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: T_hills seed 5 (sinusoid hills, slope_rms 0.5, rocks, 1 cm noise; SURVEY.md §8(d)); "
                     "no weights",
             "config": {"workload": args.config, "nx": nx, "ny": ny, "n_yaw": n_yaw, "resolution_m": r,
                        "footprint_m": [cfg["ex"], cfg["ey"]], "states_per_step": n_jobs * n_states,
-                       "states_per_gpu_per_step": own_states if rows_mode else n_states,
+                       "states_per_gpu_per_step": own_states if one_map else n_states,
                        "parallelism": ("rows%d (one map, interleaved tile-row bands, NCCL halo exchange)" % world
-                                       if rows_mode else "batch%d (one independent map per GPU)" % world)
+                                       if rows_mode else "yaw%d (one map, yaw slices, replicated input)" % world
+                                       if yaw_mode else "batch%d (one independent map per GPU)" % world)
                                       if world > 1 else "single",
                        "l2": "256 MB buffer written between timed steps (outside the step events); "
                              "each step also writes %.2f GB of outputs" % (n_states * 16.125 / 1e9),

@@ -264,6 +264,12 @@ se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
 /* Number of footprint cells |P_k| for yaw bin k (0 <= k < n_yaw) and the stencil radius R. */
 se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, int32_t* radius);
 
+/* Yaw-chain restart period of the map: moments are carried from bin k-1 to bin k and
+ * recomputed from whole footprint rows at bins k = 0 (mod period); 1 = no chain (small maps).  A state's
+ * FP32 rounding depends on it, so yaw-sharded maps equal the unsharded one bit for bit exactly when both
+ * use the same period (the shard plan keeps the unsharded period unless a rank would get no bins). */
+se2m_status se2m_chain_period(const se2m_map* m, int32_t* period);
+
 /* World-aligned tile of states one CTA assesses: TX columns x TY rows (SE2M_SHARD_ROWS gives world
  * tile row TJ = floor(J / TY) to rank TJ mod world_size). */
 se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_t* tile_y);

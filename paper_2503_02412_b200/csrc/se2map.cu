@@ -15,6 +15,9 @@
 #include "../../include/se2map.h"
 #include "se2m_internal.h"
 
+#ifndef SE2M_PERIOD
+#define SE2M_PERIOD 18       // yaw-chain restart period on large maps (A/B knob; 9 and 12 measured slower)
+#endif
 #ifndef SE2M_TSPLIT
 #define SE2M_TSPLIT 1        // vertical-window-edge tiles in their own concurrent kernel (A/B knob)
 #endif
@@ -360,6 +363,51 @@ static se2m_status validate(const se2m_params* p) {
   return SE2M_OK;
 }
 
+// Yaw-chain restart period: on maps big enough that every CTA takes all its bins, the
+// moments are carried along the bins and restart every SE2M_PERIOD bins; small maps split the bins across
+// CTAs instead (period 1).  Yaw slices shard whole periods; when that would leave a rank without bins
+// (fewer periods than ranks) the period (<= SE2M_PERIOD) is the one that minimises the largest rank's
+// bin count, ties to the longer period (H = 36, G = 8 -> 5).  Otherwise the single-GPU period is kept, so
+// yaw-sharded results stay bit-identical to the unsharded map's.
+static int chain_period(int H, long long cells, int G) {
+  if (H < 18 || cells < 512LL * 512LL) return 1;
+  if (G <= 1 || (H + SE2M_PERIOD - 1) / SE2M_PERIOD >= G) return SE2M_PERIOD;
+  int best = 1, best_max = INT_MAX;
+  for (int q = 1; q <= SE2M_PERIOD; ++q) {
+    const long long nper = (H + q - 1) / q;
+    int mx = 0;
+    for (int g = 0; g < G; ++g) {
+      const int lo = (int)std::min<long long>(H, q * (nper * g / G)), hi = (int)std::min<long long>(H, q * (nper * (g + 1) / G));
+      mx = std::max(mx, hi - lo);
+    }
+    if (mx <= best_max) { best = q; best_max = mx; }
+  }
+  return best;
+}
+
+// The chain tables of one period must fit a CTA's shared memory next to the tile planes (the launch
+// splits the bins of a CTA only at period boundaries): large footprints fall back to shorter periods.
+// Decided against the B200 opt-in limit (227 KB) so that the host-only shard plan agrees with init.
+constexpr size_t kSmemOptinB200 = 227 * 1024;
+static void tables_for_period(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows, int P,
+                              std::vector<int4>& full, std::vector<int4>& chain) {
+  for (;;) {
+    m->period = P;
+    full.clear();
+    chain.clear();
+    build_tables(m, runs, nrows, full, chain);
+    if (P <= 1) return;
+    int cap = 1;
+    for (int kb = 0; kb < m->H; kb += P) {
+      const int ke = std::min(kb + P, m->H);
+      const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
+      cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
+    }
+    if (assess_smem_bytes(m->R_T, cap, P) <= kSmemOptinB200) return;
+    P = P > 9 ? 9 : P - 1;
+  }
+}
+
 extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int32_t* k_lo, int32_t* k_hi,
                                        int32_t* tile_y, int32_t* row_mod, int32_t* row_rank) {
   se2m_status st = validate(p);
@@ -376,7 +424,10 @@ extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int
   const bool yaw = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
   const bool rows = p->shard_mode == SE2M_SHARD_ROWS && p->world_size > 1;
   if (n_rep) *n_rep = m.H;
-  const int period = (m.H >= 18 && (long long)p->nx * p->ny >= 512LL * 512LL) ? 9 : 1;
+  std::vector<int4> full, chain;
+  tables_for_period(&m, runs, nrows, chain_period(m.H, (long long)p->nx * p->ny, yaw ? p->world_size : 1), full,
+                    chain);
+  const int period = m.period;
   const int nper = (m.H + period - 1) / period;
   if (k_lo) *k_lo = yaw ? std::min(m.H, period * (int32_t)((long long)nper * p->rank / p->world_size)) : 0;
   if (k_hi) *k_hi = yaw ? std::min(m.H, period * (int32_t)((long long)nper * (p->rank + 1) / p->world_size)) : m.H;
@@ -474,16 +525,15 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     fail(m, SE2M_ERR_UNSUPPORTED, "footprint stencil could not be built (radius or shape)");
     return bail(SE2M_ERR_UNSUPPORTED);
   }
-  // yaw chain: on maps big enough that every CTA takes all its bins, carry moments along
-  // the bins and restart every 9; small maps split the bins across CTAs instead (period 1)
-  m->period = (m->H >= 18 && (long long)p->nx * p->ny >= 512LL * 512LL) ? 9 : 1;
-  if (p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1) {  // shard whole chain periods
+  const bool yaw_sharded = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
+  std::vector<int4> full, chain;
+  tables_for_period(m, runs, nrows, chain_period(m->H, (long long)p->nx * p->ny, yaw_sharded ? p->world_size : 1),
+                    full, chain);
+  if (yaw_sharded) {  // shard whole chain periods
     const int nper = (m->H + m->period - 1) / m->period;
     m->k_lo = std::min(m->H, m->period * (int)((long long)nper * p->rank / p->world_size));
     m->k_hi = std::min(m->H, m->period * (int)((long long)nper * (p->rank + 1) / p->world_size));
   }
-  std::vector<int4> full, chain;
-  build_tables(m, runs, nrows, full, chain);
   // Eq. 4 (reading R6/R7): window origin = floor(x/r) - nx/2 in IEEE double
   m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
   m->J_M = (long long)floor(p->robot_y / p->resolution) - p->ny / 2;
@@ -898,6 +948,12 @@ extern "C" se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* 
     const long long W1 = std::min(TJ * a.TY + (last ? a.TY : a.R_T), m->J_M + a.ny);
     if (W0 < W1) m->dirty.push_back(Rect{m->I_M, m->I_M + a.nx, W0, W1});
   }
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_chain_period(const se2m_map* m, int32_t* period) {
+  if (!m || !period) return SE2M_ERR_INVALID_ARG;
+  *period = m->period;
   return SE2M_OK;
 }
 

@@ -32,7 +32,8 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf", "se2m_sdf_from_mask",
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
-           "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan"]
+           "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
+           "se2m_chain_period"]
 
 
 class Params(ctypes.Structure):
@@ -95,6 +96,7 @@ _lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
+_lib.se2m_chain_period.argtypes = [_vp, ctypes.POINTER(_i32)]
 _lib.se2m_halo_size.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_halo_pack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_unpack.argtypes = [_vp, _i32, _vp]
@@ -109,7 +111,7 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
-              "se2m_halo_plan"):
+              "se2m_halo_plan", "se2m_chain_period"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -425,6 +427,12 @@ class Se2Map:
 
     def synchronize(self):
         return self._check(_lib.se2m_synchronize(self.h))
+
+    def chain_period(self) -> int:
+        """Yaw-chain restart period (1 = no chain)."""
+        v = _i32()
+        self._check(_lib.se2m_chain_period(self.h, ctypes.byref(v)))
+        return v.value
 
     # -- row-band halo exchange (SE2M_SHARD_ROWS, world_size > 1) ----------------------------------
     def halo_size(self):

@@ -67,3 +67,45 @@ def test_window_of_one_row_and_column():
         assert rep["ok"], rep
         assert rep["unknown"] + rep["ill"] == rep["n"] and rep["normal"] == 0
         assert np.all(np.isnan(g["pitch"])) and np.all(g["risk"] == 1) and np.all(g["trav"] == 0)
+
+
+@pytest.mark.parametrize("robot", [(0.37, 0.61), (1.93, -0.44), (-3.05, 2.21)])
+def test_vertical_edge_tiles_second_kernel(robot):
+    """Tiles whose halo crosses only the window's left / right edge run in the column-major edge kernel
+    on the edge stream (2 launches per assess when R_T <= 12): parity with the oracle on a tall window
+    with unknown blobs next to both vertical edges (edge-kernel warps on the general path with holes
+    inside the window, warps on the interior path, warps outside the window), traversable bits included,
+    and INCREMENTAL after a sideways shift == FULL bit-exact."""
+    nx, ny, r, n_yaw = 72, 200, 0.1, 16
+    terrain = Hills(seed=17)
+    m = make_map(nx, ny, r, n_yaw, robot=robot)
+    I_M, J_M = m.origin()
+    h = world_heights(terrain, I_M, J_M, nx, ny, r)
+    rng = np.random.default_rng(11)
+    known = np.ones((ny, nx), np.uint8)
+    for _ in range(12):
+        j = int(rng.integers(0, ny - 3))
+        i = int(rng.choice([rng.integers(0, 6), rng.integers(nx - 6, nx - 1)]))
+        known[j:j + 3, i:i + 2] = 0
+    m.update_elevation(h, known)
+    n0 = m.launch_count()
+    m.assess_se2(0)
+    assert m.launch_count() - n0 == 2                       # main kernel + edge kernel
+    rep = compare(m.download(), oracle.assess_all(oracle_params(nx, ny, r, n_yaw), h, known))
+    assert rep["ok"], rep
+    # a sideways shift moves the window edges across tile columns; INCREMENTAL must equal FULL
+    full = make_map(nx, ny, r, n_yaw, robot=robot)
+    full.update_elevation(h, known)
+    full.assess_se2(0)
+    x, y = robot[0] + 0.57, robot[1]
+    for mm in (m, full):
+        di, dj = mm.shift_window(x, y)
+    I_M, J_M = m.origin()
+    h2 = world_heights(terrain, I_M, J_M, nx, ny, r)
+    m.update_elevation(np.ascontiguousarray(h2[:, nx - di:]), i0=nx - di)
+    full.update_elevation(h2, np.pad(known[:, di:], ((0, 0), (0, di)), constant_values=1))
+    m.assess_se2(1)
+    full.assess_se2(0)
+    a, b = m.download(), full.download()
+    for f in a:
+        assert np.array_equal(a[f], b[f], equal_nan=True), f

@@ -21,24 +21,31 @@ def ncu_csv(rep, *args):
 
 
 def details(rep):
+    """{kernel ID: ({(section, metric): (value, unit)}, kernel name)} of every captured kernel."""
     rows = ncu_csv(rep, "--page", "details")
     h = rows[0]
     d = {}
     for r in rows[1:]:
         x = dict(zip(h, r))
-        d[(x.get("Section Name", ""), x.get("Metric Name", ""))] = (x.get("Metric Value", ""), x.get("Metric Unit", ""))
+        kid = x.get("ID", "0")
+        m, _ = d.setdefault(kid, ({}, x.get("Kernel Name", "")))
+        m[(x.get("Section Name", ""), x.get("Metric Name", ""))] = (x.get("Metric Value", ""), x.get("Metric Unit", ""))
     return d
 
 
 def raw(rep, names):
+    """[{metric: (value, unit)}] per captured kernel, in capture order."""
     rows = ncu_csv(rep, "--page", "raw")
-    h, units, vals = rows[0], rows[1], rows[2]
-    out = {}
-    for n in names:
-        if n in h:
-            i = h.index(n)
-            out[n] = (vals[i], units[i])
-    return out
+    h, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        out = {}
+        for n in names:
+            if n in h:
+                i = h.index(n)
+                out[n] = (vals[i], units[i])
+        res.append(out)
+    return res
 
 
 def num(v):
@@ -86,7 +93,15 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--out")
     a = ap.parse_args()
-    d = details(a.rep)
+    dk = details(a.rep)
+    # one assess call may be two kernels (the main grid and the vertical-window-edge tiles, <R_T, 1>):
+    # the per-kernel fields describe the main one (the longest), the byte / time totals cover the call
+    def dur_ms(m):
+        v, u = m.get(("GPU Speed Of Light Throughput", "Duration"), ("", ""))
+        sc = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
+        return num(v) * sc[u] if num(v) is not None and u in sc else 0.0
+    ids = sorted(dk, key=lambda k: -dur_ms(dk[k][0]))
+    d = dk[ids[0]][0]
     pick = {
         "duration_ms": ("GPU Speed Of Light Throughput", "Duration"),
         "sm_throughput_pct": ("GPU Speed Of Light Throughput", "Compute (SM) Throughput"),
@@ -104,7 +119,7 @@ def main():
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
     if num(dur) is not None and unit in scale:  # ncu prints the unit it chose (us or ms)
         s["duration_ms"] = num(dur) * scale[unit]
-    rw = raw(a.rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
+    rws = raw(a.rep, ["dram__bytes_read.sum", "dram__bytes_write.sum",
                      "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
                      "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
                      "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
@@ -114,13 +129,27 @@ def main():
                      "sm__inst_executed_pipe_xu.sum", "sm__inst_executed_pipe_lsu.sum",
                      "sm__sass_inst_executed_op_shared_ld.sum"])
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    for k, (v, u) in rw.items():
-        x = num(v)
-        if x is not None and u in units:
-            x *= units[u]
-        s[k] = x
-    if s.get("dram__bytes_read.sum") is not None and s.get("dram__bytes_write.sum") is not None:
-        s["dram_bytes_per_launch"] = s["dram__bytes_read.sum"] + s["dram__bytes_write.sum"]
+
+    def vals(rw):
+        o = {}
+        for k, (v, u) in rw.items():
+            x = num(v)
+            if x is not None and u in units:
+                x *= units[u]
+            o[k] = x
+        return o
+    per = [vals(rw) for rw in rws]
+    order = sorted(dk)                      # raw rows follow the capture order of the IDs
+    main_row = order.index(ids[0]) if ids[0] in order else 0
+    s.update(per[main_row])
+    tot = 0.0
+    for v in per:
+        if v.get("dram__bytes_read.sum") is not None and v.get("dram__bytes_write.sum") is not None:
+            tot += v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]
+    s["dram_bytes_per_launch"] = tot        # one assess call: every captured kernel
+    s["kernels"] = [{"name": dk[k][1].split("(")[0], "duration_ms": dur_ms(dk[k][0]),
+                     "dram_bytes": (per[i].get("dram__bytes_read.sum") or 0) + (per[i].get("dram__bytes_write.sum") or 0)}
+                    for i, k in enumerate(order)]
     if a.launches:
         s["launch_shares"] = launches(a.launches)
     s["hot_lines"] = hot_lines(a.rep)
