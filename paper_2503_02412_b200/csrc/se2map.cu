@@ -16,7 +16,7 @@
 #include "se2m_internal.h"
 
 #ifndef SE2M_PERIOD
-#define SE2M_PERIOD 18       // yaw-chain restart period on large maps (A/B knob; 9 and 12 measured slower)
+#define SE2M_PERIOD 36       // yaw-chain restart period on large maps (A/B knob; 9 / 12 / 18 measured slower)
 #endif
 #ifndef SE2M_TSPLIT
 #define SE2M_TSPLIT 1        // vertical-window-edge tiles in their own concurrent kernel (A/B knob)
