@@ -256,8 +256,11 @@ def main():
     positions = [(x + off_x, y) for (x, y) in positions]
     robot0 = (cfg["robot"][0] + off_x, cfg["robot"][1])
 
-    import oracle  # window arithmetic only (Eq. 4 origin) and the cpu_baseline leg
-    I_M0, J_M0 = oracle.window_origin(*robot0, r, nx, ny)
+    shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS if rows_mode else S.SE2M_SHARD_YAW, rank=rank,
+                    world_size=world) if one_map else {}
+    m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
+                 robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream, **shard_kw)
+    I_M0, J_M0 = m.origin()                        # Eq. 4 window origin of the first position
     # world buffer covering every window of the path, resident in HBM (inputs of `value`)
     WX, WY = nx + 2 * margin, ny + 2 * margin
     WI0, WJ0 = I_M0 - margin, J_M0 - margin
@@ -267,10 +270,6 @@ def main():
     world_d = torch.from_numpy(world_h).to(dev)
     world_pinned = torch.from_numpy(world_h).pin_memory()
 
-    shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS if rows_mode else S.SE2M_SHARD_YAW, rank=rank,
-                    world_size=world) if one_map else {}
-    m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
-                 robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream, **shard_kw)
     rng = np.random.default_rng(1)
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -321,7 +320,18 @@ def main():
         torch.cuda.synchronize()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         evk = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-        qs = [None] * K
+        # H10 planner queries of every timed step, prepared up front in pinned memory (states inside the
+        # step's window: within nx/2 - 1 cells of the robot), read back asynchronously (se2m_query_async):
+        # the host queues step t+1 while the GPU still runs step t, as a pipelined robot loop would
+        nq = args.queries
+        q_in, q_out = [], []
+        for t in range(K):
+            x0, y0 = positions[W + t]
+            hx, hy = (nx / 2 - 1) * r, (ny / 2 - 1) * r
+            q = np.stack([rng.uniform(x0 - hx, x0 + hx, nq), rng.uniform(y0 - hy, y0 + hy, nq),
+                          rng.uniform(-math.pi, math.pi, nq)], axis=1)
+            q_in.append(torch.from_numpy(q).pin_memory())
+            q_out.append(torch.empty((5, nq), dtype=torch.float32).pin_memory())
         launches0 = m.launch_count()
         with ClockSampler(local) as clk:
             for t in range(K):
@@ -334,10 +344,10 @@ def main():
                 evk[t][0].record(stream)
                 m.assess_se2(S.SE2M_FULL)
                 evk[t][1].record(stream)
-                q = m.query(queries(I_M, J_M))     # H10 (synchronises: the planner reads the map)
+                m.query_async(q_in[t], q_out[t])     # H10 (D2H of the answers inside the step)
                 ev[t][1].record(stream)
-                qs[t] = q
             stream.synchronize()
+        n_unanswered = sum(int(torch.isnan(o[0]).sum()) for o in q_out)  # all queries lie inside the window
         launches = m.launch_count() - launches0
         step_ms = [a.elapsed_time(b) for a, b in ev]
         kern_ms = [a.elapsed_time(b) for a, b in evk]
@@ -476,9 +486,10 @@ def main():
                        "l2": "256 MB buffer written between timed steps (outside the step events); "
                              "each step also writes %.2f GB of outputs" % (n_states * 16.125 / 1e9),
                        "step": ("shift_window + update_elevation(own rows, D2D from HBM) + exchange_halo (NCCL) + "
-                                "assess_se2(FULL, own tile rows) + query(%d states)" if rows_mode else
+                                "assess_se2(FULL, own tile rows) + query_async(%d states)" if rows_mode else
                                 "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
-                                "query(%d states)") % args.queries},
+                                "query_async(%d states, answers D2H to pinned memory)") % args.queries,
+                       "queries_unanswered": n_unanswered},
             "ms_per_full_update": kern_s / K * 1e3,
             "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
             "ms_per_full_update_p10_p50_p90": [float(np.percentile(kern_ms, q)) for q in (10, 50, 90)],
@@ -622,7 +633,6 @@ def small_configs(S, stream, torch):
     """paper-like FULL update time and the rolling-window stream step (INCREMENTAL), in microseconds."""
     out = {}
     from synth.terrain import robot_path
-    import oracle
     for name in ("paper", "stream"):
         cfg = CONFIGS[name]
         nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]

@@ -150,6 +150,14 @@ se2m_status se2m_step(se2m_map* m, double x, double y, const float* world, int64
 se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, float* pitch,
                        float* roll, float* z, uint8_t* trav);
 
+/* Asynchronous query (the planner's pipelined read): the same lookups as se2m_query, written to
+ * out = 5 x n floats, planar: risk[n], pitch[n], roll[n], z[n], trav[n] (1.0 / 0.0); states outside the
+ * window (or not owned) give NaN / risk 1 / trav 0.  xyt and out are host (mem = SE2M_MEM_HOST; use
+ * pinned memory for a truly asynchronous copy) or device pointers.  Queued on the map's stream and not
+ * synchronised: out is valid after se2m_synchronize (or an event recorded on the stream); xyt must stay
+ * untouched until then.  No out-of-range status (read the NaNs). */
+se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xyt, float* out, int32_t mem);
+
 /* Whole output planes in LOGICAL window order, layout [k][j][i] (n_yaw * ny * nx entries per
  * non-NULL pointer; trav as bytes 0/1).  mem says whether the output pointers are host or
  * device memory.  States this rank does not own (yaw bins or tile-row bands, see se2m_shard_plan) are

@@ -1019,6 +1019,23 @@ extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, flo
   return n_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query: some states outside the window / not owned") : SE2M_OK;
 }
 
+extern "C" se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xyt, float* out, int32_t mem) {
+  if (!m) return SE2M_ERR_INVALID_ARG;
+  if (n < 0 || (n > 0 && (!xyt || !out)) || n > (1ll << 30) || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(m, SE2M_ERR_INVALID_ARG, "query_async: bad n / pointers / mem");
+  if (n == 0) return SE2M_OK;
+  se2m_status st = stage_queries(m, n, xyt);  // (a device xyt is copied device-to-device by cudaMemcpyAsync)
+  if (st != SE2M_OK) return st;
+  AssessParams p = make_params(m);
+  float* dst = mem == SE2M_MEM_DEVICE ? out : m->d_qout;
+  CUDA_TRY(m, launch_query(p, query_geo(m), (int)n, m->d_qxyt, dst, m->d_qcnt, m->stream), "query kernel");
+  m->launches++;
+  if (mem == SE2M_MEM_HOST)
+    CUDA_TRY(m, cudaMemcpyAsync(out, m->d_qout, (size_t)n * 5 * sizeof(float), cudaMemcpyDeviceToHost, m->stream),
+             "D2H query");
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z, uint8_t* trav,
                                      int32_t mem) {
   if (!m) return SE2M_ERR_INVALID_ARG;

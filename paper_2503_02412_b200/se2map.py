@@ -33,7 +33,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
            "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
-           "se2m_chain_period"]
+           "se2m_chain_period", "se2m_query_async"]
 
 
 class Params(ctypes.Structure):
@@ -96,6 +96,7 @@ _lib.se2m_download_compact_rep.argtypes = [_vp, _vp, _vp, _i32]
 _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
+_lib.se2m_query_async.argtypes = [_vp, _i64, _vp, _vp, _i32]
 _lib.se2m_chain_period.argtypes = [_vp, ctypes.POINTER(_i32)]
 _lib.se2m_halo_size.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_halo_pack.argtypes = [_vp, _i32, _vp]
@@ -111,7 +112,7 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
-              "se2m_halo_plan", "se2m_chain_period"):
+              "se2m_halo_plan", "se2m_chain_period", "se2m_query_async"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -295,6 +296,17 @@ class Se2Map:
         self._check(st, ok=(SE2M_OK, SE2M_ERR_OUT_OF_RANGE))
         out["status"] = st
         return out
+
+    def query_async(self, xyt, out):
+        """Queue the lookups of xyt (n x 3 float64: pinned host tensor / NumPy view of one, or CUDA tensor)
+        into out (5 x n float32, same memory kind: risk, pitch, roll, z, trav as rows); valid after
+        synchronize().  Both buffers must stay alive and untouched until then."""
+        n = xyt.shape[0]
+        xp, mem, _ = _ptr_nocopy(xyt)
+        op, mem2, _ = _ptr_nocopy(out)
+        if mem != mem2 or tuple(out.shape) != (5, n):
+            raise ValueError("xyt and out: same memory kind, out of shape (5, n)")
+        return self._check(_lib.se2m_query_async(self.h, n, xp, op, mem))
 
     def download(self, planes=("risk", "pitch", "roll", "z", "trav"), out=None):
         """Whole planes in logical [k][j][i] order as NumPy arrays (or into ``out`` dict of arrays/tensors)."""
