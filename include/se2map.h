@@ -125,10 +125,13 @@ se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w
 se2m_status se2m_shift_window(se2m_map* m, double robot_x, double robot_y, int32_t* out_di,
                               int32_t* out_dj);
 
-/* Algorithm 1 for every SE(2) state of this rank's share (mode SE2M_FULL), or only for the
- * states whose footprint touches a cell changed since the last assess (SE2M_INCREMENTAL;
- * results are bit-identical to FULL).  Asynchronous on the handle's stream.
- * SE2M_ERR_STATE if no elevation was ever written. */
+/* Algorithm 1 for every SE(2) state of this rank's share (mode SE2M_FULL), or
+ * only for the states whose footprint touches a cell changed since the last assess
+ * (SE2M_INCREMENTAL; results are bit-identical to FULL).  Asynchronous on the handle's stream: the
+ * tiles at the window's left / right edge run in a second kernel on an internal stream that is
+ * forked from and joined back into the handle's stream with events, so work queued on the handle's
+ * stream after this call (and se2m_synchronize) sees all results.  SE2M_ERR_STATE if no elevation
+ * was ever written; SE2M_ERR_UNSUPPORTED if a footprint's tables cannot fit a CTA's shared memory. */
 se2m_status se2m_assess_se2(se2m_map* m, int32_t mode);
 
 /* One rolling-window step against a larger device-resident source map, H1 + H2 + H9 in one call (two
