@@ -554,33 +554,35 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
 
-  // ---- 2. validity + reference height (exact min/max: order-independent) --------------------
-  float mn = INFINITY, mxv = -INFINITY;
-  int allv = 1;
-  for (int idx = tid; idx < HX * HY; idx += NTHREADS) {
-    const float v = raw[idx];
-    if (isnan(v)) allv = 0;
-    else { mn = fminf(mn, v); mxv = fmaxf(mxv, v); }
-  }
+  // ---- 2. reference height, validity and the tile plane in one pass over the halo ---------------
+  // href = the halo's centre cell (any height near the data keeps the FP32 sums accurate); a tile whose
+  // centre is unknown takes the exact min / max midpoint of its known cells instead (extra pass)
+  float href = raw[(HY / 2) * HX + HX / 2];
+  if (isnan(href)) {  // CTA-uniform
+    float mn = INFINITY, mxv = -INFINITY;
+    for (int idx = tid; idx < HX * HY; idx += NTHREADS) {
+      const float v = raw[idx];
+      if (!isnan(v)) { mn = fminf(mn, v); mxv = fmaxf(mxv, v); }
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mxv = fmaxf(mxv, __shfl_xor_sync(0xffffffffu, mxv, o));
-  }
-  allv = __all_sync(0xffffffffu, allv);
-  if (lane == 0) { red[warp] = mn; red[8 + warp] = mxv; red[16 + warp] = allv ? 1.f : 0.f; }
-  __syncthreads();
-  mn = red[0]; mxv = red[8];
-  float allvf = red[16];
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mxv = fmaxf(mxv, __shfl_xor_sync(0xffffffffu, mxv, o));
+    }
+    if (lane == 0) { red[warp] = mn; red[8 + warp] = mxv; }
+    __syncthreads();
+    mn = red[0]; mxv = red[8];
 #pragma unroll
-  for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); allvf = fminf(allvf, red[16 + w]); }
-  const bool fast = allvf > 0.5f && !p.force_general;
-  const float href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
+    for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); }
+    href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
+    __syncthreads();  // red[] is reused below
+  }
 
   // ---- 2b. tile plane: least squares over the valid halo cells (fixed reduction order) ----------
   // The prefix sums below hold h^ = h - href - (c + gx x' + gy y'), so their magnitudes are the
   // terrain's deviation from the tile plane; the covariance is mapped back exactly in the epilogue
   // (Cov(x, h) = Cov(x, h^) + G Cov(x, x), G = g / r).  Any plane is correct; this one is accurate.
+  // The count of valid cells also decides the interior ("fast") path: every halo cell known.
   constexpr float XC = (float)(R_T + TX / 2);  // x' = col - XC; the state at lane l has x' = l - TX/2
   constexpr float YC = (float)(R_T + TY / 2);  // y' = row - YC; tile row t has y' = t - TY/2
   float* tplane = red + 8 * 9;
@@ -604,7 +606,6 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       q6 += __shfl_xor_sync(0xffffffffu, q6, o); q7 += __shfl_xor_sync(0xffffffffu, q7, o);
       q8 += __shfl_xor_sync(0xffffffffu, q8, o);
     }
-    __syncthreads();  // red[] (min/max) consumed by every thread above
     if (lane == 0) {
       red[0 * 8 + warp] = q0; red[1 * 8 + warp] = q1; red[2 * 8 + warp] = q2; red[3 * 8 + warp] = q3;
       red[4 * 8 + warp] = q4; red[5 * 8 + warp] = q5; red[6 * 8 + warp] = q6; red[7 * 8 + warp] = q7;
@@ -632,10 +633,12 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         c = mhq - gx * mxq - gy * myq;
       }
       tplane[0] = c; tplane[1] = gx; tplane[2] = gy;
+      tplane[3] = t[0] == (float)(HX * HY) ? 1.f : 0.f;  // exact: counts below 2^24
     }
     __syncthreads();
   }
   const float pc = tplane[0], pgx = tplane[1], pgy = tplane[2];
+  const bool fast = tplane[3] > 0.5f && !p.force_general;
 
   // run entries of this CTA's bins as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj)
   // (interior tiles: the yaw chain table; border tiles: full rows)
