@@ -11,7 +11,8 @@
 //                    consecutive columns: the words are shared);
 //   sdf_rows_kernel  one thread per cell: min over |dx| <= W of dx^2 + g(x + dx)^2 with g the column
 //                    distance to the other class (squares staged in shared memory, "none" = a large
-//                    sentinel, so the loop is branch-free), stopping once dx^2 reaches the best; a
+//                    sentinel, so the loop is branch-free; two offsets per step), stopping once dx^2
+//                    reaches the best; a
 //                    row-prefix count of the columns that have such a cell within W rejects cells with
 //                    none in O(1).
 #include <math.h>
@@ -80,13 +81,16 @@ __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
 
 __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
   extern __shared__ unsigned char sm[];
-  const int W = p.W, RW = SDF_ROWT + 2 * W;
+  // the region reaches P = W + 1 columns past the tile on either side, so the scan below can test two
+  // offsets per step; a candidate at |dx| = W + 1 lies beyond d_max (W = ceil(d_max / r)) and clamps to
+  // d_max exactly like "none"
+  const int W = p.W, P = W + 1, RW = SDF_ROWT + 2 * P;
   int* g2O = reinterpret_cast<int*>(sm);          // [RW] dO^2 (kFar: none within W / outside)
   int* g2F = g2O + RW;                            // [RW] dF^2
   unsigned short* cO = reinterpret_cast<unsigned short*>(g2F + RW);  // [RW + 1] prefix counts of dO <= W
   unsigned short* cF = cO + RW + 1;                                  // ... of dF <= W
   constexpr int kFar = 1 << 24;
-  const int L = blockIdx.z, j = blockIdx.y, x0 = blockIdx.x * SDF_ROWT - W;
+  const int L = blockIdx.z, j = blockIdx.y, x0 = blockIdx.x * SDF_ROWT - P;
   const uint16_t* grow = p.g + ((size_t)L * p.ny + j) * p.nx;
   for (int c = threadIdx.x; c < RW; c += SDF_ROWT) {
     const int x = x0 + c;
@@ -116,17 +120,19 @@ __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
     }
   }
   __syncthreads();
-  const int x = x0 + W + threadIdx.x;
+  const int x = x0 + P + threadIdx.x;
   if (x >= p.nx) return;
-  const int c = W + threadIdx.x;
+  const int c = P + threadIdx.x;
   const bool obst = g2O[c] == 0;          // own row distance to an obstacle is 0: the cell is one
   const int* g2 = obst ? g2F : g2O;       // distance to the other class
   const unsigned short* cnt = obst ? cF : cO;
   int best = kFar;
   if (cnt[c + W + 1] != cnt[c - W]) {     // some column within W has a cell of the other class
     best = g2[c];
-    for (int dx = 1, dx2 = 1; dx <= W && dx2 < best; dx2 += 2 * dx + 1, ++dx)
+    for (int dx = 1, dx2 = 1; dx <= W && dx2 < best; dx2 += 4 * dx + 4, dx += 2) {  // offsets dx, dx + 1
       best = min(best, dx2 + min(g2[c - dx], g2[c + dx]));
+      best = min(best, dx2 + 2 * dx + 1 + min(g2[c - dx - 1], g2[c + dx + 1]));
+    }
   }
   float d = best >= kFar ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
   if (obst) d = -d;
@@ -146,7 +152,7 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   sdf_cols_kernel<<<dim3((p.nx + 127) / 128, (p.ny + SDF_SEG - 1) / SDF_SEG, p.layers), 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int RW = SDF_ROWT + 2 * p.W;
+  const int RW = SDF_ROWT + 2 * (p.W + 1);
   const size_t smem = (size_t)RW * 8 + 2 * (size_t)(RW + 1) * 2;
   sdf_rows_kernel<<<dim3((p.nx + SDF_ROWT - 1) / SDF_ROWT, p.ny, p.layers), SDF_ROWT, smem, s>>>(p);
   return cudaGetLastError();
