@@ -8,10 +8,11 @@
 //                    segment plus W = ceil(d_max / r) rows on each side give, per cell, the row distance
 //                    to the nearest obstacle and to the nearest free cell of its column (255 beyond W);
 //                    the class bit of a column is one word load + shift per row (consecutive threads =
-//                    consecutive columns: the words are shared);
+//                    consecutive columns: the words are shared); the downward sweep is kept in shared
+//                    memory, so each cell's (dO | dF << 8) is written to HBM once;
 //   sdf_rows_kernel  one thread per cell: min over |dx| <= W of dx^2 + g(x + dx)^2 with g the column
 //                    distance to the other class (squares staged in shared memory, "none" = a large
-//                    sentinel, so the loop is branch-free; two offsets per step), stopping once dx^2
+//                    sentinel, so the loop is branch-free; four offsets per step), stopping once dx^2
 //                    reaches the best; a
 //                    row-prefix count of the columns that have such a cell within W rejects cells with
 //                    none in O(1).
@@ -26,6 +27,7 @@ constexpr int SDF_SEG = 128;    // rows per column-pass thread
 constexpr int SDF_ROWT = 256;   // columns per row-pass CTA
 
 __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
+  __shared__ uint16_t down[SDF_SEG][128];  // the downward sweep's (dO | dF << 8) of the segment's rows
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int L = blockIdx.z;
   if (i >= p.nx) return;
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
     const int ob = obstacle(j, py);
     dO = ob ? 0 : min(dO + 1, 255);
     dF = ob ? min(dF + 1, 255) : 0;
-    if (j >= j0) g[(size_t)j * p.nx] = (uint16_t)(dO | (dF << 8));
+    if (j >= j0) down[j - j0][threadIdx.x] = (uint16_t)(dO | (dF << 8));
     if (++py == p.ny) py = 0;
   }
   // upward, from W rows below the segment; keep the nearer one, clamp beyond W
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
     dO = ob ? 0 : min(dO + 1, 255);
     dF = ob ? min(dF + 1, 255) : 0;
     if (j < j1) {
-      const uint16_t v = g[(size_t)j * p.nx];
+      const uint16_t v = down[j - j0][threadIdx.x];
       int o = min(dO, (int)(v & 0xff)), f = min(dF, (int)(v >> 8));
       if (o > W) o = 255;
       if (f > W) f = 255;
@@ -81,10 +83,10 @@ __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
 
 __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
   extern __shared__ unsigned char sm[];
-  // the region reaches P = W + 1 columns past the tile on either side, so the scan below can test two
-  // offsets per step; a candidate at |dx| = W + 1 lies beyond d_max (W = ceil(d_max / r)) and clamps to
+  // the region reaches P = W + 3 columns past the tile on either side, so the scan below can test four
+  // offsets per step; a candidate at |dx| > W lies beyond d_max (W = ceil(d_max / r)) and clamps to
   // d_max exactly like "none"
-  const int W = p.W, P = W + 1, RW = SDF_ROWT + 2 * P;
+  const int W = p.W, P = W + 3, RW = SDF_ROWT + 2 * P;
   int* g2O = reinterpret_cast<int*>(sm);          // [RW] dO^2 (kFar: none within W / outside)
   int* g2F = g2O + RW;                            // [RW] dF^2
   unsigned short* cO = reinterpret_cast<unsigned short*>(g2F + RW);  // [RW + 1] prefix counts of dO <= W
@@ -129,9 +131,11 @@ __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
   int best = kFar;
   if (cnt[c + W + 1] != cnt[c - W]) {     // some column within W has a cell of the other class
     best = g2[c];
-    for (int dx = 1, dx2 = 1; dx <= W && dx2 < best; dx2 += 4 * dx + 4, dx += 2) {  // offsets dx, dx + 1
-      best = min(best, dx2 + min(g2[c - dx], g2[c + dx]));
-      best = min(best, dx2 + 2 * dx + 1 + min(g2[c - dx - 1], g2[c + dx + 1]));
+    for (int dx = 1, dx2 = 1; dx <= W && dx2 < best; dx2 += 8 * dx + 16, dx += 4) {  // offsets dx .. dx + 3
+      const int m0 = min(g2[c - dx], g2[c + dx]), m1 = min(g2[c - dx - 1], g2[c + dx + 1]);
+      const int m2 = min(g2[c - dx - 2], g2[c + dx + 2]), m3 = min(g2[c - dx - 3], g2[c + dx + 3]);
+      best = min(min(best, dx2 + m0), dx2 + 2 * dx + 1 + m1);
+      best = min(min(best, dx2 + 4 * dx + 4 + m2), dx2 + 6 * dx + 9 + m3);
     }
   }
   float d = best >= kFar ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
@@ -152,7 +156,7 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   sdf_cols_kernel<<<dim3((p.nx + 127) / 128, (p.ny + SDF_SEG - 1) / SDF_SEG, p.layers), 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int RW = SDF_ROWT + 2 * (p.W + 1);
+  const int RW = SDF_ROWT + 2 * (p.W + 3);
   const size_t smem = (size_t)RW * 8 + 2 * (size_t)(RW + 1) * 2;
   sdf_rows_kernel<<<dim3((p.nx + SDF_ROWT - 1) / SDF_ROWT, p.ny, p.layers), SDF_ROWT, smem, s>>>(p);
   return cudaGetLastError();
