@@ -50,11 +50,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--queries", type=int, default=4096)
-    ap.add_argument("--shard", default="maps", choices=["maps", "rows", "yaw"],
-                    help="N > 1: 'maps' = one independent map per GPU (weak scaling, default); 'rows' = ONE map "
-                         "split into interleaved tile-row bands, each rank fed only its own rows, halo rows "
-                         "exchanged by NCCL send/recv every step; 'yaw' = ONE map, every rank fed the whole "
-                         "window, each assessing its slice of yaw bins (both strong scaling, SURVEY.md §8(e))")
+    ap.add_argument("--shard", default="auto", choices=["auto", "maps", "rows", "yaw"],
+                    help="N > 1: 'rows' = ONE map split into interleaved tile-row bands, each rank fed only its own "
+                         "rows, halo rows exchanged inside the library by NCCL send/recv every step "
+                         "(se2m_exchange_halo); 'yaw' = ONE map, every rank fed the whole window, each assessing "
+                         "its slice of yaw bins (both strong scaling, SURVEY.md §8(e)); 'maps' = one independent "
+                         "map per GPU (weak scaling); 'auto' (default) = the north_star's split of the config: "
+                         "rows for large, yaw for highres, maps otherwise")
     return ap.parse_args()
 
 
@@ -237,6 +239,12 @@ def main():
     from paper_2503_02412_b200 import se2map as S
 
     world, rank, local = rank_env()
+    if args.shard == "auto":
+        args.shard = {"large": "rows", "highres": "yaw"}.get(args.config, "maps")
+    if world > 1:  # NCCL's communicator-init lines (nRanks, transports) on stderr, for the scaling record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -258,6 +266,16 @@ def main():
 
     shard_kw = dict(shard_mode=S.SE2M_SHARD_ROWS if rows_mode else S.SE2M_SHARD_YAW, rank=rank,
                     world_size=world) if one_map else {}
+    nccl_version = None
+    if rows_mode:
+        # the library's own NCCL communicator carries the halo (se2m_exchange_halo); torch.distributed only
+        # bootstraps its unique id (plumbing): rank 0 makes it, a broadcast hands it to the other ranks
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid, nccl_version = S.nccl_unique_id()
+            idt.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
+        dist.broadcast(idt, src=0)
+        shard_kw["nccl_unique_id"] = bytes(idt.cpu().numpy().tobytes())
     m = S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, ellipse_ex=cfg["ex"], ellipse_ey=cfg["ey"],
                  robot_x=robot0[0], robot_y=robot0[1], device=local, cuda_stream=stream.cuda_stream, **shard_kw)
     I_M0, J_M0 = m.origin()                        # Eq. 4 window origin of the first position
@@ -325,11 +343,18 @@ def main():
         # the host queues step t+1 while the GPU still runs step t, as a pipelined robot loop would
         nq = args.queries
         q_in, q_out = [], []
+        TYq = m.tile_info()[1]
         for t in range(K):
             x0, y0 = positions[W + t]
             hx, hy = (nx / 2 - 1) * r, (ny / 2 - 1) * r
-            q = np.stack([rng.uniform(x0 - hx, x0 + hx, nq), rng.uniform(y0 - hy, y0 + hy, nq),
-                          rng.uniform(-math.pi, math.pi, nq)], axis=1)
+            ys = rng.uniform(y0 - hy, y0 + hy, nq)
+            if rows_mode:  # a row-band rank answers for its own rows: the planner routes queries by row
+                Jq = np.floor(ys / r).astype(np.int64)
+                Jq = Jq + (((rank - np.floor_divide(Jq, TYq)) % world) * TYq)   # same offset in the own band
+                Jlo = int(math.floor(y0 / r)) - ny // 2
+                Jq = np.where(Jq < Jlo + ny, Jq, Jq - world * TYq)
+                ys = (Jq + rng.uniform(0.01, 0.99, nq)) * r
+            q = np.stack([rng.uniform(x0 - hx, x0 + hx, nq), ys, rng.uniform(-math.pi, math.pi, nq)], axis=1)
             q_in.append(torch.from_numpy(q).pin_memory())
             q_out.append(torch.empty((5, nq), dtype=torch.float32).pin_memory())
         launches0 = m.launch_count()
@@ -407,6 +432,8 @@ def main():
                        "t overlaps step t+1 on a copy stream; host wall clock to the last D2H"}
 
     if rank != 0:
+        m.close()
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -489,7 +516,10 @@ def main():
                                 "assess_se2(FULL, own tile rows) + query_async(%d states)" if rows_mode else
                                 "shift_window + update_elevation(full window, D2D from HBM) + assess_se2(FULL) + "
                                 "query_async(%d states, answers D2H to pinned memory)") % args.queries,
-                       "queries_unanswered": n_unanswered},
+                       "queries_unanswered": n_unanswered,
+                       "halo_transport": ("se2m_exchange_halo: the library's NCCL communicator (version %s, %d ranks), "
+                                          "ncclSend/ncclRecv of the packed halo slabs on the map's stream"
+                                          % (nccl_version, world)) if rows_mode else None},
             "ms_per_full_update": kern_s / K * 1e3,
             "ms_per_step_p10_p50_p90": [float(np.percentile(step_ms, q)) for q in (10, 50, 90)],
             "ms_per_full_update_p10_p50_p90": [float(np.percentile(kern_ms, q)) for q in (10, 50, 90)],
@@ -497,6 +527,9 @@ def main():
             "cpu_baseline": cpu, "extras": extras,
             "setup": {"terrain_gen_s": round(gen_s, 2)}}
     print(json.dumps(line), flush=True)
+    m.close()                                      # free the map's streams / memory before interpreter teardown
+    del world_d, l2_flush
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

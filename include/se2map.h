@@ -45,7 +45,8 @@ typedef enum {
   SE2M_ERR_CUDA = 3,          /* a CUDA runtime call or kernel launch failed */
   SE2M_ERR_UNSUPPORTED = 4,   /* parameter combination not built into this library */
   SE2M_ERR_OUT_OF_RANGE = 5,  /* a query / rectangle lies (partly) outside the window */
-  SE2M_ERR_STATE = 6          /* call order violated, e.g. assess before any elevation */
+  SE2M_ERR_STATE = 6,         /* call order violated, e.g. assess before any elevation */
+  SE2M_ERR_NCCL = 7           /* NCCL missing, communicator creation or a halo transfer failed */
 } se2m_status;
 
 enum { SE2M_FULL = 0, SE2M_INCREMENTAL = 1 };          /* se2m_assess_se2 mode */
@@ -79,6 +80,12 @@ typedef struct {
    *     refreshed automatically when the map changed since the last refresh. */
   int32_t inpaint;
   int32_t reserved1;
+  /* Row-band halo transport (SE2M_SHARD_ROWS with world_size > 1, se2m_exchange_halo): the 128-byte NCCL
+   * unique id every rank of the job passes (made by se2m_nccl_unique_id on one rank and sent to the others
+   * by the caller's own bootstrap channel), or NULL for no communicator.  With an id, se2m_init creates the
+   * library's NCCL communicator (rank, world_size) on `device` — a collective: every rank must call se2m_init
+   * with the same id.  The library copies the id; the pointer need not outlive the call. */
+  const void* nccl_unique_id;
 } se2m_params;
 
 /* NEXT-1: one LiDAR frame.  Rotations row-major (world <- body, body <- sensor), covariances 3x3. */
@@ -196,8 +203,8 @@ se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t* n);
  * rank g + 1 own.  Exchange, per step, before se2m_assess_se2:
  *   se2m_halo_pack(m, -1, a)  -> send a to rank g - 1;   se2m_halo_pack(m, +1, b) -> send b to rank g + 1;
  *   receive c from rank g + 1 -> se2m_halo_unpack(m, +1, c);  d from rank g - 1 -> se2m_halo_unpack(m, -1, d).
- * The transfer (NCCL send/recv over NVLink) is the caller's; the Python binding's Se2Map.exchange_halo
- * does it with torch.distributed on the map's stream.  Buffers: device memory of cap x slab_rows x nx
+ * se2m_exchange_halo does all of it inside the library over NCCL (below); pack / unpack stay public for
+ * callers with their own transport.  Buffers: device memory of cap x slab_rows x nx
  * floats (se2m_halo_size), slab q = slab_rows window-width rows in logical column order; rows outside the
  * window are NaN in a packed buffer and ignored on unpack.  Slab lists are derived from the window origin,
  * which every rank shares, so sender and receiver agree without metadata.  pack only reads the ring;
@@ -207,6 +214,21 @@ se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t* n);
 se2m_status se2m_halo_size(const se2m_map* m, int32_t* cap, int32_t* slab_rows);
 se2m_status se2m_halo_pack(se2m_map* m, int32_t dir, float* dst);
 se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* src);
+/* The exchange itself, inside the library ("ncclSend/Recv to (g +- 1) mod G"): packs this
+ * rank's outgoing slabs (as se2m_halo_pack, both directions), runs ncclGroupStart; ncclSend(first rows ->
+ * g - 1); ncclRecv(<- g + 1); ncclSend(last rows -> g + 1); ncclRecv(<- g - 1); ncclGroupEnd on the map's
+ * stream over the communicator made by se2m_init from params.nccl_unique_id, and unpacks what arrived (as
+ * se2m_halo_unpack from both sides).  Every rank calls it once per step after writing its own rows and before
+ * se2m_assess_se2; all of it is asynchronous on the map's stream (no host synchronisation).  With G = 2 both
+ * neighbours are the same peer: sends and receives between a pair match in issue order, and the order above
+ * pairs each send with the peer's receive of the same slab set.  SE2M_ERR_INVALID_ARG unless row-sharded with
+ * world_size > 1; SE2M_ERR_STATE without a communicator; SE2M_ERR_NCCL when a transfer fails to enqueue.
+ * Device buffers (4 x cap x slab_rows x nx floats) are allocated on first use. */
+se2m_status se2m_exchange_halo(se2m_map* m);
+/* Host-only: a fresh NCCL unique id (out, bytes >= 128) for params.nccl_unique_id; SE2M_ERR_NCCL when NCCL
+ * cannot be loaded.  *version (may be NULL) = the loaded NCCL's version code (e.g. 22809). */
+se2m_status se2m_nccl_unique_id(void* out, int32_t bytes, int32_t* version);
+
 /* Host-only (no device): the slab list of rank `sender` for window origin row J_M: first_rows[q] = first
  * world row of slab q (slab_rows rows), or INT64_MIN past the end of the list; last = 0: the first rows of
  * the sender's tile rows (the slabs it sends to rank sender - 1), 1: the last rows (to sender + 1).
@@ -248,7 +270,9 @@ se2m_status se2m_download_inpainted(se2m_map* m, float* heights, int32_t mem);
  * between cell centres to the nearest obstacle state of the same layer, an obstacle state's value is
  * minus the distance to the nearest free state; cells outside the window are neither; values are
  * clamped to [-d_max, d_max] (d_max / resolution <= 96).  Exact within d_max.  Asynchronous.
- * Bins k and k + n/2 share an obstacle set and thus a layer.  SE2M_ERR_UNSUPPORTED with row sharding. */
+ * Bins k and k + n/2 share an obstacle set and thus a layer.  SE2M_ERR_UNSUPPORTED with row sharding;
+ * SE2M_ERR_STATE when the risk map is stale (no assess since the last shift / update / scan).  With yaw
+ * sharding only the owned layers are computed: the others read as NaN. */
 se2m_status se2m_compute_sdf(se2m_map* m, double d_max);
 
 /* The SDF in logical order, out[k][j][i] for all n_yaw bins (mem: host or device).  Synchronises. */
@@ -277,8 +301,9 @@ se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, in
 
 /* Yaw-chain restart period of the map: moments are carried from bin k-1 to bin k and
  * recomputed from whole footprint rows at bins k = 0 (mod period); 1 = no chain (small maps).  A state's
- * FP32 rounding depends on it, so yaw-sharded maps equal the unsharded one bit for bit exactly when both
- * use the same period (the shard plan keeps the unsharded period unless a rank would get no bins). */
+ * FP32 rounding depends on it; it does not depend on sharding: a yaw shard (se2m_shard_plan: the balanced
+ * split [H g / G, H (g + 1) / G) of the representative bins) whose first bin lies inside a period replays the
+ * chain from the period's restart without storing, so yaw-sharded maps equal the unsharded one bit for bit. */
 se2m_status se2m_chain_period(const se2m_map* m, int32_t* period);
 
 /* World-aligned tile of states one CTA assesses: TX columns x TY rows (SE2M_SHARD_ROWS gives world

@@ -682,8 +682,9 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   if (tmode) {
     const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
     const size_t twplane = (size_t)p.ny * p.trav_words;
-    for (int idx = tid; idx < (ke - kb) * TY; idx += NTHREADS) {
-      const int b = idx / TY, row = idx - b * TY;
+    const int kz = max(kb, p.k_store);  // (replayed bins are not this launch's to store)
+    for (int idx = tid; idx < (ke - kz) * TY; idx += NTHREADS) {
+      const int b = idx / TY + (kz - kb), row = idx - (idx / TY) * TY;
       int py = p.pyM + (int)(lj0 + R_T + row); if (py >= p.ny) py -= p.ny;  // rows are inside the window
       const size_t w = (size_t)(kb + b) * twplane + (size_t)py * p.trav_words + gword;
       p.trav[w] = 0u;
@@ -881,6 +882,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           SYp[q] = fma2(bc(sdj), h, SYp[q]);
         }
       }
+      if (k < p.k_store) continue;  // chain replay only (a yaw shard's first period): nothing to store
       const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
       const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
       unsigned tmine = 0;
@@ -1011,6 +1013,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           Sxyv = fma2(bc(cxy), v, Sxyv);
           Syyv = fma2(bc(cyy), v, Syyv);
         }
+        if (k < p.k_store) continue;  // chain replay only (see AssessParams::k_store)
         float4* outk = p.out + (size_t)k * plane;
         float4* outk2 = p.out + (size_t)(k + p.H) * plane;
         uint32_t* travk = p.trav + (size_t)k * twplane;
@@ -1153,13 +1156,13 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
     if ((e = launch_mode<R_T, 1>(p, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
     ++*n_launch;
   }
-  if ((e = launch_mode<R_T, 0>(p, n_tiles, tmap, stream)) != cudaSuccess) return e;
-  ++*n_launch;
-  if (p.tsplit) {
+  const cudaError_t e0 = launch_mode<R_T, 0>(p, n_tiles, tmap, stream);
+  if (e0 == cudaSuccess) ++*n_launch;
+  if (p.tsplit) {  // join the edge kernel even when the main launch failed: later work must not race it
     if ((e = cudaEventRecord(join, edge)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(stream, join, 0)) != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  return e0;
 }
 
 size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {

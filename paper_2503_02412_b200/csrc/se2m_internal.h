@@ -76,7 +76,10 @@ struct AssessParams {
   int own_G, own_rank, own_ty;
   int n_rects;
   int4 rects[kMaxRects];
-  int k_begin, k_end;    // representative-bin range this launch covers
+  int k_begin, k_end;    // representative-bin range this launch covers (k_begin: a yaw-chain restart)
+  int k_store;           // first bin stored: bins [k_begin, k_store) only replay the yaw chain (a yaw shard
+                         // whose first bin lies inside a chain period carries the moments from the period's
+                         // restart, so its states are bit-identical to the unsharded map's)
   int k_chunk;           // rep bins per CTA (grid.y = ceil((k_end-k_begin)/k_chunk))
   // vertical-window-edge tiles (tile columns tcols[0 .. n_tcols) of the launch) run in a second kernel,
   // assess_kernel<R_T, 1>, on the edge stream (tsplit = 1); the main launch skips them

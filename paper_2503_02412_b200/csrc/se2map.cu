@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/se2map.h"
+#include "nccl_dl.h"
 #include "se2m_internal.h"
 
 #ifndef SE2M_PERIOD
@@ -104,6 +105,10 @@ struct se2m_map {
   bool all_dirty = true;
   std::vector<Rect> dirty;
   long long launches = 0;
+  // row-band halo transport (se2m_exchange_halo): the library's NCCL communicator and its 4 device slab
+  // buffers (to g - 1, to g + 1, from g + 1, from g - 1), allocated on first use
+  ncclComm_t comm = nullptr;
+  float* d_halo[4] = {nullptr, nullptr, nullptr, nullptr};
   std::string err;
 };
 
@@ -116,6 +121,23 @@ static se2m_status fail(se2m_map* m, se2m_status st, const std::string& msg) {
 static se2m_status cuda_fail(se2m_map* m, cudaError_t e, const char* what) {
   return fail(m, SE2M_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+// Every handle call runs on the handle's device and restores the caller's current device on return
+// (two maps on two GPUs in one thread must not see each other's device selection).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DevGuard(const DevGuard&) = delete;
+  DevGuard& operator=(const DevGuard&) = delete;
+};
+#define SE2M_ENTER(m)                          \
+  if (!(m)) return SE2M_ERR_INVALID_ARG;       \
+  DevGuard dev_guard_((m)->prm.device)
 #define CUDA_TRY(m, call, what)                         \
   do {                                                  \
     cudaError_t e_ = (call);                            \
@@ -311,7 +333,8 @@ static AssessParams make_params(const se2m_map* m) {
   p.wk = (float)(m->prm.w_r[0] / m->prm.kappa_max);
   p.wx = (float)(m->prm.w_r[1] / m->prm.phi_x_max);
   p.wy = (float)(m->prm.w_r[2] / m->prm.phi_y_max);
-  p.k_begin = m->k_lo; p.k_end = m->k_hi; p.k_chunk = 1;
+  // the launch starts at the chain restart at or before the first owned bin (replayed, not stored)
+  p.k_begin = m->k_lo - m->k_lo % std::max(1, m->period); p.k_end = m->k_hi; p.k_store = m->k_lo; p.k_chunk = 1;
   p.use_tma = m->tma_ok ? 1 : 0;
   p.force_general = m->force_general ? 1 : 0;
   const bool rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
@@ -365,24 +388,18 @@ static se2m_status validate(const se2m_params* p) {
 
 // Yaw-chain restart period: on maps big enough that every CTA takes all its bins, the
 // moments are carried along the bins and restart every SE2M_PERIOD bins; small maps split the bins across
-// CTAs instead (period 1).  Yaw slices shard whole periods; when that would leave a rank without bins
-// (fewer periods than ranks) the period (<= SE2M_PERIOD) is the one that minimises the largest rank's
-// bin count, ties to the longer period (H = 36, G = 8 -> 5).  Otherwise the single-GPU period is kept, so
-// yaw-sharded results stay bit-identical to the unsharded map's.
-static int chain_period(int H, long long cells, int G) {
+// CTAs instead (period 1).  The period does not depend on yaw sharding: a yaw shard whose first bin lies
+// inside a period replays the chain from that period's restart without storing (AssessParams::k_store),
+// so every state's FP32 arithmetic — and result — is the unsharded map's, bit for bit (pin Q13).
+static int chain_period(int H, long long cells) {
   if (H < 18 || cells < 512LL * 512LL) return 1;
-  if (G <= 1 || (H + SE2M_PERIOD - 1) / SE2M_PERIOD >= G) return SE2M_PERIOD;
-  int best = 1, best_max = INT_MAX;
-  for (int q = 1; q <= SE2M_PERIOD; ++q) {
-    const long long nper = (H + q - 1) / q;
-    int mx = 0;
-    for (int g = 0; g < G; ++g) {
-      const int lo = (int)std::min<long long>(H, q * (nper * g / G)), hi = (int)std::min<long long>(H, q * (nper * (g + 1) / G));
-      mx = std::max(mx, hi - lo);
-    }
-    if (mx <= best_max) { best = q; best_max = mx; }
-  }
-  return best;
+  return SE2M_PERIOD;
+}
+
+// Yaw shards: rank g of G owns the representative bins [H g / G, H (g + 1) / G) (balanced, contiguous).
+static void yaw_share(int H, int rank, int G, int* lo, int* hi) {
+  *lo = (int)((long long)H * rank / G);
+  *hi = (int)((long long)H * (rank + 1) / G);
 }
 
 // The chain tables of one period must fit a CTA's shared memory next to the tile planes (the launch
@@ -424,13 +441,10 @@ extern "C" se2m_status se2m_shard_plan(const se2m_params* p, int32_t* n_rep, int
   const bool yaw = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
   const bool rows = p->shard_mode == SE2M_SHARD_ROWS && p->world_size > 1;
   if (n_rep) *n_rep = m.H;
-  std::vector<int4> full, chain;
-  tables_for_period(&m, runs, nrows, chain_period(m.H, (long long)p->nx * p->ny, yaw ? p->world_size : 1), full,
-                    chain);
-  const int period = m.period;
-  const int nper = (m.H + period - 1) / period;
-  if (k_lo) *k_lo = yaw ? std::min(m.H, period * (int32_t)((long long)nper * p->rank / p->world_size)) : 0;
-  if (k_hi) *k_hi = yaw ? std::min(m.H, period * (int32_t)((long long)nper * (p->rank + 1) / p->world_size)) : m.H;
+  int lo = 0, hi = m.H;
+  if (yaw) yaw_share(m.H, p->rank, p->world_size, &lo, &hi);
+  if (k_lo) *k_lo = lo;
+  if (k_hi) *k_hi = hi;
   if (tile_y) *tile_y = tile_rows(m.R_T);
   if (row_mod) *row_mod = rows ? p->world_size : 1;
   if (row_rank) *row_rank = rows ? p->rank : 0;
@@ -505,8 +519,11 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     se2m_destroy(m);
     return s;
   };
-  cudaError_t e = cudaSetDevice(p->device);
-  if (e != cudaSuccess) { cuda_fail(m, e, "cudaSetDevice"); return bail(SE2M_ERR_CUDA); }
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
+  if (e != cudaSuccess) { cuda_fail(m, e, "cudaGetDeviceCount"); return bail(SE2M_ERR_CUDA); }
+  if (p->device < 0 || p->device >= n_dev) { fail(m, SE2M_ERR_INVALID_ARG, "device ordinal out of range"); return bail(SE2M_ERR_INVALID_ARG); }
+  DevGuard dev_guard_(p->device);
   if (p->cuda_stream) m->stream = (cudaStream_t)p->cuda_stream;
   else {
     e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
@@ -527,13 +544,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   }
   const bool yaw_sharded = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
   std::vector<int4> full, chain;
-  tables_for_period(m, runs, nrows, chain_period(m->H, (long long)p->nx * p->ny, yaw_sharded ? p->world_size : 1),
-                    full, chain);
-  if (yaw_sharded) {  // shard whole chain periods
-    const int nper = (m->H + m->period - 1) / m->period;
-    m->k_lo = std::min(m->H, m->period * (int)((long long)nper * p->rank / p->world_size));
-    m->k_hi = std::min(m->H, m->period * (int)((long long)nper * (p->rank + 1) / p->world_size));
-  }
+  tables_for_period(m, runs, nrows, chain_period(m->H, (long long)p->nx * p->ny), full, chain);
+  if (yaw_sharded) yaw_share(m->H, p->rank, p->world_size, &m->k_lo, &m->k_hi);
   // Eq. 4 (reading R6/R7): window origin = floor(x/r) - nx/2 in IEEE double
   m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
   m->J_M = (long long)floor(p->robot_y / p->resolution) - p->ny / 2;
@@ -577,6 +589,19 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     cuda_fail(m, e, "init upload");
     return bail(SE2M_ERR_CUDA);
   }
+  if (p->nccl_unique_id && p->world_size > 1) {  // the row-band halo transport (collective over the ranks)
+    const NcclApi& nc = nccl_api();
+    if (!nc.ok) { fail(m, SE2M_ERR_NCCL, "NCCL: " + nc.err); return bail(SE2M_ERR_NCCL); }
+    ncclUniqueId id;
+    memcpy(&id, p->nccl_unique_id, sizeof id);
+    const ncclResult_t r = nc.CommInitRank(&m->comm, p->world_size, id, p->rank);
+    if (r != ncclSuccess) {
+      m->comm = nullptr;
+      fail(m, SE2M_ERR_NCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
+      return bail(SE2M_ERR_NCCL);
+    }
+  }
+  m->prm.nccl_unique_id = nullptr;  // copied (the caller's pointer need not outlive se2m_init)
   m->tma_ok = make_tensor_map(m, &m->tmap, m->d_h);
   {
     int optin = 0;
@@ -589,6 +614,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
 
 extern "C" void se2m_destroy(se2m_map* m) {
   if (!m) return;
+  DevGuard dev_guard_(m->prm.device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
                   m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
@@ -611,13 +637,16 @@ extern "C" void se2m_destroy(se2m_map* m) {
   }
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
+  for (float* b : m->d_halo)
+    if (b) cudaFree(b);
+  if (m->comm) nccl_api().CommDestroy(m->comm);  // after the stream drained: no transfer in flight
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
 
 extern "C" se2m_status se2m_update_elevation(se2m_map* m, int32_t i0, int32_t j0, int32_t w, int32_t h,
                                              const float* heights, int64_t ld, const uint8_t* known, int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (w == 0 || h == 0) return SE2M_OK;  // nothing to write (the pointer of an empty array may be NULL)
   if (!heights || w < 0 || h < 0 || ld < w || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
     return fail(m, SE2M_ERR_INVALID_ARG, "update_elevation: bad pointer / size / mem");
@@ -698,7 +727,7 @@ static void clamp_out(long long d, int32_t* out) {
 }
 
 extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_t* out_di, int32_t* out_dj) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "shift_window: position not finite");
   long long di, dj;
   int4 strips[2];
@@ -719,7 +748,7 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
 extern "C" se2m_status se2m_step(se2m_map* m, double x, double y, const float* world, int64_t world_ld,
                                  int64_t world_I0, int64_t world_J0, int32_t world_w, int32_t world_h,
                                  int32_t mem, int32_t* out_di, int32_t* out_dj) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (!isfinite(x) || !isfinite(y)) return fail(m, SE2M_ERR_INVALID_ARG, "step: position not finite");
   if (!world || mem != SE2M_MEM_DEVICE || world_w < 0 || world_h < 0 || world_ld < world_w)
     return fail(m, SE2M_ERR_INVALID_ARG, "step: world must be a device plane with ld >= w");
@@ -772,7 +801,7 @@ static se2m_status run_inpaint(se2m_map* m, int* n_known) {
 }
 
 extern "C" se2m_status se2m_inpaint(se2m_map* m) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   int n_known = 0;
   se2m_status st = run_inpaint(m, &n_known);
   if (st != SE2M_OK) return st;
@@ -781,7 +810,7 @@ extern "C" se2m_status se2m_inpaint(se2m_map* m) {
 }
 
 extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (mode != SE2M_FULL && mode != SE2M_INCREMENTAL) return fail(m, SE2M_ERR_INVALID_ARG, "assess: bad mode");
   if (!m->have_data) return fail(m, SE2M_ERR_STATE, "assess before any update_elevation");
   if (m->prm.inpaint && !m->inpaint_valid) {  // NEXT-4: assess the inpainted view
@@ -837,7 +866,8 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   // yaw chunking: all bins per CTA (tile reuse) unless that leaves SMs idle; then split the bins so the
   // CTAs fill one wave (2 resident CTAs on each of the 148 SMs) — each CTA pays the tile load, plane fit
   // and prefix build once, so more, shorter CTAs than that only add fixed cost
-  const int nk = m->k_hi - m->k_lo;
+  const int kbeg = p.k_begin;  // chain restart at or before k_lo
+  const int nk = m->k_hi - kbeg;
   int chunk = nk;
   if (n_tiles > 0) {
     const long long slots = 2LL * 148;
@@ -850,7 +880,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   int cap = 1;
   for (;;) {
     cap = 1;
-    for (int kb = m->k_lo; kb < m->k_hi; kb += chunk) {
+    for (int kb = kbeg; kb < m->k_hi; kb += chunk) {
       const int ke = std::min(kb + chunk, m->k_hi);
       const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
       cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
@@ -886,7 +916,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
       p.n_tcols = 0;
     }
   }
-  if (n_tiles > 0 && nk > 0) {
+  if (n_tiles > 0 && nk > 0 && m->k_hi > m->k_lo) {
     int nl = 0;
     cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
@@ -917,7 +947,7 @@ static HaloArgs halo_args(se2m_map* m, int sender, int last, float* buf, int unp
 }
 
 extern "C" se2m_status se2m_halo_pack(se2m_map* m, int32_t dir, float* dst) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   se2m_status st = halo_check(&m->prm, m->R_T);
   if (st != SE2M_OK) return fail(m, st, "halo_pack: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
   if (!dst || (dir != -1 && dir != 1)) return fail(m, SE2M_ERR_INVALID_ARG, "halo_pack: dir must be -1 or +1, dst non-NULL");
@@ -929,7 +959,7 @@ extern "C" se2m_status se2m_halo_pack(se2m_map* m, int32_t dir, float* dst) {
 }
 
 extern "C" se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* src) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   se2m_status st = halo_check(&m->prm, m->R_T);
   if (st != SE2M_OK) return fail(m, st, "halo_unpack: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
   if (!src || (from != -1 && from != 1)) return fail(m, SE2M_ERR_INVALID_ARG, "halo_unpack: from must be -1 or +1, src non-NULL");
@@ -947,6 +977,52 @@ extern "C" se2m_status se2m_halo_unpack(se2m_map* m, int32_t from, const float* 
     const long long W0 = std::max(TJ * a.TY + (last ? a.TY - a.R_T : 0), m->J_M);
     const long long W1 = std::min(TJ * a.TY + (last ? a.TY : a.R_T), m->J_M + a.ny);
     if (W0 < W1) m->dirty.push_back(Rect{m->I_M, m->I_M + a.nx, W0, W1});
+  }
+  return SE2M_OK;
+}
+
+extern "C" se2m_status se2m_exchange_halo(se2m_map* m) {
+  SE2M_ENTER(m);
+  se2m_status st = halo_check(&m->prm, m->R_T);
+  if (st != SE2M_OK) return fail(m, st, "exchange_halo: needs SE2M_SHARD_ROWS, world_size > 1, R_T <= tile rows");
+  if (!m->comm) return fail(m, SE2M_ERR_STATE, "exchange_halo: no communicator (params.nccl_unique_id was NULL)");
+  const int G = m->prm.world_size, g = m->prm.rank, TY = tile_rows(m->R_T);
+  const size_t count = (size_t)halo_cap(m->prm.ny, TY, G) * m->R_T * m->prm.nx;
+  for (float*& b : m->d_halo)
+    if (!b) CUDA_TRY(m, cudaMalloc(&b, count * sizeof(float)), "cudaMalloc(halo)");
+  float *to_lo = m->d_halo[0], *to_hi = m->d_halo[1], *from_hi = m->d_halo[2], *from_lo = m->d_halo[3];
+  if ((st = se2m_halo_pack(m, -1, to_lo)) != SE2M_OK) return st;
+  if ((st = se2m_halo_pack(m, +1, to_hi)) != SE2M_OK) return st;
+  const NcclApi& nc = nccl_api();
+  const int lo = (g - 1 + G) % G, hi = (g + 1) % G;
+  ncclResult_t r = nc.GroupStart();
+  if (r == ncclSuccess) {
+    // issue order (send to lo, recv from hi, send to hi, recv from lo) pairs every send with the peer's
+    // receive of the same slab set, also when lo == hi (G = 2)
+    ncclResult_t q = nc.Send(to_lo, count, ncclFloat32, lo, m->comm, m->stream);
+    if (q == ncclSuccess) q = nc.Recv(from_hi, count, ncclFloat32, hi, m->comm, m->stream);
+    if (q == ncclSuccess) q = nc.Send(to_hi, count, ncclFloat32, hi, m->comm, m->stream);
+    if (q == ncclSuccess) q = nc.Recv(from_lo, count, ncclFloat32, lo, m->comm, m->stream);
+    r = nc.GroupEnd();  // always close the group
+    if (q != ncclSuccess) r = q;
+  }
+  if (r != ncclSuccess) return fail(m, SE2M_ERR_NCCL, std::string("halo send/recv: ") + nc.GetErrorString(r));
+  m->launches += 1;  // the NCCL group kernel
+  if ((st = se2m_halo_unpack(m, +1, from_hi)) != SE2M_OK) return st;
+  return se2m_halo_unpack(m, -1, from_lo);
+}
+
+extern "C" se2m_status se2m_nccl_unique_id(void* out, int32_t bytes, int32_t* version) {
+  if (!out || bytes < (int32_t)sizeof(ncclUniqueId)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "nccl_unique_id: need 128 bytes");
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return fail(nullptr, SE2M_ERR_NCCL, "NCCL: " + nc.err);
+  ncclUniqueId id;
+  const ncclResult_t r = nc.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, SE2M_ERR_NCCL, std::string("ncclGetUniqueId: ") + nc.GetErrorString(r));
+  memcpy(out, &id, sizeof id);
+  if (version) {
+    int v = 0;
+    *version = nc.GetVersion(&v) == ncclSuccess ? v : 0;
   }
   return SE2M_OK;
 }
@@ -990,14 +1066,15 @@ static se2m_status stage_queries(se2m_map* m, int64_t n, const double* xyt) {
   }
   if (!m->d_qcnt) CUDA_TRY(m, cudaMalloc(&m->d_qcnt, sizeof(int)), "cudaMalloc(query)");
   CUDA_TRY(m, cudaMemsetAsync(m->d_qcnt, 0, sizeof(int), m->stream), "query counter");
-  CUDA_TRY(m, cudaMemcpyAsync(m->d_qxyt, xyt, (size_t)n * 3 * sizeof(double), cudaMemcpyHostToDevice, m->stream),
-           "H2D query");
+  // host or device xyt (se2m_query_async with SE2M_MEM_DEVICE): the direction comes from the pointer (UVA)
+  CUDA_TRY(m, cudaMemcpyAsync(m->d_qxyt, xyt, (size_t)n * 3 * sizeof(double), cudaMemcpyDefault, m->stream),
+           "stage query");
   return SE2M_OK;
 }
 
 extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, float* pitch, float* roll,
                                   float* z, uint8_t* trav) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (n < 0 || (n > 0 && !xyt) || n > (1ll << 30)) return fail(m, SE2M_ERR_INVALID_ARG, "query: bad n / xyt");
   if (n == 0) return SE2M_OK;
   se2m_status st = stage_queries(m, n, xyt);
@@ -1020,11 +1097,11 @@ extern "C" se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, flo
 }
 
 extern "C" se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xyt, float* out, int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (n < 0 || (n > 0 && (!xyt || !out)) || n > (1ll << 30) || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
     return fail(m, SE2M_ERR_INVALID_ARG, "query_async: bad n / pointers / mem");
   if (n == 0) return SE2M_OK;
-  se2m_status st = stage_queries(m, n, xyt);  // (a device xyt is copied device-to-device by cudaMemcpyAsync)
+  se2m_status st = stage_queries(m, n, xyt);
   if (st != SE2M_OK) return st;
   AssessParams p = make_params(m);
   float* dst = mem == SE2M_MEM_DEVICE ? out : m->d_qout;
@@ -1038,7 +1115,7 @@ extern "C" se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xy
 
 extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z, uint8_t* trav,
                                      int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download: bad mem");
   const size_t nst = (size_t)m->prm.nx * m->prm.ny * m->prm.n_yaw;
   AssessParams p = make_params(m);
@@ -1092,7 +1169,7 @@ extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, flo
 }
 
 extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact: bad mem");
   const int wpr = (m->prm.nx + 31) / 32;
   const size_t nst = (size_t)m->prm.nx * m->prm.ny * m->prm.n_yaw;
@@ -1155,7 +1232,7 @@ extern "C" se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t
 }
 
 extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact_rep: bad mem");
   const int wpr = (m->prm.nx + 31) / 32;
   const int n_rep = m->paired ? m->H : m->prm.n_yaw;
@@ -1211,7 +1288,7 @@ extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, 
 // ---- NEXT-1: LiDAR frame integration --------------------------------------------------------------------
 extern "C" se2m_status se2m_integrate_scan(se2m_map* m, const float* points, int64_t n, const se2m_pose* pose,
                                            int32_t mem, int64_t* out_counts) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (n < 0 || n > (1ll << 30) || (n > 0 && !points) || !pose || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
     return fail(m, SE2M_ERR_INVALID_ARG, "integrate_scan: bad arguments");
   if (out_counts) memset(out_counts, 0, 5 * sizeof(int64_t));
@@ -1294,7 +1371,8 @@ static se2m_status ring_to_logical(se2m_map* m, const float* ring, float* dst_de
 }
 
 extern "C" se2m_status se2m_download_elevation(se2m_map* m, float* heights, float* variances, int32_t mem) {
-  if (!m || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE)) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
+  if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_elevation: bad mem");
   const size_t cells = (size_t)m->prm.nx * m->prm.ny;
   const float* rings[2] = {m->d_h, m->d_var};
   float* outs[2] = {heights, variances};
@@ -1316,7 +1394,7 @@ extern "C" se2m_status se2m_download_elevation(se2m_map* m, float* heights, floa
 }
 
 extern "C" se2m_status se2m_download_inpainted(se2m_map* m, float* heights, int32_t mem) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (!heights || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
     return fail(m, SE2M_ERR_INVALID_ARG, "download_inpainted: bad pointer / mem");
   if (!m->inpaint_valid) {
@@ -1338,15 +1416,22 @@ extern "C" se2m_status se2m_download_inpainted(se2m_map* m, float* heights, int3
 static int sdf_radius(double d_max, double r) { return (int)ceil(d_max / r - 1e-9); }
 
 extern "C" se2m_status se2m_compute_sdf(se2m_map* m, double d_max) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (!(d_max > 0) || !isfinite(d_max)) return fail(m, SE2M_ERR_INVALID_ARG, "compute_sdf: d_max must be > 0");
   const int W = sdf_radius(d_max, m->prm.resolution);
   if (W > 96) return fail(m, SE2M_ERR_UNSUPPORTED, "compute_sdf: d_max / resolution > 96 cells");
   if (m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1)
     return fail(m, SE2M_ERR_UNSUPPORTED, "compute_sdf: needs whole layers (not available with row sharding)");
   if (!m->have_data) return fail(m, SE2M_ERR_STATE, "compute_sdf before any assess");
+  // the obstacle set is the last assess's: stale once the window moved or cells changed since then
+  if (m->all_dirty || !m->dirty.empty() || (m->prm.inpaint && !m->inpaint_valid))
+    return fail(m, SE2M_ERR_STATE, "compute_sdf: the risk map is stale (assess after the last shift / update)");
   const size_t plane = (size_t)m->prm.nx * m->prm.ny;
-  if (!m->d_sdf) CUDA_TRY(m, cudaMalloc(&m->d_sdf, plane * m->H * sizeof(float)), "cudaMalloc(sdf)");
+  if (!m->d_sdf) {
+    CUDA_TRY(m, cudaMalloc(&m->d_sdf, plane * m->H * sizeof(float)), "cudaMalloc(sdf)");
+    // layers of representative bins this rank does not own (yaw shards) stay NaN (never written)
+    CUDA_TRY(m, cudaMemsetAsync(m->d_sdf, 0xff, plane * m->H * sizeof(float), m->stream), "sdf init");
+  }
   if (!m->d_sdf_g) CUDA_TRY(m, cudaMalloc(&m->d_sdf_g, plane * m->H * sizeof(uint16_t)), "cudaMalloc(sdf scratch)");
   SdfParams sp;
   memset(&sp, 0, sizeof sp);
@@ -1372,8 +1457,11 @@ extern "C" se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32
     return fail(nullptr, SE2M_ERR_INVALID_ARG, "sdf_from_mask: bad arguments");
   const int W = sdf_radius(d_max, resolution);
   if (W > 96) return fail(nullptr, SE2M_ERR_UNSUPPORTED, "sdf_from_mask: d_max / resolution > 96 cells");
-  cudaError_t e = cudaSetDevice(device);
+  int n_dev = 0;
+  cudaError_t e = cudaGetDeviceCount(&n_dev);
   if (e != cudaSuccess) return fail(nullptr, SE2M_ERR_CUDA, cudaGetErrorString(e));
+  if (device < 0 || device >= n_dev) return fail(nullptr, SE2M_ERR_INVALID_ARG, "sdf_from_mask: device ordinal out of range");
+  DevGuard dev_guard_(device);
   const size_t n = (size_t)nx * ny * layers;
   uint8_t* dm = const_cast<uint8_t*>(mask);
   float* dout = out;
@@ -1403,7 +1491,7 @@ extern "C" se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32
 // ---- NEXT-3: trilinear query of Risk / SDF with gradient ------------------------------
 extern "C" se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double* xyt, int32_t field,
                                             float* value, float* grad) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   if (n < 0 || (n > 0 && !xyt) || n > (1ll << 30) || (field != 0 && field != 1))
     return fail(m, SE2M_ERR_INVALID_ARG, "query_trilinear: bad n / xyt / field");
   if (field == 1 && !m->sdf_valid) return fail(m, SE2M_ERR_STATE, "query_trilinear: no SDF (call se2m_compute_sdf)");
@@ -1431,7 +1519,8 @@ extern "C" se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double
 
 // SDF planes in logical order: out[k][j][i] for all n_yaw bins (bins k and k + n/2 share a layer).
 extern "C" se2m_status se2m_download_sdf(se2m_map* m, float* out, int32_t mem) {
-  if (!m || !out || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE)) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
+  if (!out || (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE)) return fail(m, SE2M_ERR_INVALID_ARG, "download_sdf: bad pointer / mem");
   if (!m->sdf_valid) return fail(m, SE2M_ERR_STATE, "download_sdf: no SDF (call se2m_compute_sdf)");
   const int nx = m->prm.nx, ny = m->prm.ny;
   const size_t plane = (size_t)nx * ny, nst = plane * m->prm.n_yaw;
@@ -1479,7 +1568,7 @@ extern "C" se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* 
 }
 
 extern "C" se2m_status se2m_synchronize(se2m_map* m) {
-  if (!m) return SE2M_ERR_INVALID_ARG;
+  SE2M_ENTER(m);
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "synchronize");
   if (m->copy_stream) CUDA_TRY(m, cudaStreamSynchronize(m->copy_stream), "synchronize(copy stream)");
   return SE2M_OK;

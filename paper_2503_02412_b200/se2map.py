@@ -21,7 +21,7 @@ if not os.path.exists(_LIB_PATH):
         "libse2map.so is not built (%s); run __graft_entry__.build() — there is no CPU fallback" % _LIB_PATH)
 
 SE2M_OK, SE2M_ERR_INVALID_ARG, SE2M_ERR_OOM, SE2M_ERR_CUDA, SE2M_ERR_UNSUPPORTED, SE2M_ERR_OUT_OF_RANGE, \
-    SE2M_ERR_STATE = range(7)
+    SE2M_ERR_STATE, SE2M_ERR_NCCL = range(8)
 SE2M_FULL, SE2M_INCREMENTAL = 0, 1
 SE2M_MEM_HOST, SE2M_MEM_DEVICE = 0, 1
 SE2M_SHARD_NONE, SE2M_SHARD_YAW, SE2M_SHARD_ROWS = 0, 1, 2
@@ -33,7 +33,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
            "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
-           "se2m_chain_period", "se2m_query_async"]
+           "se2m_chain_period", "se2m_query_async", "se2m_exchange_halo", "se2m_nccl_unique_id"]
 
 
 class Params(ctypes.Structure):
@@ -47,7 +47,7 @@ class Params(ctypes.Structure):
                 ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("fe_z_min", ctypes.c_double), ("fe_z_max", ctypes.c_double), ("fe_gate", ctypes.c_double),
                 ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double),
-                ("inpaint", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
+                ("inpaint", ctypes.c_int32), ("reserved1", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
 
 
 class Pose(ctypes.Structure):
@@ -103,6 +103,8 @@ _lib.se2m_halo_pack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_unpack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_plan.argtypes = [ctypes.POINTER(Params), _i64, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                 _vp]
+_lib.se2m_exchange_halo.argtypes = [_vp]
+_lib.se2m_nccl_unique_id.argtypes = [_vp, _i32, ctypes.POINTER(_i32)]
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
 _lib.se2m_last_error.argtypes = [_vp]
@@ -112,7 +114,8 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
-              "se2m_halo_plan", "se2m_chain_period", "se2m_query_async"):
+              "se2m_halo_plan", "se2m_chain_period", "se2m_query_async", "se2m_exchange_halo",
+              "se2m_nccl_unique_id"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -127,14 +130,30 @@ class Se2mError(RuntimeError):
 
 
 def default_params(**kw) -> Params:
+    """se2m_default_params + overrides; nccl_unique_id may be given as the 128 bytes of nccl_unique_id()."""
     p = Params()
     _lib.se2m_default_params(ctypes.byref(p))
     for k, v in kw.items():
         if k == "w_r":
             p.w_r = (ctypes.c_double * 3)(*v)
+        elif k == "nccl_unique_id" and isinstance(v, (bytes, bytearray)):
+            buf = ctypes.create_string_buffer(bytes(v), len(v))
+            p._nccl_id_buf = buf                        # keep alive until se2m_init copied it
+            p.nccl_unique_id = ctypes.addressof(buf)
         else:
             setattr(p, k, v)
     return p
+
+
+def nccl_unique_id():
+    """(128-byte NCCL unique id, NCCL version code) made by the library's NCCL (host-only, no GPU): one rank
+    makes it and sends it to the others over the caller's bootstrap channel (e.g. torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    ver = _i32()
+    st = _lib.se2m_nccl_unique_id(buf, 128, ctypes.byref(ver))
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    return buf.raw, ver.value
 
 
 def _ptr(a):
@@ -461,50 +480,11 @@ class Se2Map:
         """Write the slabs received from rank g + frm (frm = -1 / +1) into the map (asynchronous)."""
         return self._check(_lib.se2m_halo_unpack(self.h, frm, _cuda_ptr(src)))
 
-    def exchange_halo(self, group=None):
-        """One halo exchange over torch.distributed (NCCL on the GPU): pack both directions, send to the
-        neighbouring ranks g - 1 and g + 1 and receive from them, unpack — all ordered on the map's stream
-        (the NCCL transfers run on that stream too).  Call after update_elevation of the rank's own rows and
-        before assess_se2."""
-        import torch
-        import torch.distributed as dist
-        G, g = self.params.world_size, self.params.rank
-        if G < 2:
-            return
-        bufs = getattr(self, "_halo_bufs", None)
-        if bufs is None:
-            cap, rows = self.halo_size()
-            dev = torch.device("cuda", self.params.device)
-            bufs = [torch.empty((cap, rows, self.params.nx), dtype=torch.float32, device=dev) for _ in range(4)]
-            self._halo_bufs = bufs
-        send_dn, send_up, recv_up, recv_dn = bufs          # to g - 1, to g + 1, from g + 1, from g - 1
-        stream = torch.cuda.ExternalStream(self.params.cuda_stream) if self.params.cuda_stream \
-            else torch.cuda.current_stream()
-        own_stream = not self.params.cuda_stream            # the library made its own stream
-        with torch.cuda.stream(stream):
-            self.halo_pack(-1, send_dn)
-            self.halo_pack(+1, send_up)
-            if own_stream:
-                self.synchronize()
-            halo_transfer(send_dn, send_up, recv_up, recv_dn, g, G, group)
-            if own_stream:
-                stream.synchronize()
-            self.halo_unpack(recv_up, +1)
-            self.halo_unpack(recv_dn, -1)
+    def exchange_halo(self):
+        """se2m_exchange_halo: pack, NCCL send / recv to ranks g -+ 1 and unpack, all inside the library on the
+        map's stream (needs the map created with nccl_unique_id).  Call after update_elevation of the rank's own
+        rows and before assess_se2."""
+        return self._check(_lib.se2m_exchange_halo(self.h))
 
     def launch_count(self) -> int:
         return int(_lib.se2m_launch_count(self.h))
-
-
-def halo_transfer(send_dn, send_up, recv_up, recv_dn, rank: int, world: int, group=None):
-    """The exchange step of the row-band halo (torch.distributed P2P: NCCL on device tensors, gloo on host
-    tensors in the CPU tests): send_dn -> rank - 1, send_up -> rank + 1; recv_up <- rank + 1 (its send_dn),
-    recv_dn <- rank - 1 (its send_up).  With two ranks both neighbours are the same peer: point-to-point
-    messages between a pair match in issue order, and every rank issues (send_dn, recv_up, send_up, recv_dn),
-    so each receive still gets the right slab set.  NCCL waits are stream-ordered (no host sync)."""
-    import torch.distributed as dist
-    lo, hi = (rank - 1) % world, (rank + 1) % world
-    ops = [dist.P2POp(dist.isend, send_dn, lo, group), dist.P2POp(dist.irecv, recv_up, hi, group),
-           dist.P2POp(dist.isend, send_up, hi, group), dist.P2POp(dist.irecv, recv_dn, lo, group)]
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()

@@ -75,9 +75,22 @@ def test_shard_plan_partitions_and_max_reduce(world):
                     assert len(owners) == 1
 
 
+def halo_transfer(send_dn, send_up, recv_up, recv_dn, rank: int, world: int):
+    """The transfer step of se2m_exchange_halo (csrc/se2map.cu) in the same issue order, over gloo: send_dn ->
+    rank - 1, recv_up <- rank + 1 (its send_dn), send_up -> rank + 1, recv_dn <- rank - 1 (its send_up).  With two
+    ranks both neighbours are one peer; point-to-point messages between a pair match in issue order, so each
+    receive still gets the right slab set (the library's ncclGroupStart/Send/Recv/GroupEnd relies on the same)."""
+    lo, hi = (rank - 1) % world, (rank + 1) % world
+    ops = [dist.P2POp(dist.isend, send_dn, lo), dist.P2POp(dist.irecv, recv_up, hi),
+           dist.P2POp(dist.isend, send_up, hi), dist.P2POp(dist.irecv, recv_dn, lo)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
 def _halo_worker(rank, world, port, q):
     """Each rank holds only its own rows of a random map; slabs are cut by the library's host-only slab
-    plan (se2m_halo_plan), exchanged with se2map.halo_transfer over gloo, and written back by the plan of
+    plan (se2m_halo_plan), exchanged by halo_transfer (the library's send / recv order) over gloo, and written
+    back by the plan of
     the sending rank — then every row the rank's tiles read (owned tile rows +- R_T) must be present."""
     import sys
     sys.path.insert(0, ROOT)
@@ -116,7 +129,7 @@ def _halo_worker(rank, world, port, q):
 
             send_dn, send_up = pack(rank, 0), pack(rank, 1)
             recv_up, recv_dn = torch.empty_like(send_dn), torch.empty_like(send_up)
-            S.halo_transfer(send_dn, send_up, recv_up, recv_dn, rank, world)
+            halo_transfer(send_dn, send_up, recv_up, recv_dn, rank, world)
             unpack(recv_up, (rank + 1) % world, 0)
             unpack(recv_dn, (rank - 1) % world, 1)
             R_T = S.halo_plan(p, J_M, rank, 0)["slab_rows"]
@@ -144,3 +157,12 @@ def test_halo_exchange_gloo(world):
         p_.join(timeout=60)
         assert p_.exitcode == 0
     assert all(n > 0 for _, n in res)
+
+
+def test_nccl_unique_id_host_only():
+    """se2m_nccl_unique_id loads NCCL through the library (dlopen, no GPU) and returns a 128-byte id."""
+    from paper_2503_02412_b200 import se2map as S
+    a, ver = S.nccl_unique_id()
+    b, _ = S.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+    assert ver >= 21800
