@@ -397,7 +397,7 @@ def main():
         wpr = (nx + 31) // 32
         n_rep = n_yaw // 2 if n_yaw % 2 == 0 else n_yaw
         own = len(m.owned_rows())                   # row-band ranks download their own rows only
-        comp = [{"risk_q": torch.empty((n_rep, own, nx), dtype=torch.int16).pin_memory(),
+        comp = [{"risk_h": torch.empty((n_rep, own, nx), dtype=torch.float16).pin_memory(),
                  "trav_bits": torch.empty((n_rep, own, wpr), dtype=torch.int32).pin_memory()} for _ in range(2)]
         ke = max(3, min(K, 8))
         with torch.cuda.stream(stream):
@@ -426,7 +426,7 @@ def main():
                "steps": ke,
                "note": "per step: H2D of the full window (--shard rows: the rank's own rows, then the NCCL halo "
                        "exchange) from pinned host memory, assess FULL, and D2H of the "
-                       "risk map (u16, 1.5e-5 resolution) + traversable bits in logical order to pinned host "
+                       "risk map (IEEE binary16: within the north_star risk tolerance of the FP32 state) + traversable bits in logical order to pinned host "
                        "memory (se2m_download_compact_rep: the n_yaw/2 representative planes, Risk being "
                        "pi-periodic in theta; the paper sends the risk map to the CPU, PAPER.md:95); D2H of step "
                        "t overlaps step t+1 on a copy stream; host wall clock to the last D2H"}
@@ -559,12 +559,31 @@ def next_rows(m, stream, torch, cfg, d_max=2.0, n_queries=1 << 20):
     q = np.stack([rng.uniform((I_M + 1) * r, (I_M + nx - 1) * r, n_queries),
                   rng.uniform((J_M + 1) * r, (J_M + ny - 1) * r, n_queries),
                   rng.uniform(-math.pi, math.pi, n_queries)], axis=1)
-    m.query_trilinear(q[:1024], 0)
-    t0 = time.perf_counter()
-    m.query_trilinear(q, 0)
-    dt = time.perf_counter() - t0
-    out["trilinear_queries_per_s"] = n_queries / dt
-    out["trilinear_note"] = "host wall clock of se2m_query_trilinear (H2D of the queries, device index math + interpolation, D2H), 1 Mi queries"
+    # NEXT-3: warmed at the timed size (staging buffers grown), CUDA events on the map's stream; device-resident
+    # queries (kernel throughput) and pinned host buffers (H2D of the queries + kernel + D2H of the answers)
+    q_pin = torch.from_numpy(q).pin_memory()
+    o_pin = torch.empty((4, n_queries), dtype=torch.float32).pin_memory()
+    q_dev = q_pin.to(f"cuda:{torch.cuda.current_device()}")
+    o_dev = torch.empty((4, n_queries), dtype=torch.float32, device=q_dev.device)
+    res = {}
+    with torch.cuda.stream(stream):
+        for name, (qi, oi) in (("device", (q_dev, o_dev)), ("host", (q_pin, o_pin))):
+            for _ in range(3):
+                m.query_trilinear_async(qi, oi, 0)
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                m.query_trilinear_async(qi, oi, 0)
+            e1.record(stream)
+            stream.synchronize()
+            res[name] = n_queries * 10 / (e0.elapsed_time(e1) * 1e-3)
+    out["trilinear_queries_per_s"] = res["device"]
+    out["trilinear_queries_per_s_host_buffers"] = res["host"]
+    out["trilinear_nan_answers"] = int(torch.isnan(o_pin[0]).sum())
+    out["trilinear_note"] = ("se2m_query_trilinear_async of 1 Mi random states (Risk field, value + gradient), CUDA "
+                             "events over 10 calls after 3 warm-up calls of the same size: device-resident queries "
+                             "(kernel) and pinned host buffers (H2D + kernel + D2H)")
     m.inpaint()                                      # NEXT-4 on the bench map (fully known: a pass over
     t0 = time.perf_counter()                         # every cell, nothing to fill)
     for _ in range(5):

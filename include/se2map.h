@@ -67,7 +67,8 @@ typedef struct {
   double robot_x, robot_y; /* initial robot position (m): window origin by Eq. 4 */
   int32_t rank, world_size;/* shard index / count (1 = single GPU) */
   int32_t device;          /* CUDA device ordinal */
-  int32_t reserved0;
+  int32_t chain_segments;  /* yaw-chain segments S (0 = auto; see se2m_chain_segments); a tuning knob: changes FP32
+                            * rounding only, results stay within the parity tolerances */
   void* cuda_stream;       /* cudaStream_t to order all work on, or NULL: the library creates one */
   /* NEXT-1 front-end (se2m_integrate_scan, readings R26-R30): */
   double fe_z_min, fe_z_max; /* body-frame height band of used points, m (default -1.5, 1.5) */
@@ -171,16 +172,18 @@ se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xyt, float* o
 /* Whole output planes in LOGICAL window order, layout [k][j][i] (n_yaw * ny * nx entries per
  * non-NULL pointer; trav as bytes 0/1).  mem says whether the output pointers are host or
  * device memory.  States this rank does not own (yaw bins or tile-row bands, see se2m_shard_plan) are
- * NaN / 0 (compact downloads: 65535 / 0).  Synchronises. */
+ * NaN / 0 (compact downloads: risk 1.0 / trav 0).  Synchronises. */
 se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, float* roll, float* z,
                           uint8_t* trav, int32_t mem);
 
 /* Compact copy of the map for planners (the paper sends the risk map to the CPU):
- * risk_q[k][j][i] = rint(risk * 65535) (u16, resolution 1.5e-5; unknown / not owned = 65535) and the
- * traversable bits re-packed in logical order, trav_bits[k][j][w] bit b = column 32 w + b
- * (ceil(nx/32) words per row, bits past nx zero).  Either pointer may be NULL; mem as in se2m_download.
- * Synchronises. */
-se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+ * risk_h[k][j][i] = the IEEE-754 binary16 bit pattern of risk (round to nearest even; relative error
+ * <= 2^-12 for risk >= 2^-14 and absolute <= 2^-25 below, so within the parity tolerance 1e-3 |risk| + 1e-6 of
+ * the FP32 state everywhere on [0, 1]; unknown / not owned = 1.0) and the traversable bits re-packed in
+ * logical order, trav_bits[k][j][w] bit b = column 32 w + b (ceil(nx/32) words per row, bits past nx zero).
+ * Either pointer may be NULL; mem as in se2m_download.  Synchronises.  (pitch, roll and z stay on the device:
+ * se2m_query / se2m_download.) */
+se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_h, uint32_t* trav_bits, int32_t mem);
 
 /* The same compact map without its redundant half: Risk and traversability are pi-periodic in theta
  * (bins k and k + n_yaw/2 have the same footprint and pitch / roll of opposite sign, and Alg. 1 uses only
@@ -190,7 +193,7 @@ se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_
  * filled ASYNCHRONOUSLY from double-buffered device staging on the map's copy stream, so the transfer
  * overlaps the next update / assess; the buffers may be read after se2m_synchronize.  Device
  * destinations are written on the map's stream. */
-se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem);
+se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_h, uint32_t* trav_bits, int32_t mem);
 /* (With row-band sharding, se2m_download_compact_rep writes only the rank's own logical rows, packed in
  * increasing order: planes of n_rows rows.)  The rank's own logical rows of the current window
  * (all ny rows unless row-band sharded): *n of them, listed in rows[] if rows is not NULL. */
@@ -293,18 +296,26 @@ se2m_status se2m_sdf_from_mask(const uint8_t* mask, int32_t nx, int32_t ny, int3
 se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double* xyt, int32_t field, float* value,
                                  float* grad);
 
+/* Asynchronous form (the planner's pipelined access): the same interpolation written to out = 4 x n floats,
+ * planar: value[n], d/dx[n], d/dy[n], d/dtheta[n] (NaN where a corner is outside / not owned).  xyt and out
+ * are host (pinned for a truly asynchronous copy) or device pointers per mem; queued on the map's stream, not
+ * synchronised (out valid after se2m_synchronize; xyt untouched until then). */
+se2m_status se2m_query_trilinear_async(se2m_map* m, int64_t n, const double* xyt, int32_t field, float* out,
+                                       int32_t mem);
+
 /* Window origin (world cell of logical (0,0)) and the owned representative-yaw range. */
 se2m_status se2m_get_origin(const se2m_map* m, int64_t* I_M, int64_t* J_M);
 
 /* Number of footprint cells |P_k| for yaw bin k (0 <= k < n_yaw) and the stencil radius R. */
 se2m_status se2m_stencil_info(const se2m_map* m, int32_t k, int32_t* n_cells, int32_t* radius);
 
-/* Yaw-chain restart period of the map: moments are carried from bin k-1 to bin k and
- * recomputed from whole footprint rows at bins k = 0 (mod period); 1 = no chain (small maps).  A state's
- * FP32 rounding depends on it; it does not depend on sharding: a yaw shard (se2m_shard_plan: the balanced
- * split [H g / G, H (g + 1) / G) of the representative bins) whose first bin lies inside a period replays the
- * chain from the period's restart without storing, so yaw-sharded maps equal the unsharded one bit for bit. */
-se2m_status se2m_chain_period(const se2m_map* m, int32_t* period);
+/* Yaw-chain segments of the map: the representative bins [0, H) are cut into S segments at the
+ * bounds floor(H s / S); moments are carried from bin k-1 to bin k inside a segment and recomputed from whole
+ * footprint rows at each bound; S = H: no chain (small maps).  A state's FP32 rounding depends on S, never on
+ * sharding: a yaw shard (se2m_shard_plan: the balanced split [H g / G, H (g + 1) / G) of the representative bins)
+ * that does not start on a bound replays the chain from its segment's bound without storing, so yaw-sharded
+ * maps equal the unsharded one bit for bit (with no replay when G divides S). */
+se2m_status se2m_chain_segments(const se2m_map* m, int32_t* segments);
 
 /* World-aligned tile of states one CTA assesses: TX columns x TY rows (SE2M_SHARD_ROWS gives world
  * tile row TJ = floor(J / TY) to rank TJ mod world_size). */

@@ -25,6 +25,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cuda_fp16.h>
+
 #include <type_traits>
 
 #include "se2m_internal.h"
@@ -510,8 +512,9 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const long long TJ = p.TJ0 + ty_rel;
   const long long li0 = TI * TX - R_T - p.I_M;  // logical (window) index of halo column 0
   const long long lj0 = TJ * TY - R_T - p.J_M;
-  const int kb = p.k_begin + blockIdx.y * p.k_chunk;
-  const int ke = min(kb + p.k_chunk, p.k_end);
+  const int s0 = seg_of(p.H, p.seg, p.k_begin) + (int)blockIdx.y * p.seg_chunk;  // this CTA's first segment
+  const int kb = max(p.k_begin, seg_bound(p.H, p.seg, s0));
+  const int ke = min(p.k_end, seg_bound(p.H, p.seg, min(p.seg, s0 + p.seg_chunk)));
   if (kb >= ke) return;
   // Vertical-window-edge tiles (the halo crosses the window's left or right edge only; they are never
   // "fast"): in MODE 1, warps own RPW tile COLUMNS each (lane = tile row), so the warps whose column band
@@ -664,7 +667,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       c.e0 = __ldg(tab_off + k) - tab_base;
       c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
       c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
-      c.restart = (b == 0 || k % p.period == 0) ? 1 : 0;
+      c.restart = (b == 0 || seg_restart(p.H, p.seg, k)) ? 1 : 0;
       c.f0 = n_chain + __ldg(p.full_off + k) - full_base;
       c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
       c.pad0 = c.pad1 = 0;
@@ -882,7 +885,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
           SYp[q] = fma2(bc(sdj), h, SYp[q]);
         }
       }
-      if (k < p.k_store) continue;  // chain replay only (a yaw shard's first period): nothing to store
+      if (k < p.k_store) continue;  // chain replay only (a yaw shard's first segment): nothing to store
       const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
       const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
       unsigned tmine = 0;
@@ -1137,8 +1140,7 @@ static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensor
     }
     configured_bytes = (int)smem;
   }
-  const int nk = p.k_end - p.k_begin;
-  dim3 grid(grid_x, (nk + p.k_chunk - 1) / p.k_chunk);
+  dim3 grid(grid_x, p.n_chunks);
   assess_kernel<R_T, MODE><<<grid, NTHREADS, smem, stream>>>(p, *tmap);
   return cudaGetLastError();
 }
@@ -1163,6 +1165,33 @@ static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMa
     if ((e = cudaStreamWaitEvent(stream, join, 0)) != cudaSuccess) return e;
   }
   return e0;
+}
+
+template <int R_T>
+static int ctas_per_sm_t(size_t smem) {
+  int n = 0;
+  cudaFuncAttributes fa;
+  // raise-only (launch_mode caches the size it configured per device)
+  if (cudaFuncGetAttributes(&fa, assess_kernel<R_T, 0>) != cudaSuccess ||
+      ((size_t)fa.maxDynamicSharedSizeBytes < smem &&
+       cudaFuncSetAttribute(assess_kernel<R_T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assess_kernel<R_T, 0>, NTHREADS, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int assess_ctas_per_sm(int R_T, size_t smem) {
+  switch (R_T) {
+    case 4: return ctas_per_sm_t<4>(smem);
+    case 8: return ctas_per_sm_t<8>(smem);
+    case 12: return ctas_per_sm_t<12>(smem);
+    case 16: return ctas_per_sm_t<16>(smem);
+    case 24: return ctas_per_sm_t<24>(smem);
+    case 32: return ctas_per_sm_t<32>(smem);
+    default: return 0;
+  }
 }
 
 size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
@@ -1327,9 +1356,11 @@ cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, flo
   return cudaGetLastError();
 }
 
-// Compact download: risk quantised to u16 (q = rint(risk * 65535), unknown = 65535) and traversable bits
-// re-packed in logical order (word w of logical row j holds logical columns 32w .. 32w+31, bit = column
-// mod 32; bits beyond nx are 0).  Bins outside [k_lo, k_hi) (not owned) read as risk 65535, trav 0.
+// Compact download: risk as IEEE-754 binary16 (round to nearest even: relative error <= 2^-12 for
+// risk >= 2^-14, absolute <= 2^-25 below — inside the north_star risk tolerance 1e-3 |risk| + 1e-6 everywhere
+// on [0, 1]; unknown = 1.0) and traversable bits re-packed in logical order (word w of logical row j holds
+// logical columns 32w .. 32w+31, bit = column mod 32; bits beyond nx are 0).  Bins outside [k_lo, k_hi)
+// (not owned) read as risk 1.0, trav 0.
 // packed = 1 (row-band sharding): output row q is the rank's q-th own logical row (own rows only, in
 // increasing order; rows_out rows per plane)
 __device__ __forceinline__ int packed_row(const AssessParams& p, int q) {
@@ -1348,7 +1379,7 @@ __device__ __forceinline__ int packed_row(const AssessParams& p, int q) {
   return (int)(J - J_M);
 }
 
-__global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, uint16_t* __restrict__ risk_q,
+__global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, uint16_t* __restrict__ risk_h,
                                       uint32_t* __restrict__ bits, int wpr, int packed, int rows_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int q = blockIdx.y;  // output row
@@ -1356,10 +1387,10 @@ __global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, 
   const int k = blockIdx.z;
   int py = p.pyM + j; if (py >= p.ny) py -= p.ny;
   const bool owned = k >= k_lo && k < k_hi && row_owned(p, j);
-  if (risk_q && i < p.nx) {
+  if (risk_h && i < p.nx) {
     int px = p.pxM + i; if (px >= p.nx) px -= p.nx;
     const float r = owned ? p.out[((size_t)k * p.ny + py) * p.nx + px].x : 1.f;
-    risk_q[((size_t)k * rows_out + q) * p.nx + i] = (uint16_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 65535.f);
+    risk_h[((size_t)k * rows_out + q) * p.nx + i] = __half_as_ushort(__float2half_rn(r));
   }
   if (bits && i < wpr) {
     uint32_t w = 0;
@@ -1379,12 +1410,12 @@ __global__ void gather_compact_kernel(const AssessParams p, int k_lo, int k_hi, 
   }
 }
 
-cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
+cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_h, uint32_t* bits,
                                   int words_per_row, cudaStream_t s, int packed_rows) {
   const int rows = packed_rows > 0 ? packed_rows : p.ny;
   if (rows <= 0) return cudaSuccess;
   dim3 grid((p.nx + 255) / 256, rows, p.n_yaw);
-  gather_compact_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk_q, bits, words_per_row, packed_rows > 0 ? 1 : 0,
+  gather_compact_kernel<<<grid, 256, 0, s>>>(p, k_lo, k_hi, risk_h, bits, words_per_row, packed_rows > 0 ? 1 : 0,
                                              rows);
   return cudaGetLastError();
 }

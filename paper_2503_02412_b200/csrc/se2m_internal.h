@@ -55,7 +55,10 @@ struct AssessParams {
   const int4* chain;
   const int* chain_off;  // [H+1]
   const int* chain_mid;  // [H]
-  int period;            // yaw-chain restart period (1 = no chain); chunks start at multiples of it
+  // yaw chain in S = seg segments: bin k restarts the chain (moments from whole footprint rows) iff k is a
+  // segment bound floor(H s / S) (seg_bound); S = H: no chain.  A CTA takes seg_chunk consecutive segments
+  // (its chunk): blockIdx.y covers segments [s0 + c y, s0 + c (y + 1)), s0 = the segment of k_begin.
+  int seg, seg_chunk, n_chunks;
   int tab_cap;           // max entries of one CTA's chunk (shared-memory table size)
   const float4* geo;     // [H] full-stencil (N, Sxx, Sxy, Syy) in cell units (Sx = Sy = 0)
   const float4* geoc;    // [H][4] full-stencil geometry for interior tiles (see assess.cu, arrow2), metres
@@ -89,9 +92,22 @@ struct AssessParams {
   int force_general;     // some full stencil is degenerate (< 3 cells or collinear): no interior fast path
 };
 
+// Yaw-chain segments (AssessParams::seg): segment s covers representative bins [seg_bound(s), seg_bound(s + 1)).
+// With S <= H every segment holds >= 1 bin; the balanced yaw shards of se2m_shard_plan, [H g / G, H (g + 1) / G),
+// start on segment bounds whenever G divides S (a shard starting elsewhere replays from its segment's bound).
+__host__ __device__ inline int seg_bound(int H, int S, int s) { return (int)((long long)H * s / S); }
+__host__ __device__ inline int seg_of(int H, int S, int k) {
+  int s = (int)((long long)k * S / H);
+  if (s + 1 <= S && seg_bound(H, S, s + 1) <= k) ++s;  // (at most one step: segments hold >= 1 bin)
+  return s;
+}
+__host__ __device__ inline bool seg_restart(int H, int S, int k) { return seg_bound(H, S, seg_of(H, S, k)) == k; }
+
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.
 // dynamic shared memory of one assess CTA (halo, prefix planes, h^ plane, run tables of tab_cap entries)
 size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk);
+// resident CTAs per SM of the main assess kernel at that dynamic shared memory (occupancy API; 0 on error)
+int assess_ctas_per_sm(int R_T, size_t smem);
 // With p.tsplit the edge-tile kernel runs on `edge` (forked from / joined into `stream` with the two
 // events); *n_launch = kernels launched.
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
@@ -135,7 +151,7 @@ cudaError_t launch_halo(const HaloArgs& a, int cap, cudaStream_t s);
 cudaError_t launch_gather_logical(const AssessParams& p, int k_lo, int k_hi, float* risk,
                                   float* pitch, float* roll, float* z, uint8_t* trav, cudaStream_t s);
 // packed_rows > 0: only the rank's own rows (row-band sharding), packed in increasing order
-cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_q, uint32_t* bits,
+cudaError_t launch_gather_compact(const AssessParams& p, int k_lo, int k_hi, uint16_t* risk_h, uint32_t* bits,
                                   int words_per_row, cudaStream_t s, int packed_rows = 0);
 // World (x, y, theta) -> ring indices, resolved on the device in FP64 exactly as readings R3/R6 state.
 struct QueryGeo {

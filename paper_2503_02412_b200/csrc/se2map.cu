@@ -69,7 +69,7 @@ struct se2m_map {
   int* d_chain_off = nullptr;
   std::vector<int> full_off, chain_off, chain_mid;
   int* d_chain_mid = nullptr;
-  int period = 1;
+  int seg = 1;  // yaw-chain segments (AssessParams::seg; H = no chain)
   float4* d_geo = nullptr;
   float4* d_geoc = nullptr;
   float2* d_cs = nullptr;
@@ -83,6 +83,8 @@ struct se2m_map {
   CUtensorMap tmap;
   bool tma_ok = false;
   int smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the device
+  int n_sm = 148;               // cudaDevAttrMultiProcessorCount of the device
+  int slots_per_sm = 0;         // resident assess CTAs per SM (occupancy API, first assess)
   // NEXT-4: nearest-neighbour inpainted view (ring layout like d_h), allocated on first use
   float* d_hin = nullptr;
   int* d_site = nullptr;
@@ -259,7 +261,7 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
       if (cur[d].y >= cur[d].x) full.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
     m->chain_off[k] = (int)chain.size();
     std::vector<int4> cells;
-    if (k % m->period == 0) {
+    if (seg_restart(m->H, m->seg, k)) {
       for (int d = 0; d < NR; ++d)
         if (cur[d].y >= cur[d].x) chain.push_back(pent(ea(d, cur[d].x), eb(d, cur[d].y), d));
     } else {
@@ -326,7 +328,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
   p.full = m->d_full; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off; p.chain_mid = m->d_chain_mid;
-  p.period = m->period;
+  p.seg = m->seg; p.seg_chunk = 1; p.n_chunks = 0;
   p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
   p.kappa_max = (float)m->prm.kappa_max; p.phi_x_max = (float)m->prm.phi_x_max; p.phi_y_max = (float)m->prm.phi_y_max;
@@ -334,7 +336,8 @@ static AssessParams make_params(const se2m_map* m) {
   p.wx = (float)(m->prm.w_r[1] / m->prm.phi_x_max);
   p.wy = (float)(m->prm.w_r[2] / m->prm.phi_y_max);
   // the launch starts at the chain restart at or before the first owned bin (replayed, not stored)
-  p.k_begin = m->k_lo - m->k_lo % std::max(1, m->period); p.k_end = m->k_hi; p.k_store = m->k_lo; p.k_chunk = 1;
+  p.k_begin = seg_bound(m->H, m->seg, seg_of(m->H, m->seg, m->k_lo)); p.k_end = m->k_hi; p.k_store = m->k_lo;
+  p.k_chunk = 1;
   p.use_tma = m->tma_ok ? 1 : 0;
   p.force_general = m->force_general ? 1 : 0;
   const bool rows = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
@@ -381,19 +384,30 @@ static se2m_status validate(const se2m_params* p) {
   if (!fe_unset && (!(p->fe_z_min < p->fe_z_max) || !(p->fe_gate > 0) || !(p->fe_ray_eps >= 0) || !(p->fe_prior_var > 0)))
     return fail(nullptr, SE2M_ERR_INVALID_ARG, "front-end params: need z_min < z_max, gate > 0, ray_eps >= 0, prior_var > 0");
   if (p->inpaint != 0 && p->inpaint != 1) return fail(nullptr, SE2M_ERR_INVALID_ARG, "inpaint must be 0 or 1");
+  if (p->chain_segments < 0) return fail(nullptr, SE2M_ERR_INVALID_ARG, "chain_segments must be >= 0");
   if (p->ellipse_ex / p->resolution > 32 || p->ellipse_ey / p->resolution > 32)
     return fail(nullptr, SE2M_ERR_UNSUPPORTED, "footprint radius > 32 cells is not built into this library");
   return SE2M_OK;
 }
 
-// Yaw-chain restart period: on maps big enough that every CTA takes all its bins, the
-// moments are carried along the bins and restart every SE2M_PERIOD bins; small maps split the bins across
-// CTAs instead (period 1).  The period does not depend on yaw sharding: a yaw shard whose first bin lies
-// inside a period replays the chain from that period's restart without storing (AssessParams::k_store),
-// so every state's FP32 arithmetic — and result — is the unsharded map's, bit for bit (pin Q13).
-static int chain_period(int H, long long cells) {
-  if (H < 18 || cells < 512LL * 512LL) return 1;
-  return SE2M_PERIOD;
+// Yaw chain: on maps big enough that every CTA takes all its bins, the moments are carried
+// along the bins in S segments (restart at each segment bound floor(H s / S)); small maps split the bins
+// across CTAs instead (S = H: no chain).  S does not depend on yaw sharding: a yaw shard whose first bin is
+// not a segment bound replays the chain from its segment's bound without storing (AssessParams::k_store), so
+// every state's FP32 arithmetic — and result — is the unsharded map's, bit for bit (pin Q13).  requested:
+// params.chain_segments (0 = auto: SE2M_SEGMENTS_LARGE_R segments for footprint radii R_T >= 16, where the
+// chain restarts are cheap next to the per-bin moments and the balanced shards of G = 2, 4, 8 ranks then
+// start on segment bounds, else SE2M_SEGMENTS segments).
+#ifndef SE2M_SEGMENTS
+#define SE2M_SEGMENTS 1        // one chain over all representative bins (A/B on the large map: DESIGN.md §7)
+#endif
+#ifndef SE2M_SEGMENTS_LARGE_R
+#define SE2M_SEGMENTS_LARGE_R 8
+#endif
+static int chain_segments(int H, long long cells, int R_T, int requested) {
+  if (H < 18 || cells < 512LL * 512LL) return H;
+  if (requested > 0) return std::min(H, requested);
+  return std::min(H, R_T >= 16 ? SE2M_SEGMENTS_LARGE_R : SE2M_SEGMENTS);
 }
 
 // Yaw shards: rank g of G owns the representative bins [H g / G, H (g + 1) / G) (balanced, contiguous).
@@ -402,26 +416,30 @@ static void yaw_share(int H, int rank, int G, int* lo, int* hi) {
   *hi = (int)((long long)H * (rank + 1) / G);
 }
 
-// The chain tables of one period must fit a CTA's shared memory next to the tile planes (the launch
-// splits the bins of a CTA only at period boundaries): large footprints fall back to shorter periods.
+// The chain tables of one segment must fit a CTA's shared memory next to the tile planes (the launch splits
+// the bins of a CTA only at segment bounds): large footprints fall back to more, shorter segments.
 // Decided against the B200 opt-in limit (227 KB) so that the host-only shard plan agrees with init.
 constexpr size_t kSmemOptinB200 = 227 * 1024;
-static void tables_for_period(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows, int P,
-                              std::vector<int4>& full, std::vector<int4>& chain) {
+static int seg_table_cap(const se2m_map* m, int s_lo, int s_hi) {  // run entries of segments [s_lo, s_hi)
+  const int kb = seg_bound(m->H, m->seg, s_lo), ke = seg_bound(m->H, m->seg, s_hi);
+  const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
+  return std::max(1, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
+}
+static void tables_for_segments(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows, int S,
+                                std::vector<int4>& full, std::vector<int4>& chain) {
   for (;;) {
-    m->period = P;
+    m->seg = S;
     full.clear();
     chain.clear();
     build_tables(m, runs, nrows, full, chain);
-    if (P <= 1) return;
-    int cap = 1;
-    for (int kb = 0; kb < m->H; kb += P) {
-      const int ke = std::min(kb + P, m->H);
-      const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
-      cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
+    if (S >= m->H) return;
+    int cap = 1, bins = 1;
+    for (int q = 0; q < S; ++q) {
+      cap = std::max(cap, seg_table_cap(m, q, q + 1));
+      bins = std::max(bins, seg_bound(m->H, S, q + 1) - seg_bound(m->H, S, q));
     }
-    if (assess_smem_bytes(m->R_T, cap, P) <= kSmemOptinB200) return;
-    P = P > 9 ? 9 : P - 1;
+    if (assess_smem_bytes(m->R_T, cap, bins) <= kSmemOptinB200) return;
+    S = std::min(m->H, 2 * S);
   }
 }
 
@@ -544,7 +562,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
   }
   const bool yaw_sharded = p->shard_mode == SE2M_SHARD_YAW && p->world_size > 1;
   std::vector<int4> full, chain;
-  tables_for_period(m, runs, nrows, chain_period(m->H, (long long)p->nx * p->ny), full, chain);
+  tables_for_segments(m, runs, nrows, chain_segments(m->H, (long long)p->nx * p->ny, m->R_T, p->chain_segments), full,
+                      chain);
   if (yaw_sharded) yaw_share(m->H, p->rank, p->world_size, &m->k_lo, &m->k_hi);
   // Eq. 4 (reading R6/R7): window origin = floor(x/r) - nx/2 in IEEE double
   m->I_M = (long long)floor(p->robot_x / p->resolution) - p->nx / 2;
@@ -607,6 +626,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     int optin = 0;
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device) == cudaSuccess && optin > 0)
       m->smem_optin = optin;
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device) == cudaSuccess && nsm > 0) m->n_sm = nsm;
   }
   *out = m;
   return SE2M_OK;
@@ -864,34 +885,47 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   const int grid_rows = tiles_y > p.row_first ? (tiles_y - p.row_first + p.row_mod - 1) / p.row_mod : 0;
   const int n_tiles = p.tiles_x * grid_rows;
   // yaw chunking: all bins per CTA (tile reuse) unless that leaves SMs idle; then split the bins so the
-  // CTAs fill one wave (2 resident CTAs on each of the 148 SMs) — each CTA pays the tile load, plane fit
-  // and prefix build once, so more, shorter CTAs than that only add fixed cost
-  const int kbeg = p.k_begin;  // chain restart at or before k_lo
-  const int nk = m->k_hi - kbeg;
-  int chunk = nk;
-  if (n_tiles > 0) {
-    const long long slots = 2LL * 148;
-    chunk = (int)std::max<long long>(1, std::min<long long>(nk, ((long long)n_tiles * nk + slots - 1) / slots));
-  }
-  chunk = std::max(1, chunk);
-  if (m->period > 1) chunk = std::min(nk, (chunk + m->period - 1) / m->period * m->period);  // chain-aligned
-  // run tables of a chunk must fit the CTA's shared memory next to the tile planes: large footprints take
-  // fewer bins per CTA (whole chain periods)
-  int cap = 1;
-  for (;;) {
-    cap = 1;
-    for (int kb = kbeg; kb < m->k_hi; kb += chunk) {
-      const int ke = std::min(kb + chunk, m->k_hi);
+  // CTAs fill one wave (the device's SMs x the kernel's resident CTAs per SM) — each CTA pays the tile
+  // load, plane fit and prefix build once, so more, shorter CTAs than that only add fixed cost.  Chunks are
+  // whole chain segments (AssessParams::seg): segments [s_a, s_b) cover the launch's bins [k_begin, k_hi).
+  const int H = m->H, S = m->seg;
+  const int s_a = seg_of(H, S, p.k_begin);
+  const int s_b = m->k_hi > p.k_begin ? seg_of(H, S, m->k_hi - 1) + 1 : s_a;
+  const int n_seg = s_b - s_a;
+  const int nk = m->k_hi - p.k_begin;
+  // run tables (and bins) of the largest chunk of c segments: they must fit the CTA's shared memory
+  auto chunk_need = [&](int c, int* cap_out, int* bins_out) {
+    int cap = 1, bins = 1;
+    for (int q = s_a; q < s_b; q += c) {
+      const int kb = std::max(p.k_begin, seg_bound(H, S, q)), ke = std::min(m->k_hi, seg_bound(H, S, std::min(S, q + c)));
       const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off[ke] - m->chain_off[kb];
       cap = std::max(cap, chain_border(m->R_T) ? nf + nc : std::max(nf, nc));
+      bins = std::max(bins, ke - kb);
     }
-    const int step = m->period > 1 ? m->period : 1;
-    if (assess_smem_bytes(m->R_T, cap, chunk) <= (size_t)m->smem_optin || chunk <= step) break;
-    chunk = std::max(step, (chunk / 2 + step - 1) / step * step);
+    *cap_out = cap;
+    *bins_out = bins;
+    return assess_smem_bytes(m->R_T, cap, bins);
+  };
+  if (m->slots_per_sm <= 0 && n_seg > 0) {  // resident CTAs per SM at the whole-range chunk (occupancy API, once)
+    int cap0, bins0;
+    const size_t sm_full = chunk_need(n_seg, &cap0, &bins0);
+    m->slots_per_sm = sm_full <= (size_t)m->smem_optin ? assess_ctas_per_sm(m->R_T, sm_full) : 0;
+    if (m->slots_per_sm <= 0) m->slots_per_sm = 2;  // (launch bounds: 2 CTAs of 256 threads per SM)
   }
-  if (assess_smem_bytes(m->R_T, cap, chunk) > (size_t)m->smem_optin)
+  int c = std::max(1, n_seg);
+  if (n_tiles > 0 && n_seg > 0) {
+    const long long slots = (long long)m->n_sm * m->slots_per_sm;
+    const long long want_bins = std::max<long long>(1, ((long long)n_tiles * nk + slots - 1) / slots);
+    c = (int)std::max<long long>(1, std::min<long long>(n_seg, (want_bins * n_seg + nk - 1) / nk));
+  }
+  // large footprints take fewer segments per CTA when the tables do not fit
+  int cap = 1, bins = 1;
+  while (chunk_need(c, &cap, &bins) > (size_t)m->smem_optin && c > 1) c = (c + 1) / 2;
+  if (chunk_need(c, &cap, &bins) > (size_t)m->smem_optin)
     return fail(m, SE2M_ERR_UNSUPPORTED, "assess: footprint tables exceed the shared memory of a CTA");
-  p.k_chunk = chunk;
+  p.seg_chunk = c;
+  p.n_chunks = (n_seg + c - 1) / c;
+  p.k_chunk = bins;
   p.tab_cap = cap;
   // vertical-window-edge tile columns (the halo crosses the window's left / right edge): their tiles run
   // in the column-major layout kernel on the edge stream, concurrently (tile_rows == 32 footprints only)
@@ -916,7 +950,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
       p.n_tcols = 0;
     }
   }
-  if (n_tiles > 0 && nk > 0 && m->k_hi > m->k_lo) {
+  if (n_tiles > 0 && n_seg > 0 && m->k_hi > m->k_lo) {
     int nl = 0;
     cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
@@ -1027,9 +1061,9 @@ extern "C" se2m_status se2m_nccl_unique_id(void* out, int32_t bytes, int32_t* ve
   return SE2M_OK;
 }
 
-extern "C" se2m_status se2m_chain_period(const se2m_map* m, int32_t* period) {
-  if (!m || !period) return SE2M_ERR_INVALID_ARG;
-  *period = m->period;
+extern "C" se2m_status se2m_chain_segments(const se2m_map* m, int32_t* segments) {
+  if (!m || !segments) return SE2M_ERR_INVALID_ARG;
+  *segments = m->seg;
   return SE2M_OK;
 }
 
@@ -1168,19 +1202,19 @@ extern "C" se2m_status se2m_download(se2m_map* m, float* risk, float* pitch, flo
   return SE2M_OK;
 }
 
-extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
+extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_h, uint32_t* trav_bits, int32_t mem) {
   SE2M_ENTER(m);
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact: bad mem");
   const int wpr = (m->prm.nx + 31) / 32;
   const size_t nst = (size_t)m->prm.nx * m->prm.ny * m->prm.n_yaw;
-  const size_t rb = risk_q ? nst * 2 : 0, bb = trav_bits ? (size_t)m->prm.n_yaw * m->prm.ny * wpr * 4 : 0;
+  const size_t rb = risk_h ? nst * 2 : 0, bb = trav_bits ? (size_t)m->prm.n_yaw * m->prm.ny * wpr * 4 : 0;
   if (!rb && !bb) return SE2M_OK;
-  uint16_t* dr = risk_q;
+  uint16_t* dr = risk_h;
   uint32_t* db = trav_bits;
   if (mem == SE2M_MEM_HOST) {
     se2m_status st = ensure_stage(m, rb + bb);
     if (st != SE2M_OK) return st;
-    dr = risk_q ? reinterpret_cast<uint16_t*>(m->d_stage) : nullptr;
+    dr = risk_h ? reinterpret_cast<uint16_t*>(m->d_stage) : nullptr;
     db = trav_bits ? reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(m->d_stage) + rb) : nullptr;
   }
   AssessParams p = make_params(m);
@@ -1203,7 +1237,7 @@ extern "C" se2m_status se2m_download_compact(se2m_map* m, uint16_t* risk_q, uint
     }
   }
   if (mem == SE2M_MEM_HOST) {
-    if (risk_q) CUDA_TRY(m, cudaMemcpyAsync(risk_q, dr, rb, cudaMemcpyDeviceToHost, m->stream), "D2H risk_q");
+    if (risk_h) CUDA_TRY(m, cudaMemcpyAsync(risk_h, dr, rb, cudaMemcpyDeviceToHost, m->stream), "D2H risk_h");
     if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->stream), "D2H bits");
   }
   CUDA_TRY(m, cudaStreamSynchronize(m->stream), "sync(download_compact)");
@@ -1231,7 +1265,7 @@ extern "C" se2m_status se2m_owned_rows(const se2m_map* m, int32_t* rows, int32_t
   return SE2M_OK;
 }
 
-extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, uint32_t* trav_bits, int32_t mem) {
+extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_h, uint32_t* trav_bits, int32_t mem) {
   SE2M_ENTER(m);
   if (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE) return fail(m, SE2M_ERR_INVALID_ARG, "download_compact_rep: bad mem");
   const int wpr = (m->prm.nx + 31) / 32;
@@ -1240,13 +1274,13 @@ extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, 
   const bool packed = m->prm.shard_mode == SE2M_SHARD_ROWS && m->prm.world_size > 1;
   const int rows = packed ? owned_rows(m, nullptr) : m->prm.ny;
   const size_t plane = (size_t)m->prm.nx * rows;
-  const size_t rb = risk_q ? plane * n_rep * 2 : 0, bb = trav_bits ? (size_t)n_rep * rows * wpr * 4 : 0;
+  const size_t rb = risk_h ? plane * n_rep * 2 : 0, bb = trav_bits ? (size_t)n_rep * rows * wpr * 4 : 0;
   if (!rb && !bb) return SE2M_OK;
   AssessParams p = make_params(m);
   p.n_yaw = n_rep;  // planes [0, n_rep): the representative bins (or all bins when n_yaw is odd)
-  const int klo = m->k_lo, khi = m->k_hi;  // owned representative bins (others: 65535 / 0)
+  const int klo = m->k_lo, khi = m->k_hi;  // owned representative bins (others: risk 1.0 / trav 0)
   if (mem == SE2M_MEM_DEVICE) {
-    CUDA_TRY(m, launch_gather_compact(p, klo, khi, risk_q, trav_bits, wpr, m->stream, packed ? rows : 0),
+    CUDA_TRY(m, launch_gather_compact(p, klo, khi, risk_h, trav_bits, wpr, m->stream, packed ? rows : 0),
              "gather_compact");
     m->launches++;
     return SE2M_OK;
@@ -1271,7 +1305,7 @@ extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, 
   }
   const int b = m->rep_slot;
   m->rep_slot ^= 1;
-  uint16_t* dr = risk_q ? reinterpret_cast<uint16_t*>(m->d_rep[b]) : nullptr;
+  uint16_t* dr = risk_h ? reinterpret_cast<uint16_t*>(m->d_rep[b]) : nullptr;
   uint32_t* db = trav_bits ? reinterpret_cast<uint32_t*>(m->d_rep[b] + rb) : nullptr;
   // staging b is reused only after its previous D2H finished; the D2H waits for the gather
   CUDA_TRY(m, cudaStreamWaitEvent(m->stream, m->ev_copied[b], 0), "wait(copied)");
@@ -1279,7 +1313,7 @@ extern "C" se2m_status se2m_download_compact_rep(se2m_map* m, uint16_t* risk_q, 
   m->launches++;
   CUDA_TRY(m, cudaEventRecord(m->ev_gathered[b], m->stream), "record(gathered)");
   CUDA_TRY(m, cudaStreamWaitEvent(m->copy_stream, m->ev_gathered[b], 0), "wait(gathered)");
-  if (risk_q) CUDA_TRY(m, cudaMemcpyAsync(risk_q, dr, rb, cudaMemcpyDeviceToHost, m->copy_stream), "D2H risk_q");
+  if (risk_h) CUDA_TRY(m, cudaMemcpyAsync(risk_h, dr, rb, cudaMemcpyDeviceToHost, m->copy_stream), "D2H risk_h");
   if (trav_bits) CUDA_TRY(m, cudaMemcpyAsync(trav_bits, db, bb, cudaMemcpyDeviceToHost, m->copy_stream), "D2H bits");
   CUDA_TRY(m, cudaEventRecord(m->ev_copied[b], m->copy_stream), "record(copied)");
   return SE2M_OK;
@@ -1515,6 +1549,27 @@ extern "C" se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double
     }
   return n_out ? fail(m, SE2M_ERR_OUT_OF_RANGE, "query_trilinear: some corners outside the window / not owned")
                : SE2M_OK;
+}
+
+extern "C" se2m_status se2m_query_trilinear_async(se2m_map* m, int64_t n, const double* xyt, int32_t field, float* out,
+                                                  int32_t mem) {
+  SE2M_ENTER(m);
+  if (n < 0 || (n > 0 && (!xyt || !out)) || n > (1ll << 30) || (field != 0 && field != 1) ||
+      (mem != SE2M_MEM_HOST && mem != SE2M_MEM_DEVICE))
+    return fail(m, SE2M_ERR_INVALID_ARG, "query_trilinear_async: bad n / pointers / field / mem");
+  if (field == 1 && !m->sdf_valid) return fail(m, SE2M_ERR_STATE, "query_trilinear_async: no SDF (call se2m_compute_sdf)");
+  if (n == 0) return SE2M_OK;
+  se2m_status st = stage_queries(m, n, xyt);
+  if (st != SE2M_OK) return st;
+  const float* f = field == 0 ? reinterpret_cast<const float*>(m->d_out) : m->d_sdf;
+  float* dst = mem == SE2M_MEM_DEVICE ? out : m->d_qout;
+  CUDA_TRY(m, launch_trilinear(f, field == 0 ? 4 : 1, field, query_geo(m), (int)n, m->d_qxyt, dst, m->d_qcnt, m->stream),
+           "trilinear kernel");
+  m->launches++;
+  if (mem == SE2M_MEM_HOST)
+    CUDA_TRY(m, cudaMemcpyAsync(out, m->d_qout, (size_t)n * 4 * sizeof(float), cudaMemcpyDeviceToHost, m->stream),
+             "D2H trilinear");
+  return SE2M_OK;
 }
 
 // SDF planes in logical order: out[k][j][i] for all n_yaw bins (bins k and k + n/2 share a layer).

@@ -33,7 +33,8 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_query_trilinear", "se2m_integrate_scan", "se2m_download_elevation", "se2m_inpaint",
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
            "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
-           "se2m_chain_period", "se2m_query_async", "se2m_exchange_halo", "se2m_nccl_unique_id"]
+           "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo", "se2m_nccl_unique_id",
+           "se2m_query_trilinear_async"]
 
 
 class Params(ctypes.Structure):
@@ -44,7 +45,7 @@ class Params(ctypes.Structure):
                 ("phi_x_max", ctypes.c_double), ("phi_y_max", ctypes.c_double),
                 ("robot_x", ctypes.c_double), ("robot_y", ctypes.c_double),
                 ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
+                ("chain_segments", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("fe_z_min", ctypes.c_double), ("fe_z_max", ctypes.c_double), ("fe_gate", ctypes.c_double),
                 ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double),
                 ("inpaint", ctypes.c_int32), ("reserved1", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
@@ -97,13 +98,14 @@ _lib.se2m_download_inpainted.argtypes = [_vp, _vp, _i32]
 _lib.se2m_tile_info.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_shard_plan.argtypes = [ctypes.POINTER(Params)] + [ctypes.POINTER(_i32)] * 6
 _lib.se2m_query_async.argtypes = [_vp, _i64, _vp, _vp, _i32]
-_lib.se2m_chain_period.argtypes = [_vp, ctypes.POINTER(_i32)]
+_lib.se2m_chain_segments.argtypes = [_vp, ctypes.POINTER(_i32)]
 _lib.se2m_halo_size.argtypes = [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]
 _lib.se2m_halo_pack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_unpack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_plan.argtypes = [ctypes.POINTER(Params), _i64, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                 _vp]
 _lib.se2m_exchange_halo.argtypes = [_vp]
+_lib.se2m_query_trilinear_async.argtypes = [_vp, _i64, _vp, _i32, _vp, _i32]
 _lib.se2m_nccl_unique_id.argtypes = [_vp, _i32, ctypes.POINTER(_i32)]
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
@@ -114,8 +116,8 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_shard_plan", "se2m_download_compact", "se2m_compute_sdf", "se2m_download_sdf",
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
-              "se2m_halo_plan", "se2m_chain_period", "se2m_query_async", "se2m_exchange_halo",
-              "se2m_nccl_unique_id"):
+              "se2m_halo_plan", "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo",
+              "se2m_nccl_unique_id", "se2m_query_trilinear_async"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -178,6 +180,25 @@ def _ptr_nocopy(a):
     if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
         return a.data_ptr(), (SE2M_MEM_DEVICE if a.is_cuda else SE2M_MEM_HOST), a
     return a.ctypes.data, SE2M_MEM_HOST, a
+
+
+def _check_async_buffers(xyt, out, rows):
+    """Asynchronous calls read xyt and write out after the call returned, so nothing may be converted or copied
+    here (a temporary would be freed first): validate instead — xyt (n, 3) float64 C-contiguous, out (rows, n)
+    float32 C-contiguous, both host or both device."""
+    def desc(a):
+        if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):
+            return str(a.dtype).replace("torch.", ""), tuple(a.shape), a.is_contiguous(), a.is_cuda
+        return str(a.dtype), tuple(a.shape), bool(a.flags["C_CONTIGUOUS"]), False
+    dx, sx, cx, gx = desc(xyt)
+    do, so, co, go = desc(out)
+    n = sx[0] if len(sx) == 2 else -1
+    if dx != "float64" or len(sx) != 2 or sx[1] != 3 or not cx:
+        raise ValueError("xyt must be a C-contiguous (n, 3) float64 array")
+    if do != "float32" or so != (rows, n) or not co:
+        raise ValueError("out must be a C-contiguous (%d, n) float32 array" % rows)
+    if gx != go:
+        raise ValueError("xyt and out must both be host or both be device memory")
 
 
 def shard_plan(params: Params) -> dict:
@@ -320,12 +341,10 @@ class Se2Map:
         """Queue the lookups of xyt (n x 3 float64: pinned host tensor / NumPy view of one, or CUDA tensor)
         into out (5 x n float32, same memory kind: risk, pitch, roll, z, trav as rows); valid after
         synchronize().  Both buffers must stay alive and untouched until then."""
-        n = xyt.shape[0]
+        _check_async_buffers(xyt, out, 5)
         xp, mem, _ = _ptr_nocopy(xyt)
-        op, mem2, _ = _ptr_nocopy(out)
-        if mem != mem2 or tuple(out.shape) != (5, n):
-            raise ValueError("xyt and out: same memory kind, out of shape (5, n)")
-        return self._check(_lib.se2m_query_async(self.h, n, xp, op, mem))
+        op, _, _ = _ptr_nocopy(out)
+        return self._check(_lib.se2m_query_async(self.h, xyt.shape[0], xp, op, mem))
 
     def download(self, planes=("risk", "pitch", "roll", "z", "trav"), out=None):
         """Whole planes in logical [k][j][i] order as NumPy arrays (or into ``out`` dict of arrays/tensors)."""
@@ -350,17 +369,17 @@ class Se2Map:
         return res
 
     def download_compact(self, out=None):
-        """(risk_q u16 [k][j][i], trav bits u32 [k][j][ceil(nx/32)]) in logical order (host NumPy by default)."""
+        """(risk_h float16 [k][j][i], trav bits u32 [k][j][ceil(nx/32)]) in logical order (host NumPy by default)."""
         P = self.params
         wpr = (P.nx + 31) // 32
         if out is None:
-            out = {"risk_q": np.empty((P.n_yaw, P.ny, P.nx), np.uint16),
+            out = {"risk_h": np.empty((P.n_yaw, P.ny, P.nx), np.float16),
                    "trav_bits": np.empty((P.n_yaw, P.ny, wpr), np.uint32)}
-        rp, mem, k1 = _ptr_nocopy(out.get("risk_q"))
+        rp, mem, k1 = _ptr_nocopy(out.get("risk_h"))
         bp, mem2, k2 = _ptr_nocopy(out.get("trav_bits"))
-        if out.get("risk_q") is not None and out.get("trav_bits") is not None and mem != mem2:
+        if out.get("risk_h") is not None and out.get("trav_bits") is not None and mem != mem2:
             raise ValueError("both outputs must be host or both device")
-        mem = mem if out.get("risk_q") is not None else mem2
+        mem = mem if out.get("risk_h") is not None else mem2
         self._check(_lib.se2m_download_compact(self.h, rp, bp, mem))
         return out
 
@@ -381,13 +400,13 @@ class Se2Map:
         wpr = (P.nx + 31) // 32
         if out is None:
             rows = len(self.owned_rows())
-            out = {"risk_q": np.empty((n_rep, rows, P.nx), np.uint16),
+            out = {"risk_h": np.empty((n_rep, rows, P.nx), np.float16),
                    "trav_bits": np.empty((n_rep, rows, wpr), np.uint32)}
-        rp, mem, k1 = _ptr_nocopy(out.get("risk_q"))
+        rp, mem, k1 = _ptr_nocopy(out.get("risk_h"))
         bp, mem2, k2 = _ptr_nocopy(out.get("trav_bits"))
-        if out.get("risk_q") is not None and out.get("trav_bits") is not None and mem != mem2:
+        if out.get("risk_h") is not None and out.get("trav_bits") is not None and mem != mem2:
             raise ValueError("both outputs must be host or both device")
-        mem = mem if out.get("risk_q") is not None else mem2
+        mem = mem if out.get("risk_h") is not None else mem2
         self._check(_lib.se2m_download_compact_rep(self.h, rp, bp, mem))
         return out
 
@@ -409,6 +428,15 @@ class Se2Map:
         st = _lib.se2m_query_trilinear(self.h, n, xyt.ctypes.data, field, v.ctypes.data, g.ctypes.data)
         self._check(st, ok=(SE2M_OK, SE2M_ERR_OUT_OF_RANGE))
         return v, g, st
+
+    def query_trilinear_async(self, xyt, out, field: int = 0):
+        """Queue trilinear lookups of xyt (n x 3 float64, C-contiguous: pinned host tensor / NumPy view of one, or
+        CUDA tensor) into out (4 x n float32, same memory kind: value, d/dx, d/dy, d/dtheta); valid after
+        synchronize().  Both buffers must stay alive and untouched until then."""
+        _check_async_buffers(xyt, out, 4)
+        xp, mem, _ = _ptr_nocopy(xyt)
+        op, _, _ = _ptr_nocopy(out)
+        return self._check(_lib.se2m_query_trilinear_async(self.h, xyt.shape[0], xp, field, op, mem))
 
     def integrate_scan(self, points, pose: Pose):
         """NEXT-1: one LiDAR frame (points (n, 3) float32 sensor frame: NumPy host or CUDA tensor).
@@ -459,10 +487,10 @@ class Se2Map:
     def synchronize(self):
         return self._check(_lib.se2m_synchronize(self.h))
 
-    def chain_period(self) -> int:
-        """Yaw-chain restart period (1 = no chain)."""
+    def chain_segments(self) -> int:
+        """Yaw-chain segments S (S = n_rep: no chain)."""
         v = _i32()
-        self._check(_lib.se2m_chain_period(self.h, ctypes.byref(v)))
+        self._check(_lib.se2m_chain_segments(self.h, ctypes.byref(v)))
         return v.value
 
     # -- row-band halo exchange (SE2M_SHARD_ROWS, world_size > 1) ----------------------------------

@@ -139,8 +139,8 @@ def test_highres_yaw_slices_equal_single(G):
     single = make_map(nx, ny, r, n_yaw, robot=robot)
     maps = [make_map(nx, ny, r, n_yaw, robot=robot, shard_mode=1, rank=g, world_size=G) for g in range(G)]
     try:
-        period = single.chain_period()
-        assert all(m.chain_period() == period for m in maps)
+        period = single.chain_segments()
+        assert all(m.chain_segments() == period for m in maps)
         I_M, J_M = single.origin()
         margin = 30
         world = world_heights(cfg["terrain"], I_M - margin, J_M - margin, nx + 2 * margin, ny + 2 * margin, r)

@@ -110,15 +110,15 @@ def test_sharded_equals_single(mode, G):
         # states the rank does not own come back as NaN / 0 (downloads never expose stale records)
         assert np.all(np.isnan(g["risk"][~mask])) and np.all(g["trav"][~mask] == 0)
         c = m.download_compact()
-        assert np.all(c["risk_q"][~mask] == 65535)
+        assert np.all(c["risk_h"][~mask] == 1.0)
         if mode == 2:  # the planner copy of a row-band rank: its own rows only, packed
             rows = m.owned_rows()
             assert np.array_equal(rows, np.nonzero(own_rows)[0])
             rep_ = m.download_compact_rep()
             m.synchronize()
             H2 = n_yaw // 2
-            assert rep_["risk_q"].shape == (H2, len(rows), nx)
-            assert np.array_equal(rep_["risk_q"], c["risk_q"][:H2][:, rows, :])
+            assert rep_["risk_h"].shape == (H2, len(rows), nx)
+            assert np.array_equal(rep_["risk_h"], c["risk_h"][:H2][:, rows, :])
             assert np.array_equal(rep_["trav_bits"], c["trav_bits"][:H2][:, rows, :])
     assert _equal(merged, ref)
 
@@ -160,7 +160,7 @@ def test_chain_map_incremental_and_sharded(n_yaw):
             periods = set()
             for rank in range(G):
                 m = make_map(nx, ny, r, n_yaw, robot=(2.2, -1.05), shard_mode=mode, rank=rank, world_size=G)
-                periods.add(m.chain_period())
+                periods.add(m.chain_segments())
                 m.update_elevation(h)
                 m.assess_se2(0)
                 g = m.download()
@@ -179,7 +179,7 @@ def test_chain_map_incremental_and_sharded(n_yaw):
                     merged[f][mask] = g[f][mask]
             # sharding never changes the chain period: a yaw shard starting inside a period replays the
             # chain from its restart, so the merged shards equal the single map bit for bit (pin Q13)
-            assert periods == {single.chain_period()}
+            assert periods == {single.chain_segments()}
             assert _equal(merged, ref), (mode, G)
     # and parity with the oracle on the sample
     rep = compare({f: ref[f][ijk[:, 2], ijk[:, 1], ijk[:, 0]] for f in ref}, orc)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--holes", type=float, default=0.0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--sdf", type=float, default=0.0, help="also time compute_sdf(d_max) after the assess")
+    ap.add_argument("--segments", type=int, default=0, help="params.chain_segments (0 = auto)")
     ap.add_argument("--scan", action="store_true",
                     help="the bench's paper_pipeline map instead: 180x180x30 built from 4 LiDAR frames")
     a = ap.parse_args()
@@ -51,7 +52,7 @@ def main():
             for dj in (-1, 0, 1):
                 known[cj + dj, ci + di] = 0
     m = Se2Map(nx=nx, ny=ny, n_yaw=c["n_yaw"], resolution=r, ellipse_ex=c["ex"], ellipse_ey=c["ey"],
-               robot_x=x, robot_y=y)
+               robot_x=x, robot_y=y, chain_segments=a.segments)
     m.update_elevation(h, known)
     m.assess_se2(0)
     m.synchronize()
@@ -61,7 +62,7 @@ def main():
         m.assess_se2(0)
         m.synchronize()
         ts.append(time.perf_counter() - t)
-    res = dict(config=a.config, holes=a.holes, unknown_frac=0.0 if known is None else float(1 - known.mean()),
+    res = dict(config=a.config, holes=a.holes, segments=m.chain_segments(), unknown_frac=0.0 if known is None else float(1 - known.mean()),
                ms_median=1e3 * float(np.median(ts)), ms_min=1e3 * float(np.min(ts)))
     if a.sdf > 0:
         m.compute_sdf(a.sdf)

@@ -42,6 +42,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--configs", default="large,highres")
+    ap.add_argument("--segments", type=int, default=0, help="params.chain_segments (0 = auto)")
     a = ap.parse_args()
     from paper_2503_02412_b200 import se2map as S
     stream = torch.cuda.Stream()
@@ -59,14 +60,15 @@ def main():
             for g in range(G):
                 kw2 = dict(kw, rank=g) if G > 1 else {}
                 maps.append(S.Se2Map(nx=nx, ny=ny, n_yaw=n_yaw, resolution=r, robot_x=c["robot"][0],
-                                     robot_y=c["robot"][1], cuda_stream=stream.cuda_stream, **kw2))
+                                     robot_y=c["robot"][1], cuda_stream=stream.cuda_stream,
+                                     chain_segments=a.segments, **kw2))
             if h is None:
                 I_M, J_M = maps[0].origin()
                 h = world_heights(c["terrain"], I_M, J_M, nx, ny, r)
             for m in maps:
                 m.update_elevation(h)           # (timing only: every rank gets the whole window)
             ms = [time_assess(m, stream, a.reps) for m in maps]
-            out[G] = {"rank_ms": ms, "max_ms": max(ms), "balance_eff": None}
+            out[G] = {"rank_ms": ms, "max_ms": max(ms), "balance_eff": None, "segments": maps[0].chain_segments()}
             for m in maps:
                 m.close()
             torch.cuda.empty_cache()
