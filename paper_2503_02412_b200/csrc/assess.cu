@@ -448,6 +448,17 @@ struct BinC {
   float4 gq;                  // (Gq1, Gq2, aG1, aG2): the tile plane's gradient in the bin's eigenbasis
 };
 
+#ifndef SE2M_TABG_MIN_R
+#define SE2M_TABG_MIN_R 16
+#endif
+// a run-table entry: shared memory, or (TG) global memory through the read-only path
+template <bool TG>
+__device__ __forceinline__ int4 ld_entry(const int4* e) { return TG ? __ldg(e) : *e; }
+
+// State s of a thread sits so_of(s) tile rows (T-mode: columns) after its first one: pairs of neighbouring
+// rows spread 2 NWARPS apart, so every warp holds states in every part of the tile (see the kernel).
+__host__ __device__ constexpr int so_of(int s) { return (s & 1) + (s >> 1) * 2 * NWARPS; }
+
 template <int R_T>
 struct Geom {
   static constexpr int TY = tile_rows(R_T);
@@ -469,7 +480,16 @@ struct Geom {
   static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
   // then the per-bin constants of the CTA's chunk (BinC: table offsets + interior geometry), so the
   // bin loop reads them with broadcast LDS instead of waiting on global loads at every bin
-  static size_t bytes(int tab_cap, int k_chunk) { return runs_off + (size_t)tab_cap * 16 + (size_t)k_chunk * sizeof(BinC); }
+  // then (T-mode tiles) the traversable words of the chunk: k_chunk x 32 rows
+  // TG: large footprints (R_T >= SE2M_TABG_MIN_R) read the run tables from global memory (L1-cached, warp-
+  // uniform loads) instead of staging them in shared memory, so that two CTAs fit an SM (R_T = 16: 100 KB of
+  // tile planes; the tables of a 36-bin chunk would add ~30 KB)
+  static constexpr bool TG = R_T >= SE2M_TABG_MIN_R;
+  static constexpr bool TMODE = TY == 32 && TX == 32 && CB;  // a T-mode (column-major) edge kernel exists
+  static size_t bytes(int tab_cap, int k_chunk) {
+    return runs_off + (TG ? 0 : (size_t)tab_cap * 16) +
+           (size_t)k_chunk * (sizeof(BinC) + (TMODE ? 32 * sizeof(uint32_t) : 0));
+  }
 };
 
 // MODE 0: every tile of the grid (except, with p.tsplit, the vertical-window-edge tiles); MODE 1: only
@@ -490,7 +510,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
   float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
-  BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (size_t)p.tab_cap * 16);
+  BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (G::TG ? 0 : (size_t)p.tab_cap * 16));
+  uint32_t* twd = reinterpret_cast<uint32_t*>(bins_s + p.k_chunk);  // T-mode: [bin][row] traversable words
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // MODE 1 runs the tile columns p.tcols[0 .. n_tcols) of every grid row
@@ -542,17 +563,25 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       tma_load_2d(raw, &tmap, bar, bx, by);
     }
   } else {
-    for (int idx = tid; idx < HX * HY; idx += NTHREADS) {
+    // all of a thread's loads are issued before any is consumed (one global-latency wait instead of one per
+    // element: window-edge / seam tiles, and every tile of a small map, load this way)
+    constexpr int NLD = (HX * HY + NTHREADS - 1) / NTHREADS;
+    float v[NLD];
+#pragma unroll
+    for (int q = 0; q < NLD; ++q) {
+      const int idx = tid + q * NTHREADS;
       const int row = idx / HX, col = idx - row * HX;
       const long long li = li0 + col, lj = lj0 + row;
-      float v = __int_as_float(0x7fc00000);
-      if (li >= 0 && li < p.nx && lj >= 0 && lj < p.ny) {
+      v[q] = __int_as_float(0x7fc00000);
+      if (idx < HX * HY && li >= 0 && li < p.nx && lj >= 0 && lj < p.ny) {
         int px = p.pxM + (int)li; if (px >= p.nx) px -= p.nx;
         int py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny;
-        v = __ldg(p.h + (size_t)py * p.ldh + px);
+        v[q] = __ldg(p.h + (size_t)py * p.ldh + px);
       }
-      raw[idx] = v;
     }
+#pragma unroll
+    for (int q = 0; q < NLD; ++q)
+      if (tid + q * NTHREADS < HX * HY) raw[tid + q * NTHREADS] = v[q];
   }
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
@@ -651,13 +680,15 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const int tab_base = __ldg(tab_off + kb);
   const int n_chain = (fast || G::CB) ? __ldg(tab_off + ke) - tab_base : 0;
   const int full_base = __ldg(p.full_off + kb);
-  for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
-  if (!fast) {
-    for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS) {
-      const int4 e = __ldg(p.full + full_base + idx);
-      runs_s[n_chain + idx] = make_int4(e.x * 8, e.y * 8, e.x * 4, __float_as_int((float)(e.z - R_T)));
-    }
+  if (!G::TG) {
+    for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
+    if (!fast)
+      for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS)
+        runs_s[n_chain + idx] = __ldg(p.full_fmt + full_base + idx);
   }
+  // the chunk's chain entries and full-row entries (shared memory, or global memory for TG)
+  const int4* tabc = G::TG ? p.chain + tab_base : runs_s;
+  const int4* tabf = G::TG ? p.full_fmt + full_base : runs_s + n_chain;
 
   {  // per-bin constants of the chunk
     const float Gx = pgx / p.r, Gy = pgy / p.r;
@@ -668,7 +699,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
       c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
       c.restart = (b == 0 || seg_restart(p.H, p.seg, k)) ? 1 : 0;
-      c.f0 = n_chain + __ldg(p.full_off + k) - full_base;
+      c.f0 = __ldg(p.full_off + k) - full_base;
       c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
       c.pad0 = c.pad1 = 0;
       const float2 csk = __ldg(p.cs + k);
@@ -681,19 +712,10 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
     }
   }
 
-  // T-mode: zero the tile's traversable words of the chunk (warps OR their bits in)
-  if (tmode) {
-    const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
-    const size_t twplane = (size_t)p.ny * p.trav_words;
-    const int kz = max(kb, p.k_store);  // (replayed bins are not this launch's to store)
-    for (int idx = tid; idx < (ke - kz) * TY; idx += NTHREADS) {
-      const int b = idx / TY + (kz - kb), row = idx - (idx / TY) * TY;
-      int py = p.pyM + (int)(lj0 + R_T + row); if (py >= p.ny) py -= p.ny;  // rows are inside the window
-      const size_t w = (size_t)(kb + b) * twplane + (size_t)py * p.trav_words + gword;
-      p.trav[w] = 0u;
-      if (p.paired) p.trav[w + (size_t)p.H * twplane] = 0u;
-    }
-  }
+  // T-mode: the tile's traversable words of the chunk accumulate in shared memory (zeroed here, ORed by the
+  // warps, flushed once at the end: the tile's 32 columns are one world-aligned word per row)
+  if (tmode)
+    for (int idx = tid; idx < (ke - kb) * 32; idx += NTHREADS) twd[idx] = 0u;
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {
@@ -754,20 +776,24 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   __syncthreads();
 
   // ---- 4./5. states ------------------------------------------------------------------------
-  // Thread layout: warp w owns the RPW consecutive tile rows row0 .. row0 + RPW - 1, lane = column, state
-  // s = tile row row0 + s (so that on a border tile the warps whose footprints stay clear of the border
-  // take the interior path); T-mode: warp w owns the tile columns tc0 .. tc0 + RPW - 1, lane = row, state
-  // s = column tc0 + s.  State s of a thread sits at tile (trow0 + s drow, tcol0 + s dcol).
+  // Thread layout: a thread owns RPW states as RPW / 2 pairs of neighbouring tile rows (T-mode: columns);
+  // pair q of warp w sits at tile row (column) tr0 + q PS, tr0 = 2 w, PS = 2 NWARPS — the pairs of a
+  // warp are spread over the tile, so the states of a border band (e.g. the R_T rows / columns next to a
+  // window edge, which take the general path) are shared by all warps instead of being the work of one or
+  // two of them.  Row mode: lane = column; T-mode: lane = row.  State s of a thread is at offset so(s) =
+  // (s & 1) + (s >> 1) PS from tr0 along the state direction.
+  constexpr int PS = 2 * NWARPS;
+  constexpr int NP = RPW / 2;
   const size_t plane = (size_t)p.nx * p.ny;
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
   const size_t twplane = (size_t)p.ny * p.trav_words;
-  const int row0 = warp * RPW, tc0 = warp * RPW;
-  const int trow0 = tmode ? lane : row0, tcol0 = tmode ? tc0 : lane;
-  const float xs = (float)(tcol0 - TX / 2);  // x' of state 0 (T-mode: state s at xs + s)
+  const int tr0 = 2 * warp;
+  const int trow0 = tmode ? lane : tr0, tcol0 = tmode ? tr0 : lane;
+  const float xs = (float)(tcol0 - TX / 2);  // x' of state 0 (T-mode: state s at xs + so(s))
   const long long li = TI * TX + lane - p.I_M;
   const bool col_in = li >= 0 && li < p.nx;
   const bool col_any = __any_sync(0xffffffffu, col_in);
-  // tile-plane height at state s: zref0 + s * zstep (absolute, metres)
+  // tile-plane height at state s: zref0 + so(s) * zstep (absolute, metres)
   const float zref0 = href + fmaf(pgx, xs, fmaf(pgy, (float)trow0 - (float)(TY / 2), pc));
   const float zstep = tmode ? pgx : pgy;
   // per-thread byte bases of the prefix arrays at (halo row = tile row of state 0, halo column = its column)
@@ -777,57 +803,73 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const char* bv8 = reinterpret_cast<const char*>(pv) + base * 8;
   const char* bv4 = reinterpret_cast<const char*>(pvxx) + base * 4;
   const char* bh = reinterpret_cast<const char*>(hh_s) + base * 4;
-  constexpr int RS8 = PW * 8, RS4 = PW * 4;  // state s -> s halo rows lower (T-mode: s columns right)
+  constexpr int RS8 = PW * 8, RS4 = PW * 4;  // one state step: one halo row lower (T-mode: one column right)
 
   // per state s: record index in a bin plane (-1: outside the window), traversable-word index
-  int tmy = -1;  // interior tiles: lane s < RPW writes the traversable word of state s; T-mode: lane's row word
+  int tmy = -1;  // row mode: lane s < RPW writes the traversable word of state s
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
-    const int trow = tmode ? lane : row0 + s, tcol = tmode ? tc0 + s : lane;
+    const int trow = tmode ? lane : tr0 + so_of(s), tcol = tmode ? tr0 + so_of(s) : lane;
     const long long lj = TJ * TY + trow - p.J_M, lis = TI * TX + tcol - p.I_M;
     int py = -1, px = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
     if (lis >= 0 && lis < p.nx) { px = p.pxM + (int)lis; if (px >= p.nx) px -= p.nx; }
     soff[s] = (py >= 0 && px >= 0) ? py * p.nx + px : -1;
     stoff[s] = (!tmode && py >= 0 && col_any && lane == 0) ? py * p.trav_words + gword : -1;
-    if (tmode) tmy = py >= 0 ? py * p.trav_words + gword : -1;
-    else if (lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
+    if (!tmode && lane == s) tmy = (py >= 0 && col_any) ? py * p.trav_words + gword : -1;
   }
+  // T-mode: the rows of the tile are inside the window; lane = row: its py
+  int tpy = 0;
+  if (tmode) { tpy = p.pyM + (int)(lj0 + R_T + lane); if (tpy >= p.ny) tpy -= p.ny; }
 
-  // interior tiles: moments carried along the yaw chain, packed across the state pairs (2q, 2q + 1)
-  // so that one FFMA2 / FADD2 updates a moment of two states
-  F2 S0p[RPW / 2], S2p[RPW / 2], SXp[RPW / 2], SYp[RPW / 2];
-  // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
-  float4* outk = p.out + (size_t)kb * plane;
-  float4* outk2 = outk + (size_t)p.H * plane;
-  uint32_t* travk = p.trav + (size_t)kb * twplane;
-  uint32_t* travk2 = travk + (size_t)p.H * twplane;
-  // border tile: this warp takes the interior path when every halo row its footprints reach (halo rows
-  // row0 .. row0 + RPW - 1 + 2 R_T) is fully known and inside the window (validity row totals)
-  // (T-mode: every halo row's columns tc0 .. tc0 + RPW - 1 + 2 R_T)
-  bool wfast = fast;
-  if (!fast && G::CB) {
-    bool full = true;
-    if (tmode) {
-      for (int hr = lane; hr < HY; hr += 32)
-        full &= pv[hr * PW + tc0 + RPW + 2 * R_T].x - pv[hr * PW + tc0].x == (float)(RPW + 2 * R_T);
-    } else {
-      for (int hr = row0 + lane; hr < row0 + RPW + 2 * R_T; hr += 32) full &= pv[hr * PW + HX].x == (float)HX;
+  // pairs (warp-uniform masks, bit q): pin = a state of the pair lies inside the window; pfast = the pair's
+  // footprints reach only known cells inside the window (every halo row / column of its band), so it
+  // takes the interior path; the others the general (border / unknown) path
+  unsigned pin = 0, pfast = 0;
+#pragma unroll
+  for (int q = 0; q < NP; ++q)
+    if (__any_sync(0xffffffffu, soff[2 * q] >= 0 || soff[2 * q + 1] >= 0)) pin |= 1u << q;
+  if (fast) {
+    pfast = (1u << NP) - 1u;
+  } else if (G::CB) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const int t0 = tr0 + q * PS;  // the pair's first tile row (T-mode: column) = its band's first halo index
+      bool full = true;
+      if (tmode) {
+        for (int hr = lane; hr < HY; hr += 32)
+          full &= pv[hr * PW + t0 + 2 + 2 * R_T].x - pv[hr * PW + t0].x == (float)(2 + 2 * R_T);
+      } else {
+        for (int hr = t0 + lane; hr < t0 + 2 + 2 * R_T; hr += 32) full &= pv[hr * PW + HX].x == (float)HX;
+      }
+      if (__all_sync(0xffffffffu, full)) pfast |= 1u << q;
     }
-    wfast = __all_sync(0xffffffffu, full);
   }
-  // the interior path, for both thread layouts (T: the T-mode one; compile-time state strides)
-  auto interior = [&](auto tm) {
+  pfast &= pin;
+
+  // interior path: moments carried along the yaw chain, packed across the state pairs so that one FFMA2 /
+  // FADD2 updates a moment of two states.  MASKED: a border tile with some general pairs — every pair is
+  // computed (the general ones read valid shared memory, their results are discarded), only pfast pairs
+  // are stored.
+  F2 S0p[NP], S2p[NP], SXp[NP], SYp[NP];
+  auto interior = [&](auto tm, auto masked) {
     constexpr bool T = decltype(tm)::value;
+    constexpr bool MASKED = decltype(masked)::value;
     constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
+    // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
+    float4* outk = p.out + (size_t)kb * plane;
+    float4* outk2 = outk + (size_t)p.H * plane;
+    uint32_t* travk = p.trav + (size_t)kb * twplane;
+    uint32_t* travk2 = travk + (size_t)p.H * twplane;
+    uint32_t* twk = twd;
     const BinC* bc_k = bins_s;
-    for (int k = kb; k < ke; ++k, ++bc_k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane) {
+    for (int k = kb; k < ke; ++k, ++bc_k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane, twk += 32) {
       const int4 meta = *reinterpret_cast<const int4*>(bc_k);  // (e0, npre, nr, restart)
-      const int4* rk = runs_s + meta.x;
+      const int4* rk = tabc + meta.x;
       const int nr = meta.z;
       const bool restart = meta.w != 0;
-      // interior warps' states all lie inside the window (their whole halo band does), so every one is stored
+      // interior pairs' states all lie inside the window (their whole halo band does), so each is stored
       auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
         __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
         if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
@@ -836,20 +878,20 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       // the entries are the full rows of bin k, otherwise the corrections from k-1.
       if (restart) {
 #pragma unroll
-        for (int q = 0; q < RPW / 2; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
+        for (int q = 0; q < NP; ++q) S0p[q] = S2p[q] = SXp[q] = SYp[q] = bc(0.f);
       }
       const int npre = meta.y;  // prefix entries first, then cell entries
 #pragma unroll kUnrollPre
       for (int d = 0; d < npre; ++d) {
-        const int4 o = rk[d];
+        const int4 o = ld_entry<G::TG>(rk + d);
         const float dj = __int_as_float(o.w);
         const char* pa8 = b8 + o.x;
         const char* pb8 = b8 + o.y;
         const char* pa4 = b4 + o.z;
         const char* pb4 = b4 + (o.z + ((o.y - o.x) >> 1));
 #pragma unroll
-        for (int q = 0; q < RPW / 2; ++q) {
-          const int s = 2 * q;
+        for (int q = 0; q < NP; ++q) {
+          const int s = q * PS;  // so(2q); its partner state is one step further
           const float2 A0 = *reinterpret_cast<const float2*>(pa8 + s * S8);
           const float2 B0 = *reinterpret_cast<const float2*>(pb8 + s * S8);
           const float2 A1 = *reinterpret_cast<const float2*>(pa8 + (s + 1) * S8);
@@ -868,17 +910,18 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       // single cells entering / leaving the footprint since bin k-1: one h^ load per state
 #pragma unroll kUnrollCell
       for (int d = npre; d < nr; ++d) {
-        const int4 o = rk[d];
+        const int4 o = ld_entry<G::TG>(rk + d);
         const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
         const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
         const char* ph = bh + o.x;
 #pragma unroll
-        for (int q = 0; q < RPW / 2; ++q) {
-          const F2 h = pk(*reinterpret_cast<const float*>(ph + 2 * q * S4),
-                          *reinterpret_cast<const float*>(ph + (2 * q + 1) * S4));
+        for (int q = 0; q < NP; ++q) {
+          const int s = q * PS;
+          const F2 h = pk(*reinterpret_cast<const float*>(ph + s * S4),
+                          *reinterpret_cast<const float*>(ph + (s + 1) * S4));
           const F2 sh = bc(sg) * h;
-          // (T-mode: state s sits s columns right of state 0, so its x' is xs + s)
-          const F2 cxq = T ? pk(fmaf(sg, (float)(2 * q), cx), fmaf(sg, (float)(2 * q + 1), cx)) : bc(cx);
+          // (T-mode: state so(s) columns right of state 0: its x' is xs + so(s))
+          const F2 cxq = T ? pk(fmaf(sg, (float)s, cx), fmaf(sg, (float)(s + 1), cx)) : bc(cx);
           S0p[q] = S0p[q] + sh;
           S2p[q] = fma2(sh, h, S2p[q]);
           SXp[q] = fma2(cxq, h, SXp[q]);
@@ -890,70 +933,64 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
       unsigned tmine = 0;
 #pragma unroll
-      for (int s = 0; s < RPW; s += 2) {
-        const int q = s / 2;
+      for (int q = 0; q < NP; ++q) {
+        const int s = q * PS;
         const F2 xsq = T ? pk(xs + (float)s, xs + (float)(s + 1)) : bc(xs);
         const StateOut2 o = arrow2(S0p[q], S2p[q], fma2(neg2(xsq), S0p[q], SXp[q]), SYp[q],
                                    pk(fmaf(zstep, (float)s, zref0), fmaf(zstep, (float)(s + 1), zref0)), Gq1, Gq2,
                                    aG1, aG2, gc, gd, ge, gf, p);
-        store_rec(soff[s], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
-        store_rec(soff[s + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
-        if (T) {  // this lane's row: bits tc0 + s, tc0 + s + 1 of its word
-          tmine |= (o.trav_a ? 1u : 0u) << s;
-          tmine |= (o.trav_b ? 1u : 0u) << (s + 1);
-        } else {  // the warp's 32 lanes are one world-aligned 32-group = one word
-          const unsigned ma = __ballot_sync(0xffffffffu, o.trav_a);
-          const unsigned mb = __ballot_sync(0xffffffffu, o.trav_b);
-          if (lane == s) tmine = ma;
-          if (lane == s + 1) tmine = mb;
+        if (!MASKED || (pfast >> q & 1u)) {
+          store_rec(soff[2 * q], lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z));
+          store_rec(soff[2 * q + 1], hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z));
+          if (T) {  // this lane's row: bits tr0 + s, tr0 + s + 1 of its word
+            tmine |= (o.trav_a ? 1u : 0u) << (tr0 + s);
+            tmine |= (o.trav_b ? 1u : 0u) << (tr0 + s + 1);
+          } else {  // the warp's 32 lanes are one world-aligned 32-group = one word
+            const unsigned ma = __ballot_sync(0xffffffffu, o.trav_a);
+            const unsigned mb = __ballot_sync(0xffffffffu, o.trav_b);
+            if (lane == 2 * q) tmine = ma;
+            if (lane == 2 * q + 1) tmine = mb;
+          }
         }
       }
-      if (tmy >= 0) {
-        if (T) {  // the words were zeroed before the prefix build
-          if (tmine) {
-            atomicOr(travk + tmy, tmine << tc0);
-            if (p.paired) atomicOr(travk2 + tmy, tmine << tc0);
-          }
-        } else {  // lane s writes state s's word
-          travk[tmy] = tmine;
-          if (p.paired) travk2[tmy] = tmine;
-        }
+      if (T) {  // OR into the tile's words in shared memory (flushed once at the end)
+        if (tmine) atomicOr(twk + lane, tmine);
+      } else if (tmy >= 0 && (!MASKED || (pfast >> (lane >> 1) & 1u))) {  // lane s writes state s's word
+        travk[tmy] = tmine;
+        if (p.paired) travk2[tmy] = tmine;
       }
     }
   };
-  if (wfast) {
-    interior(std::integral_constant<bool, tmode>{});
-    return;
-  }
-  // ---- border / unknown tile: two states at a time along the whole yaw chunk; per state also the validity
+
+  // ---- border / unknown pairs: two states at a time along the whole yaw chunk; per state also the validity
   // moments (N, sum di, sum dj, sum di^2, sum di dj, sum dj^2), all carried along the yaw chain like the
   // interior moments (prefix entries with validity prefixes, then single cells: h^ or NaN = unknown)
   auto border = [&](auto tm) {
     constexpr bool T = decltype(tm)::value;
     constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
   #pragma unroll 1
-    for (int sp = 0; sp < RPW; sp += 2) {
+    for (int q = 0; q < NP; ++q) {
+      if (!(pin >> q & 1u) || (pfast >> q & 1u)) continue;  // outside the window / done on the interior path
+      const int sq = q * PS;  // the offset so(2 q) of the pair's first state
       // accumulators packed across the state pair (lo = state sp, hi = state sp + 1): one FFMA2 per moment
       F2 S0g, S2g, SXHg, SYHg, Nv, Sxv, Syv, Sxxv, Sxyv, Syyv;
-      const int so8 = sp * S8, so4 = sp * S4;
-      // x' of the pair's states (from the tile centre): T-mode columns xs + sp, xs + sp + 1
-      const F2 xsp = T ? pk(xs + (float)sp, xs + (float)(sp + 1)) : bc(xs);
+      const int so8 = sq * S8, so4 = sq * S4;
+      // x' of the pair's states (from the tile centre): T-mode columns xs + sq, xs + sq + 1
+      const F2 xsp = T ? pk(xs + (float)sq, xs + (float)(sq + 1)) : bc(xs);
       const F2 xsp2 = T ? xsp * xsp : bc(xs * xs), xspm2 = T ? bc(-2.f) * xsp : bc(-2.f * xs);
       int so0 = soff[0], so1 = soff[1], st0 = stoff[0], st1 = stoff[1];
   #pragma unroll
-      for (int q = 2; q < RPW; q += 2)  // static register selection (no local-memory indexing)
-        if (sp == q) { so0 = soff[q]; so1 = soff[q + 1]; st0 = stoff[q]; st1 = stoff[q + 1]; }
-      // both rows outside the window (tile rows beyond a window edge): nothing to store, nothing to compute
-      if (!__any_sync(0xffffffffu, so0 >= 0 || so1 >= 0)) continue;
+      for (int qq = 1; qq < NP; ++qq)  // static register selection (no local-memory indexing)
+        if (q == qq) { so0 = soff[2 * qq]; so1 = soff[2 * qq + 1]; st0 = stoff[2 * qq]; st1 = stoff[2 * qq + 1]; }
   #pragma unroll 1
       for (int k = kb; k < ke; ++k) {
         const BinC* bk = bins_s + (k - kb);
         const int4 meta = *reinterpret_cast<const int4*>(&bk->e0);
         const int4 metaf = *reinterpret_cast<const int4*>(&bk->f0);
-        const int4* rkf = runs_s + metaf.x;
+        const int4* rkf = tabf + metaf.x;
         const int nf = metaf.y;
         // the yaw chain, or (R_T = 32) the full rows of every bin as prefix entries
-        const int4* rk = G::CB ? runs_s + meta.x : rkf;
+        const int4* rk = G::CB ? tabc + meta.x : rkf;
         const int nr = G::CB ? meta.z : nf;
         const int npre = G::CB ? meta.y : nf;
         const float2 csk = make_float2(bk->cs.x, bk->cs.y);
@@ -961,7 +998,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
   #pragma unroll 1
         for (int d = 0; d < npre; ++d) {
-          const int4 o = rk[d];
+          const int4 o = ld_entry<G::TG>(rk + d);
           const float dj = __int_as_float(o.w);
           const int ob4 = o.z + ((o.y - o.x) >> 1);
           const float2 A0 = *reinterpret_cast<const float2*>(b8 + so8 + o.x);
@@ -997,7 +1034,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         }
   #pragma unroll 1
         for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
-          const int4 o = rk[d];
+          const int4 o = ld_entry<G::TG>(rk + d);
           const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
           const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
           const float h0 = *reinterpret_cast<const float*>(bh + so4 + o.x);
@@ -1021,106 +1058,122 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         float4* outk2 = p.out + (size_t)(k + p.H) * plane;
         uint32_t* travk = p.trav + (size_t)k * twplane;
         uint32_t* travk2 = p.trav + (size_t)(k + p.H) * twplane;
-        auto store = [&](int off, int toff, int bit, float risk, float pitch, float roll, float z, unsigned trav) {
-          if (off >= 0) {
-            __stcs(outk + off, make_float4(risk, pitch, roll, z));
-            if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
-          }
-          if (T) {  // T-mode: bit `bit` of this lane's row word (zeroed before the prefix build)
-            if (off >= 0 && trav && tmy >= 0) {
-              atomicOr(travk + tmy, 1u << bit);
-              if (p.paired) atomicOr(travk2 + tmy, 1u << bit);
-            }
-            return;
-          }
-          const unsigned tmask = __ballot_sync(0xffffffffu, off >= 0 && trav);
-          if (lane == 0 && toff >= 0) {
-            travk[toff] = tmask;
-            if (p.paired) travk2[toff] = tmask;
-          }
-        };
-            const float N[2] = {lo(Nv), hi(Nv)}, Sx[2] = {lo(Sxv), hi(Sxv)}, Sy[2] = {lo(Syv), hi(Syv)};
-            const float Sxx[2] = {lo(Sxxv), hi(Sxxv)}, Sxy[2] = {lo(Sxyv), hi(Sxyv)}, Syy[2] = {lo(Syyv), hi(Syyv)};
-            const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
-            const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
-            Cov2 cv = cov_general(Nv, Sxv, Syv, shl, shh, S0g, S2g, SXHg, SYHg,
-                                  pk(fmaf(zstep, (float)sp, zref0), fmaf(zstep, (float)(sp + 1), zref0)), pgx, pgy, p.r);
-            // (states outside the window are not stored: they never take the direct path)
-            const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
-            const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
-            StateOut1 dres[2];
-            if (need0 | need1) {
-              // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
-              // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
-              const float m0[2] = {lo(cv.zz), hi(cv.zz)};
-              float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
-    #pragma unroll
-              for (int s = 0; s < 2; ++s) {
-                unsigned msk = s ? need1 : need0;
-                while (msk) {
-                  const int src = __ffs(msk) - 1;
-                  msk &= msk - 1;
-                  const float mu = __shfl_sync(0xffffffffu, m0[s], src);
-                  // the state's top-left footprint-box cell: halo (row, column) = its tile (row, column)
-                  const float* rb = T ? raw + src * HX + tc0 + sp + s : raw + (row0 + sp + s) * HX + src;
-                  float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
-    #pragma unroll 1
-                  for (int d = 0; d < nf; ++d) {
-                    const int4 o = rkf[d];
-                    const float dj = __int_as_float(o.w);
-                    const int dr = (int)dj + R_T;  // stencil row -> halo row offset
-                    const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
-                    for (int c = c0 + lane; c < c1; c += 32) {
-                      const float hv = rb[dr * HX + c];
-                      if (!isnan(hv)) {
-                        const float dv = hv - mu;
-                        a0 += dv;
-                        a2 = fmaf(dv, dv, a2);
-                        ax = fmaf((float)(c - R_T), dv, ax);
-                        ay = fmaf(dj, dv, ay);
-                      }
-                    }
+        const float N[2] = {lo(Nv), hi(Nv)}, Sx[2] = {lo(Sxv), hi(Sxv)}, Sy[2] = {lo(Syv), hi(Syv)};
+        const float Sxx[2] = {lo(Sxxv), hi(Sxxv)}, Sxy[2] = {lo(Sxyv), hi(Sxyv)}, Syy[2] = {lo(Syyv), hi(Syyv)};
+        const Shape shl = footprint_shape(N[0], Sx[0], Sy[0], Sxx[0], Sxy[0], Syy[0]);
+        const Shape shh = footprint_shape(N[1], Sx[1], Sy[1], Sxx[1], Sxy[1], Syy[1]);
+        Cov2 cv = cov_general(Nv, Sxv, Syv, shl, shh, S0g, S2g, SXHg, SYHg,
+                              pk(fmaf(zstep, (float)sq, zref0), fmaf(zstep, (float)(sq + 1), zref0)), pgx, pgy, p.r);
+        // (states outside the window are not stored: they never take the direct path)
+        const bool dl = so0 >= 0 && shl.ok && N[0] < kDirectN, dh = so1 >= 0 && shh.ok && N[1] < kDirectN;
+        const unsigned need0 = __ballot_sync(0xffffffffu, dl), need1 = __ballot_sync(0xffffffffu, dh);
+        StateOut1 dres[2];
+        if (need0 | need1) {
+          // direct moments of the known footprint cells, one state at a time with the warp's lanes spread
+          // over the cells of each stencil row (warp-uniform loops), then a butterfly reduction
+          const float m0[2] = {lo(cv.zz), hi(cv.zz)};
+          float t0[2] = {0.f, 0.f}, t2[2] = {0.f, 0.f}, tx[2] = {0.f, 0.f}, ty[2] = {0.f, 0.f};
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            unsigned msk = s ? need1 : need0;
+            while (msk) {
+              const int src = __ffs(msk) - 1;
+              msk &= msk - 1;
+              const float mu = __shfl_sync(0xffffffffu, m0[s], src);
+              // the state's top-left footprint-box cell: halo (row, column) = its tile (row, column)
+              const float* rb = T ? raw + src * HX + tr0 + sq + s : raw + (tr0 + sq + s) * HX + src;
+              float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
+#pragma unroll 1
+              for (int d = 0; d < nf; ++d) {
+                const int4 o = ld_entry<G::TG>(rkf + d);
+                const float dj = __int_as_float(o.w);
+                const int dr = (int)dj + R_T;  // stencil row -> halo row offset
+                const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
+                for (int c = c0 + lane; c < c1; c += 32) {
+                  const float hv = rb[dr * HX + c];
+                  if (!isnan(hv)) {
+                    const float dv = hv - mu;
+                    a0 += dv;
+                    a2 = fmaf(dv, dv, a2);
+                    ax = fmaf((float)(c - R_T), dv, ax);
+                    ay = fmaf(dj, dv, ay);
                   }
-    #pragma unroll
-                  for (int w = 16; w >= 1; w >>= 1) {
-                    a0 += __shfl_xor_sync(0xffffffffu, a0, w);
-                    a2 += __shfl_xor_sync(0xffffffffu, a2, w);
-                    ax += __shfl_xor_sync(0xffffffffu, ax, w);
-                    ay += __shfl_xor_sync(0xffffffffu, ay, w);
-                  }
-                  if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
                 }
               }
-              // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
-    #pragma unroll
-              for (int s = 0; s < 2; ++s) {
-                if (s ? dh : dl) {
-                  const double dN = N[s], iN = 1.0 / dN, r = p.r;
-                  const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
-                  const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
-                               c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
-                  const double r2n = r * r * iN * iN;
-                  dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
-                                        r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
-                                        (double)m0[s] + md, csk,
-                                        make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
-                                        make_float3(p.wk, p.wx, p.wy));
-                }
+#pragma unroll
+              for (int w = 16; w >= 1; w >>= 1) {
+                a0 += __shfl_xor_sync(0xffffffffu, a0, w);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, w);
+                ax += __shfl_xor_sync(0xffffffffu, ax, w);
+                ay += __shfl_xor_sync(0xffffffffu, ay, w);
               }
+              if (lane == src) { t0[s] = a0; t2[s] = a2; tx[s] = ax; ty[s] = ay; }
             }
-            const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
-                                             shh.ok, 0.f, 0.f, csk, p);
-            // (store() holds a warp ballot: select first, store uniformly)
-            StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
-            StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
-            if (dl) ra = dres[0];
-            if (dh) rb = dres[1];
-            store(so0, st0, tc0 + sp, ra.risk, ra.pitch, ra.roll, ra.z, ra.trav);
-            store(so1, st1, tc0 + sp + 1, rb.risk, rb.pitch, rb.roll, rb.z, rb.trav);
+          }
+          // FP64 covariance of the direct states (geometry from exact integer moments) and FP64 solve
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (s ? dh : dl) {
+              const double dN = N[s], iN = 1.0 / dN, r = p.r;
+              const double mxc = Sx[s] * iN, myc = Sy[s] * iN, md = t0[s] * iN;
+              const double a = dN * Sxx[s] - (double)Sx[s] * Sx[s], b = dN * Syy[s] - (double)Sy[s] * Sy[s],
+                           c = dN * Sxy[s] - (double)Sx[s] * Sy[s];
+              const double r2n = r * r * iN * iN;
+              dres[s] = solve1_fp64(r2n * a, r2n * c, r2n * b, r * (tx[s] * iN - mxc * md),
+                                    r * (ty[s] * iN - myc * md), t2[s] * iN - md * md, mxc * r, myc * r,
+                                    (double)m0[s] + md, csk,
+                                    make_float4(p.kappa_max, p.phi_x_max, p.phi_y_max, 0.f),
+                                    make_float3(p.wk, p.wx, p.wy));
+            }
+          }
+        }
+        const StateOut2 o = solve2<true>(cv.c00, cv.c01, cv.c11, cv.c02, cv.c12, cv.c22, cv.mx, cv.my, cv.zz, shl.ok,
+                                         shh.ok, 0.f, 0.f, csk, p);
+        StateOut1 ra{lo(o.risk), lo(o.pitch), lo(o.roll), lo(o.z), o.trav_a};
+        StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
+        if (dl) ra = dres[0];
+        if (dh) rb = dres[1];
+        if (so0 >= 0) {
+          __stcs(outk + so0, make_float4(ra.risk, ra.pitch, ra.roll, ra.z));
+          if (p.paired) __stcs(outk2 + so0, make_float4(ra.risk, -ra.pitch, -ra.roll, ra.z));
+        }
+        if (so1 >= 0) {
+          __stcs(outk + so1, make_float4(rb.risk, rb.pitch, rb.roll, rb.z));
+          if (p.paired) __stcs(outk2 + so1, make_float4(rb.risk, -rb.pitch, -rb.roll, rb.z));
+        }
+        if (T) {  // T-mode: bits tr0 + sq, tr0 + sq + 1 of this lane's row word (shared memory, flushed at the end)
+          const unsigned bits = ((so0 >= 0 && ra.trav) ? 1u << (tr0 + sq) : 0u) | ((so1 >= 0 && rb.trav) ? 2u << (tr0 + sq) : 0u);
+          if (bits) atomicOr(twd + (k - kb) * 32 + lane, bits);
+        } else {  // row mode: one warp-wide word per state row
+          const unsigned m0w = __ballot_sync(0xffffffffu, so0 >= 0 && ra.trav);
+          const unsigned m1w = __ballot_sync(0xffffffffu, so1 >= 0 && rb.trav);
+          if (lane == 0) {
+            if (st0 >= 0) { travk[st0] = m0w; if (p.paired) travk2[st0] = m0w; }
+            if (st1 >= 0) { travk[st1] = m1w; if (p.paired) travk2[st1] = m1w; }
+          }
+        }
       }
     }
   };
-  border(std::integral_constant<bool, tmode>{});
+
+  if (fast) {
+    interior(std::integral_constant<bool, tmode>{}, std::false_type{});
+  } else {
+    if (pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
+    if (pin & ~pfast) border(std::integral_constant<bool, tmode>{});
+  }
+  if (tmode) {  // flush the tile's traversable words: one plain store per (bin, row) word (+ its pair bin)
+    __syncthreads();
+    const int kz = max(kb, p.k_store);
+    for (int idx = tid; idx < (ke - kz) * 32; idx += NTHREADS) {
+      const int b = idx / 32 + (kz - kb), row = idx & 31;
+      int py = p.pyM + (int)(lj0 + R_T + row); if (py >= p.ny) py -= p.ny;  // rows are inside the window
+      const size_t w = (size_t)(kb + b) * twplane + (size_t)py * p.trav_words + gword;
+      const uint32_t v = twd[b * 32 + row];
+      p.trav[w] = v;
+      if (p.paired) p.trav[w + (size_t)p.H * twplane] = v;
+    }
+  }
 }
 
 template <int R_T, int MODE>

@@ -45,6 +45,7 @@ struct AssessParams {
   // rows of bin k; chain: the full rows when k % period == 0, else the endpoint corrections from bin
   // k-1 to bin k (moments carried along the yaw chain).  Entries of bin k: [off[k], off[k+1]).
   const int4* full;
+  const int4* full_fmt;  // the same full rows in the kernel's entry format (8 e-, 8 e+, 4 e-, float dj)
   const int* full_off;   // [H+1]
   // chain (interior tiles) is stored in the kernel's shared-memory format: per bin first the prefix
   // entries (8 e_minus, 8 e_plus, 4 e_minus, float dj) — byte offsets into {P0, P2} and PX — then, from

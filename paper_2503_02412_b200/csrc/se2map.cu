@@ -64,6 +64,7 @@ struct se2m_map {
   bool sdf_valid = false;
   double sdf_dmax = 0;
   int4* d_full = nullptr;   // run-entry tables (see AssessParams)
+  int4* d_full_fmt = nullptr;
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
   int* d_chain_off = nullptr;
@@ -327,7 +328,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.out = m->d_out; p.trav = m->d_trav;
   p.trav_words = m->trav_words;
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
-  p.full = m->d_full; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off; p.chain_mid = m->d_chain_mid;
+  p.full = m->d_full; p.full_fmt = m->d_full_fmt; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off; p.chain_mid = m->d_chain_mid;
   p.seg = m->seg; p.seg_chunk = 1; p.n_chunks = 0;
   p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
@@ -578,6 +579,7 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       {(void**)&m->d_out, nst * sizeof(float4), "state records"},
       {(void**)&m->d_trav, (size_t)n * p->ny * m->trav_words * 4, "trav"},
       {(void**)&m->d_full, std::max<size_t>(1, full.size()) * sizeof(int4), "full table"},
+      {(void**)&m->d_full_fmt, std::max<size_t>(1, full.size()) * sizeof(int4), "full table (kernel format)"},
       {(void**)&m->d_full_off, m->full_off.size() * sizeof(int), "full offsets"},
       {(void**)&m->d_chain, std::max<size_t>(1, chain.size()) * sizeof(int4), "chain table"},
       {(void**)&m->d_chain_off, m->chain_off.size() * sizeof(int), "chain offsets"},
@@ -593,7 +595,16 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       return bail(e == cudaErrorMemoryAllocation ? SE2M_ERR_OOM : SE2M_ERR_CUDA);
     }
   }
+  // the full rows in the kernel's run-entry format: byte offsets into {P0, P2} (8 B) and PX (4 B), float dj
+  std::vector<int4> full_fmt(full.size());
+  for (size_t q = 0; q < full.size(); ++q) {
+    const float dj = (float)(full[q].z - m->R_T);
+    int dji;
+    memcpy(&dji, &dj, 4);
+    full_fmt[q] = make_int4(full[q].x * 8, full[q].y * 8, full[q].x * 4, dji);
+  }
   if ((e = cudaMemcpyAsync(m->d_full, full.data(), full.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_full_fmt, full_fmt.data(), full_fmt.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_full_off, m->full_off.data(), m->full_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_chain, chain.data(), chain.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_chain_off, m->chain_off.data(), m->chain_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
@@ -638,7 +649,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
   DevGuard dev_guard_(m->prm.device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
-                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
+                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_fmt, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc, m->d_sdf_g};
   for (void* q : ptrs)
     if (q) cudaFree(q);
