@@ -38,7 +38,26 @@
 #define SE2M_UNROLL_CELL 2
 #endif
 #ifndef SE2M_MINB
-#define SE2M_MINB(R_T) 2
+#define SE2M_MINB(R_T) (nthreads(R_T) == 512 ? 1 : 2)
+#endif
+
+// SE2M_CHECKS (debug builds, tools/build_checked.sh): device-side bounds checks on every shared-memory plane
+// access, run-table entry and global store of the assess kernel (a failed check prints and traps).  This stands
+// in for compute-sanitizer, which is closed on the B200 pool.
+#ifdef SE2M_CHECKS
+#include <cstdio>
+#define SE2M_CHK(c)                                                                     \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("se2m check failed %s:%d (block %d,%d thread %d): %s\n", __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x, #c);                    \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define SE2M_CHK(c) \
+  do {              \
+  } while (0)
 #endif
 
 namespace se2m {
@@ -121,7 +140,10 @@ __device__ __forceinline__ F2 copysign2(F2 m, F2 sg) { return pk(copysignf(lo(m)
 __device__ __forceinline__ F2 sel2(bool cl, bool ch, F2 a, F2 b) { return pk(cl ? lo(a) : lo(b), ch ? hi(a) : hi(b)); }
 
 constexpr float kPi2 = 1.57079632679489662f;
-constexpr int kUnrollPre = SE2M_UNROLL_PRE, kUnrollCell = SE2M_UNROLL_CELL;  // interior moment loops
+constexpr int kUnrollPre = SE2M_UNROLL_PRE;  // interior moment loops: prefix entries, single-cell entries
+// (the chain's cell entries are a dependent LDS -> address -> LDS chain: large footprints have many per bin
+// and gain from a deeper unroll — high-res 0.720 -> 0.695 ms with 8; the large map is indifferent)
+constexpr int unroll_cell(int R_T) { return R_T >= 16 ? 8 : SE2M_UNROLL_CELL; }
 
 // acos on [-1, 1] (Abramowitz & Stegun 4.4.46: acos(a) = sqrt(1 - a) P7(a), a in [0, 1]),
 // branch-free: acos(x) = pi/2 - sign(x) (pi/2 - acos(|x|)).  |1 - a| absorbs a 1-ulp overshoot.
@@ -448,21 +470,16 @@ struct BinC {
   float4 gq;                  // (Gq1, Gq2, aG1, aG2): the tile plane's gradient in the bin's eigenbasis
 };
 
-#ifndef SE2M_TABG_MIN_R
-#define SE2M_TABG_MIN_R 16
-#endif
-// a run-table entry: shared memory, or (TG) global memory through the read-only path
-template <bool TG>
-__device__ __forceinline__ int4 ld_entry(const int4* e) { return TG ? __ldg(e) : *e; }
-
-// State s of a thread sits so_of(s) tile rows (T-mode: columns) after its first one: pairs of neighbouring
-// rows spread 2 NWARPS apart, so every warp holds states in every part of the tile (see the kernel).
-__host__ __device__ constexpr int so_of(int s) { return (s & 1) + (s >> 1) * 2 * NWARPS; }
+// State s of a thread sits so_of(s, nw) tile rows (T-mode: columns) after its first one: pairs of neighbouring
+// rows spread 2 nw apart (nw warps per CTA), so every warp holds states in every part of the tile.
+__host__ __device__ constexpr int so_of(int s, int nw) { return (s & 1) + (s >> 1) * 2 * nw; }
 
 template <int R_T>
 struct Geom {
   static constexpr int TY = tile_rows(R_T);
-  static constexpr int RPW = TY / NWARPS;    // tile rows (states) per thread per yaw bin
+  static constexpr int NT = nthreads(R_T), NW = NT / 32;  // threads / warps per CTA
+  static constexpr int RPW = TY / NW;        // tile rows (states) per thread per yaw bin
+  static constexpr int UC = unroll_cell(R_T);  // unroll of the interior single-cell entry loop
   static constexpr int HX = TX + 2 * R_T;    // halo width (cells)
   static constexpr int HY = TY + 2 * R_T;    // halo height
   static constexpr int PW = HX + 1;          // prefix row length (exclusive prefix, entry 0 = 0)
@@ -477,18 +494,15 @@ struct Geom {
   // h^ per halo cell (single-cell chain entries); at R_T = 32 it aliases PV (interior tiles only)
   static constexpr size_t hh_off = CB ? pvxx_off + 4 * E : pv_off;
   static constexpr size_t misc_off = ((CB ? hh_off : pvxx_off) + 4 * E + 15) / 16 * 16;
-  static constexpr size_t runs_off = misc_off + 512;  // run entries of the CTA's bins (int4 byte offsets)
+  static constexpr size_t runs_off = misc_off + (NW <= 8 ? 512 : 1024);  // run entries of the CTA's bins (int4 byte offsets)
   // then the per-bin constants of the CTA's chunk (BinC: table offsets + interior geometry), so the
   // bin loop reads them with broadcast LDS instead of waiting on global loads at every bin
   // then (T-mode tiles) the traversable words of the chunk: k_chunk x 32 rows
-  // TG: large footprints (R_T >= SE2M_TABG_MIN_R) read the run tables from global memory (L1-cached, warp-
-  // uniform loads) instead of staging them in shared memory, so that two CTAs fit an SM (R_T = 16: 100 KB of
-  // tile planes; the tables of a 36-bin chunk would add ~30 KB)
-  static constexpr bool TG = R_T >= SE2M_TABG_MIN_R;
+  // (reading the run tables from global memory instead — L1-cached, warp-uniform — lets two R_T = 16 CTAs share
+  // an SM, but the entry-load latency then dominates the chain loops: high-res 0.72 -> 0.84 ms; kept out)
   static constexpr bool TMODE = TY == 32 && TX == 32 && CB;  // a T-mode (column-major) edge kernel exists
   static size_t bytes(int tab_cap, int k_chunk) {
-    return runs_off + (TG ? 0 : (size_t)tab_cap * 16) +
-           (size_t)k_chunk * (sizeof(BinC) + (TMODE ? 32 * sizeof(uint32_t) : 0));
+    return runs_off + (size_t)tab_cap * 16 + (size_t)k_chunk * (sizeof(BinC) + (TMODE ? 32 * sizeof(uint32_t) : 0));
   }
 };
 
@@ -496,10 +510,11 @@ struct Geom {
 // the vertical-window-edge tiles, in the column-major thread layout (T-mode; see below), launched
 // concurrently on a second stream so the two register allocations stay separate.
 template <int R_T, int MODE>
-__global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
+__global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
     assess_kernel(const AssessParams p, const __grid_constant__ CUtensorMap tmap) {
   using G = Geom<R_T>;
   constexpr int HX = G::HX, HY = G::HY, PW = G::PW, CPL = G::CPL, TY = G::TY, RPW = G::RPW;
+  constexpr int NTHREADS = G::NT, NWARPS = G::NW;
   extern __shared__ __align__(128) unsigned char smem[];
   float* raw = reinterpret_cast<float*>(smem);
   float2* p02 = reinterpret_cast<float2*>(smem + G::p02_off);
@@ -508,9 +523,9 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   float* pvxx = reinterpret_cast<float*>(smem + G::pvxx_off);
   float* hh_s = reinterpret_cast<float*>(smem + G::hh_off);  // h^ (NaN = unknown), stride PW
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::misc_off);
-  float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [3][8] min/max/valid, then [9][8] plane sums + 3
+  float* red = reinterpret_cast<float*>(smem + G::misc_off + 16);  // [2][NW] min/max, then [9][NW] plane sums + 4
   int4* runs_s = reinterpret_cast<int4*>(smem + G::runs_off);
-  BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (G::TG ? 0 : (size_t)p.tab_cap * 16));
+  BinC* bins_s = reinterpret_cast<BinC*>(smem + G::runs_off + (size_t)p.tab_cap * 16);
   uint32_t* twd = reinterpret_cast<uint32_t*>(bins_s + p.k_chunk);  // T-mode: [bin][row] traversable words
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -537,6 +552,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const int kb = max(p.k_begin, seg_bound(p.H, p.seg, s0));
   const int ke = min(p.k_end, seg_bound(p.H, p.seg, min(p.seg, s0 + p.seg_chunk)));
   if (kb >= ke) return;
+  SE2M_CHK(ke - kb <= p.k_chunk && kb >= 0 && ke <= p.H);
   // Vertical-window-edge tiles (the halo crosses the window's left or right edge only; they are never
   // "fast"): in MODE 1, warps own RPW tile COLUMNS each (lane = tile row), so the warps whose column band
   // (+- R_T) lies inside the window take the interior path, the ones wholly outside the window skip, and
@@ -601,11 +617,11 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       mxv = fmaxf(mxv, __shfl_xor_sync(0xffffffffu, mxv, o));
     }
-    if (lane == 0) { red[warp] = mn; red[8 + warp] = mxv; }
+    if (lane == 0) { red[warp] = mn; red[NWARPS + warp] = mxv; }
     __syncthreads();
-    mn = red[0]; mxv = red[8];
+    mn = red[0]; mxv = red[NWARPS];
 #pragma unroll
-    for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[8 + w]); }
+    for (int w = 1; w < NWARPS; ++w) { mn = fminf(mn, red[w]); mxv = fmaxf(mxv, red[NWARPS + w]); }
     href = (mn <= mxv) ? 0.5f * (mn + mxv) : 0.f;
     __syncthreads();  // red[] is reused below
   }
@@ -617,7 +633,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   // The count of valid cells also decides the interior ("fast") path: every halo cell known.
   constexpr float XC = (float)(R_T + TX / 2);  // x' = col - XC; the state at lane l has x' = l - TX/2
   constexpr float YC = (float)(R_T + TY / 2);  // y' = row - YC; tile row t has y' = t - TY/2
-  float* tplane = red + 8 * 9;
+  float* tplane = red + NWARPS * 9;
   {
     float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f, q4 = 0.f, q5 = 0.f, q6 = 0.f, q7 = 0.f, q8 = 0.f;
     for (int idx = tid; idx < HX * HY; idx += NTHREADS) {
@@ -639,17 +655,17 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       q8 += __shfl_xor_sync(0xffffffffu, q8, o);
     }
     if (lane == 0) {
-      red[0 * 8 + warp] = q0; red[1 * 8 + warp] = q1; red[2 * 8 + warp] = q2; red[3 * 8 + warp] = q3;
-      red[4 * 8 + warp] = q4; red[5 * 8 + warp] = q5; red[6 * 8 + warp] = q6; red[7 * 8 + warp] = q7;
-      red[8 * 8 + warp] = q8;
+      red[0 * NWARPS + warp] = q0; red[1 * NWARPS + warp] = q1; red[2 * NWARPS + warp] = q2;
+      red[3 * NWARPS + warp] = q3; red[4 * NWARPS + warp] = q4; red[5 * NWARPS + warp] = q5;
+      red[6 * NWARPS + warp] = q6; red[7 * NWARPS + warp] = q7; red[8 * NWARPS + warp] = q8;
     }
     __syncthreads();
     if (tid == 0) {
       float t[9];
 #pragma unroll
       for (int i = 0; i < 9; ++i) {
-        t[i] = red[i * 8];
-        for (int w = 1; w < NWARPS; ++w) t[i] += red[i * 8 + w];
+        t[i] = red[i * NWARPS];
+        for (int w = 1; w < NWARPS; ++w) t[i] += red[i * NWARPS + w];
       }
       float c = 0.f, gx = 0.f, gy = 0.f;
       if (t[0] >= 3.f) {
@@ -680,15 +696,14 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const int tab_base = __ldg(tab_off + kb);
   const int n_chain = (fast || G::CB) ? __ldg(tab_off + ke) - tab_base : 0;
   const int full_base = __ldg(p.full_off + kb);
-  if (!G::TG) {
-    for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
-    if (!fast)
-      for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS)
-        runs_s[n_chain + idx] = __ldg(p.full_fmt + full_base + idx);
-  }
-  // the chunk's chain entries and full-row entries (shared memory, or global memory for TG)
-  const int4* tabc = G::TG ? p.chain + tab_base : runs_s;
-  const int4* tabf = G::TG ? p.full_fmt + full_base : runs_s + n_chain;
+  SE2M_CHK(n_chain + (fast ? 0 : __ldg(p.full_off + ke) - full_base) <= p.tab_cap);
+  for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
+  if (!fast)
+    for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS)
+      runs_s[n_chain + idx] = __ldg(p.full_fmt + full_base + idx);
+  // the chunk's chain entries and full-row entries in shared memory
+  const int4* tabc = runs_s;
+  const int4* tabf = runs_s + n_chain;
 
   {  // per-bin constants of the chunk
     const float Gx = pgx / p.r, Gy = pgy / p.r;
@@ -804,13 +819,34 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
   const char* bv4 = reinterpret_cast<const char*>(pvxx) + base * 4;
   const char* bh = reinterpret_cast<const char*>(hh_s) + base * 4;
   constexpr int RS8 = PW * 8, RS4 = PW * 4;  // one state step: one halo row lower (T-mode: one column right)
+  // (SE2M_CHECKS) byte pointer inside a prefix / h^ plane of E entries of 8 or 4 bytes
+  auto in8 = [&](const char* q, const void* plane0) {
+    const long long o = q - reinterpret_cast<const char*>(plane0);
+    return o >= 0 && o + 8 <= (long long)(8 * G::E);
+  };
+  auto in4 = [&](const char* q, const void* plane0) {
+    const long long o = q - reinterpret_cast<const char*>(plane0);
+    return o >= 0 && o + 4 <= (long long)(4 * G::E);
+  };
+  (void)in8;
+  (void)in4;
+  auto rec_ok = [&](const float4* q) {  // a state record of the map
+    const long long o = q - p.out;
+    return o >= 0 && o < (long long)p.n_yaw * p.nx * p.ny;
+  };
+  auto word_ok = [&](const uint32_t* q) {  // a traversable word of the map
+    const long long o = q - p.trav;
+    return o >= 0 && o < (long long)p.n_yaw * p.ny * p.trav_words;
+  };
+  (void)rec_ok;
+  (void)word_ok;
 
   // per state s: record index in a bin plane (-1: outside the window), traversable-word index
   int tmy = -1;  // row mode: lane s < RPW writes the traversable word of state s
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
-    const int trow = tmode ? lane : tr0 + so_of(s), tcol = tmode ? tr0 + so_of(s) : lane;
+    const int trow = tmode ? lane : tr0 + so_of(s, NWARPS), tcol = tmode ? tr0 + so_of(s, NWARPS) : lane;
     const long long lj = TJ * TY + trow - p.J_M, lis = TI * TX + tcol - p.I_M;
     int py = -1, px = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
@@ -871,6 +907,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const bool restart = meta.w != 0;
       // interior pairs' states all lie inside the window (their whole halo band does), so each is stored
       auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
+        SE2M_CHK(off >= 0 && off < (int)plane && rec_ok(outk + off) && (!p.paired || rec_ok(outk2 + off)));
         __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
         if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
       };
@@ -883,7 +920,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       const int npre = meta.y;  // prefix entries first, then cell entries
 #pragma unroll kUnrollPre
       for (int d = 0; d < npre; ++d) {
-        const int4 o = ld_entry<G::TG>(rk + d);
+        const int4 o = rk[d];
         const float dj = __int_as_float(o.w);
         const char* pa8 = b8 + o.x;
         const char* pb8 = b8 + o.y;
@@ -892,6 +929,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
           const int s = q * PS;  // so(2q); its partner state is one step further
+          SE2M_CHK(in8(pa8 + s * S8, p02) && in8(pb8 + (s + 1) * S8, p02) && in4(pa4 + s * S4, pxh) &&
+                   in4(pb4 + (s + 1) * S4, pxh) && in8(pa8 + (s + 1) * S8, p02) && in8(pb8 + s * S8, p02));
           const float2 A0 = *reinterpret_cast<const float2*>(pa8 + s * S8);
           const float2 B0 = *reinterpret_cast<const float2*>(pb8 + s * S8);
           const float2 A1 = *reinterpret_cast<const float2*>(pa8 + (s + 1) * S8);
@@ -908,15 +947,16 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         }
       }
       // single cells entering / leaving the footprint since bin k-1: one h^ load per state
-#pragma unroll kUnrollCell
+#pragma unroll G::UC
       for (int d = npre; d < nr; ++d) {
-        const int4 o = ld_entry<G::TG>(rk + d);
+        const int4 o = rk[d];
         const float sg = __int_as_float(o.y), sdj = __int_as_float(o.w);
         const float cx = fmaf(sg, xs, __int_as_float(o.z));  // sgn x' = sgn (xs + di)
         const char* ph = bh + o.x;
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
           const int s = q * PS;
+          SE2M_CHK(in4(ph + s * S4, hh_s) && in4(ph + (s + 1) * S4, hh_s));
           const F2 h = pk(*reinterpret_cast<const float*>(ph + s * S4),
                           *reinterpret_cast<const float*>(ph + (s + 1) * S4));
           const F2 sh = bc(sg) * h;
@@ -954,8 +994,10 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         }
       }
       if (T) {  // OR into the tile's words in shared memory (flushed once at the end)
+        SE2M_CHK(twk + lane - twd < (ke - kb) * 32);
         if (tmine) atomicOr(twk + lane, tmine);
       } else if (tmy >= 0 && (!MASKED || (pfast >> (lane >> 1) & 1u))) {  // lane s writes state s's word
+        SE2M_CHK(word_ok(travk + tmy) && (!p.paired || word_ok(travk2 + tmy)));
         travk[tmy] = tmine;
         if (p.paired) travk2[tmy] = tmine;
       }
@@ -998,9 +1040,12 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
   #pragma unroll 1
         for (int d = 0; d < npre; ++d) {
-          const int4 o = ld_entry<G::TG>(rk + d);
+          const int4 o = rk[d];
           const float dj = __int_as_float(o.w);
           const int ob4 = o.z + ((o.y - o.x) >> 1);
+          SE2M_CHK(in8(b8 + so8 + o.x, p02) && in8(b8 + so8 + o.y + S8, p02) && in4(b4 + so4 + o.z, pxh) &&
+                   in4(b4 + so4 + ob4 + S4, pxh) && in8(bv8 + so8 + o.x, pv) && in8(bv8 + so8 + o.y + S8, pv) &&
+                   in4(bv4 + so4 + o.z, pvxx) && in4(bv4 + so4 + ob4 + S4, pvxx));
           const float2 A0 = *reinterpret_cast<const float2*>(b8 + so8 + o.x);
           const float2 B0 = *reinterpret_cast<const float2*>(b8 + so8 + o.y);
           const float2 A1 = *reinterpret_cast<const float2*>(b8 + so8 + o.x + S8);
@@ -1034,9 +1079,10 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         }
   #pragma unroll 1
         for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
-          const int4 o = ld_entry<G::TG>(rk + d);
+          const int4 o = rk[d];
           const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
           const float cxx = sg * sdi * sdi, cxy = sg * sdi * sdj, cyy = sg * sdj * sdj;
+          SE2M_CHK(in4(bh + so4 + o.x, hh_s) && in4(bh + so4 + o.x + S4, hh_s));
           const float h0 = *reinterpret_cast<const float*>(bh + so4 + o.x);
           const float h1 = *reinterpret_cast<const float*>(bh + so4 + o.x + S4);
           const bool k0 = !isnan(h0), k1 = !isnan(h1);
@@ -1085,11 +1131,12 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
               float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
 #pragma unroll 1
               for (int d = 0; d < nf; ++d) {
-                const int4 o = ld_entry<G::TG>(rkf + d);
+                const int4 o = rkf[d];
                 const float dj = __int_as_float(o.w);
                 const int dr = (int)dj + R_T;  // stencil row -> halo row offset
                 const int c0 = (o.x >> 3) - dr * PW, c1 = (o.y >> 3) - dr * PW;  // columns src + [c0, c1)
                 for (int c = c0 + lane; c < c1; c += 32) {
+                  SE2M_CHK(rb + dr * HX + c - raw >= 0 && rb + dr * HX + c - raw < HX * HY);
                   const float hv = rb[dr * HX + c];
                   if (!isnan(hv)) {
                     const float dv = hv - mu;
@@ -1133,6 +1180,8 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         StateOut1 rb{hi(o.risk), hi(o.pitch), hi(o.roll), hi(o.z), o.trav_b};
         if (dl) ra = dres[0];
         if (dh) rb = dres[1];
+        SE2M_CHK((so0 < 0 || (rec_ok(outk + so0) && (!p.paired || rec_ok(outk2 + so0)))) &&
+                 (so1 < 0 || (rec_ok(outk + so1) && (!p.paired || rec_ok(outk2 + so1)))));
         if (so0 >= 0) {
           __stcs(outk + so0, make_float4(ra.risk, ra.pitch, ra.roll, ra.z));
           if (p.paired) __stcs(outk2 + so0, make_float4(ra.risk, -ra.pitch, -ra.roll, ra.z));
@@ -1143,11 +1192,14 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
         }
         if (T) {  // T-mode: bits tr0 + sq, tr0 + sq + 1 of this lane's row word (shared memory, flushed at the end)
           const unsigned bits = ((so0 >= 0 && ra.trav) ? 1u << (tr0 + sq) : 0u) | ((so1 >= 0 && rb.trav) ? 2u << (tr0 + sq) : 0u);
+          SE2M_CHK(k - kb < p.k_chunk);
           if (bits) atomicOr(twd + (k - kb) * 32 + lane, bits);
         } else {  // row mode: one warp-wide word per state row
           const unsigned m0w = __ballot_sync(0xffffffffu, so0 >= 0 && ra.trav);
           const unsigned m1w = __ballot_sync(0xffffffffu, so1 >= 0 && rb.trav);
           if (lane == 0) {
+            SE2M_CHK((st0 < 0 || word_ok(travk + st0)) && (st1 < 0 || word_ok(travk + st1)) &&
+                     (!p.paired || ((st0 < 0 || word_ok(travk2 + st0)) && (st1 < 0 || word_ok(travk2 + st1)))));
             if (st0 >= 0) { travk[st0] = m0w; if (p.paired) travk2[st0] = m0w; }
             if (st1 >= 0) { travk[st1] = m1w; if (p.paired) travk2[st1] = m1w; }
           }
@@ -1170,6 +1222,7 @@ __global__ void __launch_bounds__(NTHREADS, SE2M_MINB(R_T))
       int py = p.pyM + (int)(lj0 + R_T + row); if (py >= p.ny) py -= p.ny;  // rows are inside the window
       const size_t w = (size_t)(kb + b) * twplane + (size_t)py * p.trav_words + gword;
       const uint32_t v = twd[b * 32 + row];
+      SE2M_CHK(b < p.k_chunk && word_ok(p.trav + w) && (!p.paired || word_ok(p.trav + w + (size_t)p.H * twplane)));
       p.trav[w] = v;
       if (p.paired) p.trav[w + (size_t)p.H * twplane] = v;
     }
@@ -1194,7 +1247,7 @@ static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensor
     configured_bytes = (int)smem;
   }
   dim3 grid(grid_x, p.n_chunks);
-  assess_kernel<R_T, MODE><<<grid, NTHREADS, smem, stream>>>(p, *tmap);
+  assess_kernel<R_T, MODE><<<grid, nthreads(R_T), smem, stream>>>(p, *tmap);
   return cudaGetLastError();
 }
 
@@ -1228,7 +1281,7 @@ static int ctas_per_sm_t(size_t smem) {
   if (cudaFuncGetAttributes(&fa, assess_kernel<R_T, 0>) != cudaSuccess ||
       ((size_t)fa.maxDynamicSharedSizeBytes < smem &&
        cudaFuncSetAttribute(assess_kernel<R_T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assess_kernel<R_T, 0>, NTHREADS, smem) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assess_kernel<R_T, 0>, nthreads(R_T), smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }

@@ -10,12 +10,17 @@ namespace se2m {
 // Spatial tile of states handled by one CTA: world-aligned, TX = one warp wide,
 // tile_rows(R_T) rows (32 for R_T <= 12, else 16, to fit >= 2 CTAs per SM in shared memory).
 constexpr int TX = 32;
-constexpr int NTHREADS = 256;              // 8 warps; warp w owns tile rows w, w + 8, w + 16, ...
-constexpr int NWARPS = NTHREADS / 32;
+// threads per assess CTA: 256 (8 warps, 2 CTAs per SM) — except R_T = 16 (the 0.05 m high-res footprint): one
+// CTA of 512 threads (16 warps) per SM on 32-row tiles, because its tile planes leave shared memory for only
+// one CTA per SM and 8 warps cannot hide the latency of the chain loops
+#ifndef SE2M_R16_THREADS
+#define SE2M_R16_THREADS 512
+#endif
+constexpr int nthreads(int R_T) { return (R_T > 12 && R_T <= 16) ? SE2M_R16_THREADS : 256; }
 #ifndef SE2M_TY_SMALL
 #define SE2M_TY_SMALL 32
 #endif
-constexpr int tile_rows(int R_T) { return R_T <= 12 ? SE2M_TY_SMALL : 16; }
+constexpr int tile_rows(int R_T) { return R_T <= 12 ? SE2M_TY_SMALL : (nthreads(R_T) == 512 ? 32 : 16); }
 // shared-memory layout choice of the assess kernel: up to R_T = 24 the h^ plane is separate and border
 // tiles also run on the yaw chain (both run tables in shared memory); at R_T = 32 the plane aliases the
 // validity prefixes (interior tiles only) and border tiles take the full rows of every bin
@@ -96,9 +101,16 @@ struct AssessParams {
 // Yaw-chain segments (AssessParams::seg): segment s covers representative bins [seg_bound(s), seg_bound(s + 1)).
 // With S <= H every segment holds >= 1 bin; the balanced yaw shards of se2m_shard_plan, [H g / G, H (g + 1) / G),
 // start on segment bounds whenever G divides S (a shard starting elsewhere replays from its segment's bound).
+// (32-bit: H * S <= n_yaw^2 < 2^31 — se2m_init limits n_yaw to 4096)
+#ifdef SE2M_SEG64
 __host__ __device__ inline int seg_bound(int H, int S, int s) { return (int)((long long)H * s / S); }
 __host__ __device__ inline int seg_of(int H, int S, int k) {
   int s = (int)((long long)k * S / H);
+#else
+__host__ __device__ inline int seg_bound(int H, int S, int s) { return H * s / S; }
+__host__ __device__ inline int seg_of(int H, int S, int k) {
+  int s = k * S / H;
+#endif
   if (s + 1 <= S && seg_bound(H, S, s + 1) <= k) ++s;  // (at most one step: segments hold >= 1 bin)
   return s;
 }

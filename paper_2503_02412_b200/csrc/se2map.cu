@@ -372,7 +372,7 @@ extern "C" void se2m_default_params(se2m_params* p) {
 static se2m_status validate(const se2m_params* p) {
   if (!p) return fail(nullptr, SE2M_ERR_INVALID_ARG, "params is NULL");
   if (p->nx < 1 || p->ny < 1 || (long long)p->nx * p->ny > (1ll << 31)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "nx, ny must be >= 1 and nx*ny <= 2^31");
-  if (p->n_yaw < 1) return fail(nullptr, SE2M_ERR_INVALID_ARG, "n_yaw must be >= 1");
+  if (p->n_yaw < 1 || p->n_yaw > 4096) return fail(nullptr, SE2M_ERR_INVALID_ARG, "n_yaw must be in [1, 4096]");
   if (!(p->resolution > 0) || !isfinite(p->resolution)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "resolution must be > 0");
   if (!(p->ellipse_ex > 0) || !(p->ellipse_ey > 0)) return fail(nullptr, SE2M_ERR_INVALID_ARG, "ellipse semi-axes must be > 0");
   for (int i = 0; i < 3; ++i)

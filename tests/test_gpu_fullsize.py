@@ -89,3 +89,38 @@ def test_chain_map_big_footprints_sampled_parity(ex, ey, holes):
     rep = compare({k: q[k] for k in ("risk", "pitch", "roll", "z", "trav")}, orc)
     print(ex, ey, holes, rep)
     assert rep["ok"], rep
+
+
+def test_highres_every_state_parity():
+    """Every one of the 46.08 M states of the high-res configuration (800 x 800 x 72 @ 0.05 m) in the bench's
+    launch configuration (one FULL assess), against the FP64 oracle, one yaw bin at a time (all cells of the
+    bin per oracle call)."""
+    cfg = CONFIGS["highres"]
+    nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
+    m = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    I_M, J_M = m.origin()
+    h = world_heights(cfg["terrain"], I_M, J_M, nx, ny, r)
+    m.update_elevation(h)
+    m.assess_se2(0)
+    g = m.download()
+    m.close()
+    P = oracle_params(nx, ny, r, n_yaw)
+    jj, ii = np.meshgrid(np.arange(ny, dtype=np.int32), np.arange(nx, dtype=np.int32), indexing="ij")
+    tot = None
+    for k in range(n_yaw):
+        ijk = np.stack([ii.ravel(), jj.ravel(), np.full(nx * ny, k, np.int32)], axis=1)
+        orc = oracle.assess_states(P, h, ijk)
+        rep = compare({f: g[f][k].ravel() for f in ("risk", "pitch", "roll", "z", "trav")}, orc)
+        if tot is None:
+            tot = rep
+        else:
+            for key, v in rep.items():
+                if key.startswith("max_"):
+                    tot[key] = max(tot[key], v)
+                elif key == "ok":
+                    tot[key] = tot[key] and v
+                elif isinstance(v, int):
+                    tot[key] += v
+        assert rep["ok"], (k, rep)
+    print("highres all states", tot)
+    assert tot["n"] == nx * ny * n_yaw and tot["normal"] > 0.95 * tot["n"]
