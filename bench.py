@@ -616,8 +616,29 @@ def highres_update(S, stream, torch, reps=10):
     ms = sorted(a.elapsed_time(b) for a, b in ts)
     m.close()
     n = nx * ny * n_yaw
-    return {"highres_ms": ms[len(ms) // 2], "highres_states": n, "highres_states_per_s": n / (ms[len(ms) // 2] * 1e-3),
-            "highres_W_ops_per_state": 4 * stencil_cells(cfg) + 200}
+    t = ms[len(ms) // 2]
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6450.6)
+    bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
+    out = {"highres_ms": t, "highres_states": n, "highres_states_per_s": n / (t * 1e-3),
+           "highres_W_ops_per_state": 4 * stencil_cells(cfg) + 200}
+    # the binding bound of this config is the kernels' own instruction issue, not HBM: its floor is
+    # the warp instructions of one assess call (ncu, profiles/) at one instruction per cycle per scheduler
+    roof = {"hbm": {"achieved_gbs": n * bytes_state / (t * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                    "frac": n * bytes_state / (t * 1e-3) / 1e9 / hbm_peak, "bytes_per_state": bytes_state}}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_highres.json")))
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        mhz = prof.get("sm_frequency_ghz", 1.9) * 1e3
+        floor_ms = prof["executed_instructions_per_call"] / (4 * n_sm * mhz * 1e6) * 1e3
+        roof["issue"] = {"floor_ms": floor_ms, "frac": floor_ms / t, "executed_warp_instructions_per_call":
+                         prof["executed_instructions_per_call"], "sm_mhz": mhz,
+                         "source": "profiles/latest_ncu_highres.json (ncu --set full of one assess call: both kernels)"}
+        roof["bound"] = "issue"
+    except Exception:
+        roof["bound"] = "issue (no ncu summary in profiles/)"
+    out["highres_roofline"] = roof
+    return out
 
 
 def paper_pipeline(S, stream, torch, n_frames=6, n_iters=40, warm=4):

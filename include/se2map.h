@@ -324,6 +324,13 @@ se2m_status se2m_tile_info(const se2m_map* m, int32_t* tile_x, int32_t* tile_y);
 /* Block until all work queued on the handle's streams (its stream and its copy stream) is done. */
 se2m_status se2m_synchronize(se2m_map* m);
 
+/* Diagnostics (debug builds compiled with SE2M_PHASES, tools/build_phases.sh; SE2M_ERR_UNSUPPORTED otherwise):
+ * per-warp records of the assess kernels' phase boundaries (%globaltimer ns: start, halo in shared memory, tile
+ * plane, prefix planes and tables, states done, end; then blockIdx.x, blockIdx.y, kernel mode, flags), 64 bytes
+ * each, copied into out (host memory, up to max_records); *n = records written since the last reset (process-
+ * wide, all handles).  reset != 0 restarts the count.  Synchronises the stream. */
+se2m_status se2m_debug_phases(se2m_map* m, void* out, int64_t max_records, int32_t reset, int64_t* n);
+
 /* Kernel launches issued by this handle since creation (for the bench's gpu_launches). */
 int64_t se2m_launch_count(const se2m_map* m);
 

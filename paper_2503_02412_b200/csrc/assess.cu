@@ -27,6 +27,7 @@
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "se2m_internal.h"
@@ -61,6 +62,32 @@
 #endif
 
 namespace se2m {
+
+// SE2M_PHASES (debug builds, tools/build_phases.sh): every warp of every assess CTA records %globaltimer at the
+// kernel's phase boundaries (start, halo in shared memory, tile plane, prefix planes + tables, states done, end)
+// into a device buffer read back by se2m_debug_phases — the per-CTA latency breakdown of small maps.
+struct PhaseRec {
+  unsigned long long t[6];
+  int bx, by, mode, flags;  // flags: bit 0 fast tile, bits 8..15 pin, bits 16..23 pfast
+};
+[[maybe_unused]] constexpr int kPhaseSlots = 1 << 17;  // warp records
+#ifdef SE2M_PHASES
+__device__ PhaseRec g_phase[kPhaseSlots];
+__device__ unsigned int g_phase_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SE2M_PHASE(i) \
+  do {                \
+    if (lane == 0 && ph_slot >= 0 && ph_slot < kPhaseSlots) g_phase[ph_slot].t[i] = gtimer(); \
+  } while (0)
+#else
+#define SE2M_PHASE(i) \
+  do {                \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------------
 // TMA / mbarrier helpers (inline PTX, sm_90+ / sm_100a)
@@ -529,6 +556,15 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   uint32_t* twd = reinterpret_cast<uint32_t*>(bins_s + p.k_chunk);  // T-mode: [bin][row] traversable words
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef SE2M_PHASES
+  int ph_slot = -1;
+  if (lane == 0) ph_slot = (int)atomicAdd(&g_phase_n, 1u);
+  if (lane == 0 && ph_slot < kPhaseSlots) {
+    g_phase[ph_slot].bx = blockIdx.x; g_phase[ph_slot].by = blockIdx.y; g_phase[ph_slot].mode = MODE;
+    g_phase[ph_slot].flags = 0;
+  }
+  SE2M_PHASE(0);
+#endif
   // MODE 1 runs the tile columns p.tcols[0 .. n_tcols) of every grid row
   const int gx = MODE == 1 ? p.n_tcols : p.tiles_x;
   const int tx_rel = MODE == 1 ? p.tcols[blockIdx.x % (unsigned)gx] : (int)(blockIdx.x % (unsigned)gx);
@@ -548,9 +584,10 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   const long long TJ = p.TJ0 + ty_rel;
   const long long li0 = TI * TX - R_T - p.I_M;  // logical (window) index of halo column 0
   const long long lj0 = TJ * TY - R_T - p.J_M;
-  const int s0 = seg_of(p.H, p.seg, p.k_begin) + (int)blockIdx.y * p.seg_chunk;  // this CTA's first segment
-  const int kb = max(p.k_begin, seg_bound(p.H, p.seg, s0));
-  const int ke = min(p.k_end, seg_bound(p.H, p.seg, min(p.seg, s0 + p.seg_chunk)));
+  // this CTA's segments [s0, s0 + seg_chunk) (bounds from the host table: no integer division here)
+  const int s0 = p.seg_first + (int)blockIdx.y * p.seg_chunk;
+  const int kb = max(p.k_begin, __ldg(p.segb + s0));
+  const int ke = min(p.k_end, __ldg(p.segb + min(p.seg, s0 + p.seg_chunk)));
   if (kb >= ke) return;
   SE2M_CHK(ke - kb <= p.k_chunk && kb >= 0 && ke <= p.H);
   // Vertical-window-edge tiles (the halo crosses the window's left or right edge only; they are never
@@ -601,6 +638,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   }
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
+  SE2M_PHASE(1);
 
   // ---- 2. reference height, validity and the tile plane in one pass over the halo ---------------
   // href = the halo's centre cell (any height near the data keeps the FP32 sums accurate); a tile whose
@@ -687,6 +725,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   }
   const float pc = tplane[0], pgx = tplane[1], pgy = tplane[2];
   const bool fast = tplane[3] > 0.5f && !p.force_general;
+  SE2M_PHASE(2);
 
   // run entries of this CTA's bins as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj)
   // (interior tiles: the yaw chain table; border tiles: full rows)
@@ -713,7 +752,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
       c.e0 = __ldg(tab_off + k) - tab_base;
       c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
       c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
-      c.restart = (b == 0 || seg_restart(p.H, p.seg, k)) ? 1 : 0;
+      c.restart = (b == 0 || __ldg(p.seg_rst + k)) ? 1 : 0;
       c.f0 = __ldg(p.full_off + k) - full_base;
       c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
       c.pad0 = c.pad1 = 0;
@@ -893,24 +932,14 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
     constexpr bool T = decltype(tm)::value;
     constexpr bool MASKED = decltype(masked)::value;
     constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
-    // per-bin output bases, advanced by one plane per bin (no 64-bit multiplies in the loop)
-    float4* outk = p.out + (size_t)kb * plane;
-    float4* outk2 = outk + (size_t)p.H * plane;
-    uint32_t* travk = p.trav + (size_t)kb * twplane;
-    uint32_t* travk2 = travk + (size_t)p.H * twplane;
-    uint32_t* twk = twd;
+    // (the per-bin output bases are formed where they are used, from the bin index: loop-carried 64-bit pointers
+    // cost registers the epilogue needs)
     const BinC* bc_k = bins_s;
-    for (int k = kb; k < ke; ++k, ++bc_k, outk += plane, outk2 += plane, travk += twplane, travk2 += twplane, twk += 32) {
+    for (int k = kb; k < ke; ++k, ++bc_k) {
       const int4 meta = *reinterpret_cast<const int4*>(bc_k);  // (e0, npre, nr, restart)
       const int4* rk = tabc + meta.x;
       const int nr = meta.z;
       const bool restart = meta.w != 0;
-      // interior pairs' states all lie inside the window (their whole halo band does), so each is stored
-      auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
-        SE2M_CHK(off >= 0 && off < (int)plane && rec_ok(outk + off) && (!p.paired || rec_ok(outk2 + off)));
-        __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
-        if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
-      };
       // ---- 4 moments per state from {P0, P2} and PX; geometry is per-bin constant.  At a chain restart
       // the entries are the full rows of bin k, otherwise the corrections from k-1.
       if (restart) {
@@ -971,6 +1000,14 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
       if (k < p.k_store) continue;  // chain replay only (a yaw shard's first segment): nothing to store
       const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
       const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
+      float4* const outk = p.out + (size_t)k * plane;
+      float4* const outk2 = outk + (size_t)p.H * plane;
+      // interior pairs' states all lie inside the window (their whole halo band does), so each is stored
+      auto store_rec = [&](int off, float risk, float pitch, float roll, float z) {
+        SE2M_CHK(off >= 0 && off < (int)plane && rec_ok(outk + off) && (!p.paired || rec_ok(outk2 + off)));
+        __stcs(outk + off, make_float4(risk, pitch, roll, z));  // write-once stream: evict-first stores
+        if (p.paired) __stcs(outk2 + off, make_float4(risk, -pitch, -roll, z));
+      };
       unsigned tmine = 0;
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
@@ -994,9 +1031,11 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
         }
       }
       if (T) {  // OR into the tile's words in shared memory (flushed once at the end)
-        SE2M_CHK(twk + lane - twd < (ke - kb) * 32);
-        if (tmine) atomicOr(twk + lane, tmine);
+        SE2M_CHK((k - kb) * 32 + lane < (ke - kb) * 32);
+        if (tmine) atomicOr(twd + (k - kb) * 32 + lane, tmine);
       } else if (tmy >= 0 && (!MASKED || (pfast >> (lane >> 1) & 1u))) {  // lane s writes state s's word
+        uint32_t* const travk = p.trav + (size_t)k * twplane;
+        uint32_t* const travk2 = travk + (size_t)p.H * twplane;
         SE2M_CHK(word_ok(travk + tmy) && (!p.paired || word_ok(travk2 + tmy)));
         travk[tmy] = tmine;
         if (p.paired) travk2[tmy] = tmine;
@@ -1208,12 +1247,18 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
     }
   };
 
+  SE2M_PHASE(3);
+#ifdef SE2M_PHASES
+  if (lane == 0 && ph_slot >= 0 && ph_slot < kPhaseSlots)
+    g_phase[ph_slot].flags = (fast ? 1 : 0) | (int)(pin << 8) | (int)(pfast << 16);
+#endif
   if (fast) {
     interior(std::integral_constant<bool, tmode>{}, std::false_type{});
   } else {
     if (pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
     if (pin & ~pfast) border(std::integral_constant<bool, tmode>{});
   }
+  SE2M_PHASE(4);
   if (tmode) {  // flush the tile's traversable words: one plain store per (bin, row) word (+ its pair bin)
     __syncthreads();
     const int kz = max(kb, p.k_store);
@@ -1227,6 +1272,30 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
       if (p.paired) p.trav[w + (size_t)p.H * twplane] = v;
     }
   }
+  SE2M_PHASE(5);
+}
+
+// se2m_debug_phases: copy (and optionally reset) the phase records; *n = records written since the last reset
+cudaError_t debug_phases(void* out, long long max_records, int reset, long long* n, cudaStream_t s) {
+#ifdef SE2M_PHASES
+  unsigned int cnt = 0;
+  cudaError_t e = cudaMemcpyFromSymbolAsync(&cnt, g_phase_n, sizeof cnt, 0, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *n = cnt;
+  const long long m = std::min<long long>(std::min<long long>(cnt, kPhaseSlots), max_records);
+  if (out && m > 0) e = cudaMemcpyFromSymbolAsync(out, g_phase, (size_t)m * sizeof(PhaseRec), 0, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && reset) {
+    const unsigned int z = 0;
+    e = cudaMemcpyToSymbolAsync(g_phase_n, &z, sizeof z, 0, cudaMemcpyHostToDevice, s);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+#else
+  (void)out; (void)max_records; (void)reset; (void)s;
+  *n = -1;
+  return cudaErrorNotSupported;
+#endif
 }
 
 template <int R_T, int MODE>

@@ -65,6 +65,9 @@ struct AssessParams {
   // segment bound floor(H s / S) (seg_bound); S = H: no chain.  A CTA takes seg_chunk consecutive segments
   // (its chunk): blockIdx.y covers segments [s0 + c y, s0 + c (y + 1)), s0 = the segment of k_begin.
   int seg, seg_chunk, n_chunks;
+  int seg_first;                // the segment of k_begin
+  const int* segb;              // [seg + 1] segment bounds seg_bound(s)
+  const unsigned char* seg_rst; // [H] 1 where a bin is a segment bound (chain restart)
   int tab_cap;           // max entries of one CTA's chunk (shared-memory table size)
   const float4* geo;     // [H] full-stencil (N, Sxx, Sxy, Syy) in cell units (Sx = Sy = 0)
   const float4* geoc;    // [H][4] full-stencil geometry for interior tiles (see assess.cu, arrow2), metres
@@ -101,20 +104,14 @@ struct AssessParams {
 // Yaw-chain segments (AssessParams::seg): segment s covers representative bins [seg_bound(s), seg_bound(s + 1)).
 // With S <= H every segment holds >= 1 bin; the balanced yaw shards of se2m_shard_plan, [H g / G, H (g + 1) / G),
 // start on segment bounds whenever G divides S (a shard starting elsewhere replays from its segment's bound).
-// (32-bit: H * S <= n_yaw^2 < 2^31 — se2m_init limits n_yaw to 4096)
-#ifdef SE2M_SEG64
-__host__ __device__ inline int seg_bound(int H, int S, int s) { return (int)((long long)H * s / S); }
-__host__ __device__ inline int seg_of(int H, int S, int k) {
+// (host side; the kernels read the bounds and restart flags from tables built from these)
+inline int seg_bound(int H, int S, int s) { return (int)((long long)H * s / S); }
+inline int seg_of(int H, int S, int k) {
   int s = (int)((long long)k * S / H);
-#else
-__host__ __device__ inline int seg_bound(int H, int S, int s) { return H * s / S; }
-__host__ __device__ inline int seg_of(int H, int S, int k) {
-  int s = k * S / H;
-#endif
   if (s + 1 <= S && seg_bound(H, S, s + 1) <= k) ++s;  // (at most one step: segments hold >= 1 bin)
   return s;
 }
-__host__ __device__ inline bool seg_restart(int H, int S, int k) { return seg_bound(H, S, seg_of(H, S, k)) == k; }
+inline bool seg_restart(int H, int S, int k) { return seg_bound(H, S, seg_of(H, S, k)) == k; }
 
 // Launch the assess kernel (one CTA per (tile, yaw chunk)).  Returns cudaSuccess or the launch error.
 // dynamic shared memory of one assess CTA (halo, prefix planes, h^ plane, run tables of tab_cap entries)
@@ -126,6 +123,9 @@ int assess_ctas_per_sm(int R_T, size_t smem);
 cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
                           cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join,
                           int* n_launch);
+
+// SE2M_PHASES debug builds: per-warp phase timestamps of the assess kernel (PhaseRec in assess.cu: 6 x u64 + 4 x i32)
+cudaError_t debug_phases(void* out, long long max_records, int reset, long long* n, cudaStream_t s);
 
 // Small helpers (same file as the kernels).
 // se2m_step: the window cells that entered (up to 2 logical rectangles (i0, j0, w, h)) from a device

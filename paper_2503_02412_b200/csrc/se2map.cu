@@ -65,6 +65,8 @@ struct se2m_map {
   double sdf_dmax = 0;
   int4* d_full = nullptr;   // run-entry tables (see AssessParams)
   int4* d_full_fmt = nullptr;
+  int* d_segb = nullptr;              // [seg + 1] yaw-chain segment bounds
+  unsigned char* d_seg_rst = nullptr; // [H] chain restart flags
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
   int* d_chain_off = nullptr;
@@ -330,6 +332,7 @@ static AssessParams make_params(const se2m_map* m) {
   p.n_yaw = m->prm.n_yaw; p.H = m->H; p.paired = m->paired; p.R = m->R;
   p.full = m->d_full; p.full_fmt = m->d_full_fmt; p.full_off = m->d_full_off; p.chain = m->d_chain; p.chain_off = m->d_chain_off; p.chain_mid = m->d_chain_mid;
   p.seg = m->seg; p.seg_chunk = 1; p.n_chunks = 0;
+  p.segb = m->d_segb; p.seg_rst = m->d_seg_rst;
   p.geo = m->d_geo; p.geoc = m->d_geoc; p.cs = m->d_cs;
   p.r = (float)m->prm.resolution;
   p.kappa_max = (float)m->prm.kappa_max; p.phi_x_max = (float)m->prm.phi_x_max; p.phi_y_max = (float)m->prm.phi_y_max;
@@ -337,7 +340,8 @@ static AssessParams make_params(const se2m_map* m) {
   p.wx = (float)(m->prm.w_r[1] / m->prm.phi_x_max);
   p.wy = (float)(m->prm.w_r[2] / m->prm.phi_y_max);
   // the launch starts at the chain restart at or before the first owned bin (replayed, not stored)
-  p.k_begin = seg_bound(m->H, m->seg, seg_of(m->H, m->seg, m->k_lo)); p.k_end = m->k_hi; p.k_store = m->k_lo;
+  p.seg_first = seg_of(m->H, m->seg, m->k_lo);
+  p.k_begin = seg_bound(m->H, m->seg, p.seg_first); p.k_end = m->k_hi; p.k_store = m->k_lo;
   p.k_chunk = 1;
   p.use_tma = m->tma_ok ? 1 : 0;
   p.force_general = m->force_general ? 1 : 0;
@@ -587,6 +591,8 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
       {(void**)&m->d_geo, geo.size() * sizeof(float4), "geo"},
       {(void**)&m->d_geoc, geoc.size() * sizeof(float4), "geoc"},
       {(void**)&m->d_cs, cs.size() * sizeof(float2), "cs"},
+      {(void**)&m->d_segb, (size_t)(m->seg + 1) * sizeof(int), "segment bounds"},
+      {(void**)&m->d_seg_rst, (size_t)m->H, "restart flags"},
   };
   for (auto& a : allocs) {
     e = cudaMalloc(a.ptr, a.bytes);
@@ -603,7 +609,13 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     memcpy(&dji, &dj, 4);
     full_fmt[q] = make_int4(full[q].x * 8, full[q].y * 8, full[q].x * 4, dji);
   }
-  if ((e = cudaMemcpyAsync(m->d_full, full.data(), full.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+  std::vector<int> segb(m->seg + 1);
+  std::vector<unsigned char> seg_rst(m->H);
+  for (int q = 0; q <= m->seg; ++q) segb[q] = seg_bound(m->H, m->seg, q);
+  for (int k = 0; k < m->H; ++k) seg_rst[k] = seg_restart(m->H, m->seg, k) ? 1 : 0;
+  if ((e = cudaMemcpyAsync(m->d_segb, segb.data(), segb.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_seg_rst, seg_rst.data(), seg_rst.size(), cudaMemcpyHostToDevice, m->stream)) ||
+      (e = cudaMemcpyAsync(m->d_full, full.data(), full.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_full_fmt, full_fmt.data(), full_fmt.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_full_off, m->full_off.data(), m->full_off.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
       (e = cudaMemcpyAsync(m->d_chain, chain.data(), chain.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
@@ -649,7 +661,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
   DevGuard dev_guard_(m->prm.device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   void* ptrs[] = {m->d_sdf, m->d_var, m->d_pts, m->fe.key, m->fe.idx, m->fe.skey, m->fe.sidx, m->fe.meas,
-                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_fmt, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
+                  m->fe.counts, m->fe.bbox, m->fe.temp, m->d_h, m->d_out, m->d_trav, m->d_full, m->d_full_fmt, m->d_segb, m->d_seg_rst, m->d_full_off, m->d_chain, m->d_chain_off, m->d_chain_mid, m->d_geo, m->d_geoc,
                   m->d_cs, m->d_stage, m->d_qxyt, m->d_qout, m->d_qcnt, m->d_hin, m->d_site, m->d_ipc, m->d_sdf_g};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -1641,6 +1653,16 @@ extern "C" se2m_status se2m_synchronize(se2m_map* m) {
 }
 
 extern "C" int64_t se2m_launch_count(const se2m_map* m) { return m ? m->launches : 0; }
+
+extern "C" se2m_status se2m_debug_phases(se2m_map* m, void* out, int64_t max_records, int32_t reset, int64_t* n) {
+  SE2M_ENTER(m);
+  long long cnt = 0;
+  const cudaError_t e = debug_phases(out, max_records, reset, &cnt, m->stream);
+  if (n) *n = cnt;
+  if (e == cudaErrorNotSupported) return fail(m, SE2M_ERR_UNSUPPORTED, "debug_phases: library built without SE2M_PHASES");
+  if (e != cudaSuccess) return cuda_fail(m, e, "debug_phases");
+  return SE2M_OK;
+}
 
 extern "C" const char* se2m_last_error(const se2m_map* m) {
   return m ? m->err.c_str() : g_init_error.c_str();

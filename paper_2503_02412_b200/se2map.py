@@ -34,7 +34,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
            "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
            "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo", "se2m_nccl_unique_id",
-           "se2m_query_trilinear_async"]
+           "se2m_query_trilinear_async", "se2m_debug_phases"]
 
 
 class Params(ctypes.Structure):
@@ -68,6 +68,26 @@ class Pose(ctypes.Structure):
 
 
 _lib = ctypes.CDLL(_LIB_PATH)
+if os.environ.get("SE2M_LIB"):  # an A/B build may predate some entry points: give the missing ones a stub
+    class _Missing:
+        def __init__(self, name):
+            self.name = name
+
+        def __call__(self, *a):
+            raise RuntimeError("%s is not exported by %s" % (self.name, _LIB_PATH))
+
+    class _LibView:
+        def __init__(self, lib):
+            self._lib = lib
+
+        def __getattr__(self, name):
+            try:
+                return getattr(self._lib, name)
+            except AttributeError:
+                stub = _Missing(name)
+                setattr(self, name, stub)
+                return stub
+    _lib = _LibView(_lib)
 _vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 _lib.se2m_default_params.argtypes = [ctypes.POINTER(Params)]
 _lib.se2m_default_params.restype = None
@@ -105,6 +125,7 @@ _lib.se2m_halo_unpack.argtypes = [_vp, _i32, _vp]
 _lib.se2m_halo_plan.argtypes = [ctypes.POINTER(Params), _i64, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                                 _vp]
 _lib.se2m_exchange_halo.argtypes = [_vp]
+_lib.se2m_debug_phases.argtypes = [_vp, _vp, _i64, _i32, ctypes.POINTER(_i64)]
 _lib.se2m_query_trilinear_async.argtypes = [_vp, _i64, _vp, _i32, _vp, _i32]
 _lib.se2m_nccl_unique_id.argtypes = [_vp, _i32, ctypes.POINTER(_i32)]
 _lib.se2m_launch_count.argtypes = [_vp]
@@ -117,7 +138,7 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
               "se2m_halo_plan", "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo",
-              "se2m_nccl_unique_id", "se2m_query_trilinear_async"):
+              "se2m_nccl_unique_id", "se2m_query_trilinear_async", "se2m_debug_phases"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -513,6 +534,14 @@ class Se2Map:
         map's stream (needs the map created with nccl_unique_id).  Call after update_elevation of the rank's own
         rows and before assess_se2."""
         return self._check(_lib.se2m_exchange_halo(self.h))
+
+    def debug_phases(self, max_records: int = 1 << 17, reset: bool = True):
+        """SE2M_PHASES builds only: the assess kernels' per-warp phase records as a structured NumPy array."""
+        dt = np.dtype([("t", np.uint64, 6), ("bx", np.int32), ("by", np.int32), ("mode", np.int32), ("flags", np.int32)])
+        out = np.zeros(max_records, dt)
+        n = _i64()
+        self._check(_lib.se2m_debug_phases(self.h, out.ctypes.data, max_records, 1 if reset else 0, ctypes.byref(n)))
+        return out[:min(n.value, max_records)]
 
     def launch_count(self) -> int:
         return int(_lib.se2m_launch_count(self.h))

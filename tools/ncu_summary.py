@@ -147,9 +147,13 @@ def main():
         if v.get("dram__bytes_read.sum") is not None and v.get("dram__bytes_write.sum") is not None:
             tot += v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"]
     s["dram_bytes_per_launch"] = tot        # one assess call: every captured kernel
+    def insts(m):
+        return num(m.get(("Instruction Statistics", "Executed Instructions"), ("", ""))[0]) or 0.0
     s["kernels"] = [{"name": dk[k][1].split("(")[0], "duration_ms": dur_ms(dk[k][0]),
-                     "dram_bytes": (per[i].get("dram__bytes_read.sum") or 0) + (per[i].get("dram__bytes_write.sum") or 0)}
+                     "dram_bytes": (per[i].get("dram__bytes_read.sum") or 0) + (per[i].get("dram__bytes_write.sum") or 0),
+                     "executed_instructions": insts(dk[k][0])}
                     for i, k in enumerate(order)]
+    s["executed_instructions_per_call"] = sum(kk["executed_instructions"] for kk in s["kernels"])
     if a.launches:
         s["launch_shares"] = launches(a.launches)
     s["hot_lines"] = hot_lines(a.rep)
