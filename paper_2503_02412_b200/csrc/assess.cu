@@ -636,6 +636,43 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
     for (int q = 0; q < NLD; ++q)
       if (tid + q * NTHREADS < HX * HY) raw[tid + q * NTHREADS] = v[q];
   }
+
+  // ---- 1b. while the halo is in flight: the chunk's run tables and per-bin constants into shared memory ------
+  // run entries as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj) — the yaw-chain table (shared-
+  // memory format) for every tile, then the full rows of each bin (border / unknown tiles and the direct path)
+  const int* tab_off = p.chain_off;
+  const int tab_base = __ldg(tab_off + kb);
+  const int full_base = __ldg(p.full_off + kb);
+  int n_chain = 0;
+  if (G::CB) {
+    n_chain = __ldg(tab_off + ke) - tab_base;
+    const int n_full = __ldg(p.full_off + ke) - full_base;
+    SE2M_CHK(n_chain + n_full <= p.tab_cap);
+    for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
+    for (int idx = tid; idx < n_full; idx += NTHREADS) runs_s[n_chain + idx] = __ldg(p.full_fmt + full_base + idx);
+  }
+  for (int b = tid; b < ke - kb; b += NTHREADS) {  // per-bin constants of the chunk (gq after the tile plane)
+    const int k = kb + b;
+    BinC c;
+    c.e0 = __ldg(tab_off + k) - tab_base;
+    c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
+    c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
+    c.restart = (b == 0 || __ldg(p.seg_rst + k)) ? 1 : 0;
+    c.f0 = __ldg(p.full_off + k) - full_base;
+    c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
+    c.pad0 = c.pad1 = 0;
+    const float2 csk = __ldg(p.cs + k);
+    c.cs = make_float4(csk.x, csk.y, 0.f, 0.f);
+    c.gc = __ldg(p.geoc + 4 * k); c.gd = __ldg(p.geoc + 4 * k + 1);
+    c.ge = __ldg(p.geoc + 4 * k + 2); c.gf = __ldg(p.geoc + 4 * k + 3);
+    c.gq = make_float4(0.f, 0.f, 0.f, 0.f);
+    bins_s[b] = c;
+  }
+  // T-mode: the tile's traversable words of the chunk accumulate in shared memory (zeroed here, ORed by the
+  // warps, flushed once at the end: the tile's 32 columns are one world-aligned word per row)
+  if (tmode)
+    for (int idx = tid; idx < (ke - kb) * 32; idx += NTHREADS) twd[idx] = 0u;
+
   __syncthreads();
   if (via_tma) mbar_wait(bar, 0);
   SE2M_PHASE(1);
@@ -727,49 +764,27 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   const bool fast = tplane[3] > 0.5f && !p.force_general;
   SE2M_PHASE(2);
 
-  // run entries of this CTA's bins as byte offsets into the prefix arrays: (8 e-, 8 e+, 4 e-, dj)
-  // (interior tiles: the yaw chain table; border tiles: full rows)
-  // run tables of the chunk's bins: the yaw-chain table (shared-memory format) for every tile, and for
-  // border / unknown tiles also the full rows of each bin (the direct path walks whole footprints)
-  const int* tab_off = p.chain_off;
-  const int tab_base = __ldg(tab_off + kb);
-  const int n_chain = (fast || G::CB) ? __ldg(tab_off + ke) - tab_base : 0;
-  const int full_base = __ldg(p.full_off + kb);
-  SE2M_CHK(n_chain + (fast ? 0 : __ldg(p.full_off + ke) - full_base) <= p.tab_cap);
-  for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
-  if (!fast)
-    for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS)
-      runs_s[n_chain + idx] = __ldg(p.full_fmt + full_base + idx);
+  // run tables: border tiles of R_T = 32 maps (no border chain, see chain_border) take the full rows only
+  if (!G::CB) {
+    n_chain = fast ? __ldg(tab_off + ke) - tab_base : 0;
+    SE2M_CHK(n_chain + (fast ? 0 : __ldg(p.full_off + ke) - full_base) <= p.tab_cap);
+    if (fast)
+      for (int idx = tid; idx < n_chain; idx += NTHREADS) runs_s[idx] = __ldg(p.chain + tab_base + idx);
+    else
+      for (int idx = tid; idx < __ldg(p.full_off + ke) - full_base; idx += NTHREADS)
+        runs_s[idx] = __ldg(p.full_fmt + full_base + idx);
+  }
   // the chunk's chain entries and full-row entries in shared memory
   const int4* tabc = runs_s;
   const int4* tabf = runs_s + n_chain;
-
-  {  // per-bin constants of the chunk
+  {  // the tile plane's gradient in each bin's footprint eigenbasis (the rest of BinC was filled before)
     const float Gx = pgx / p.r, Gy = pgy / p.r;
     for (int b = tid; b < ke - kb; b += NTHREADS) {
-      const int k = kb + b;
-      BinC c;
-      c.e0 = __ldg(tab_off + k) - tab_base;
-      c.npre = __ldg(p.chain_mid + k) - __ldg(tab_off + k);
-      c.nr = __ldg(tab_off + k + 1) - __ldg(tab_off + k);
-      c.restart = (b == 0 || __ldg(p.seg_rst + k)) ? 1 : 0;
-      c.f0 = __ldg(p.full_off + k) - full_base;
-      c.nf = __ldg(p.full_off + k + 1) - __ldg(p.full_off + k);
-      c.pad0 = c.pad1 = 0;
-      const float2 csk = __ldg(p.cs + k);
-      c.cs = make_float4(csk.x, csk.y, 0.f, 0.f);
-      c.gc = __ldg(p.geoc + 4 * k); c.gd = __ldg(p.geoc + 4 * k + 1);
-      c.ge = __ldg(p.geoc + 4 * k + 2); c.gf = __ldg(p.geoc + 4 * k + 3);
+      BinC& c = bins_s[b];
       const float Gq1 = fmaf(Gx, c.ge.x, Gy * c.ge.y), Gq2 = fmaf(Gy, c.ge.x, -Gx * c.ge.y);
       c.gq = make_float4(Gq1, Gq2, c.gd.y * Gq1, c.gd.z * Gq2);
-      bins_s[b] = c;
     }
   }
-
-  // T-mode: the tile's traversable words of the chunk accumulate in shared memory (zeroed here, ORed by the
-  // warps, flushed once at the end: the tile's 32 columns are one world-aligned word per row)
-  if (tmode)
-    for (int idx = tid; idx < (ke - kb) * 32; idx += NTHREADS) twd[idx] = 0u;
 
   // ---- 3. per-row exclusive prefix sums (warp w: rows w, w+8, ...) ---------------------------
   for (int row = warp; row < HY; row += NWARPS) {

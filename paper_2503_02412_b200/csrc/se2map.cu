@@ -113,6 +113,9 @@ struct se2m_map {
   // row-band halo transport (se2m_exchange_halo): the library's NCCL communicator and its 4 device slab
   // buffers (to g - 1, to g + 1, from g + 1, from g - 1), allocated on first use
   ncclComm_t comm = nullptr;
+  // se2m_step as a CUDA graph (params.step_graph): the executable graph, updated in place every step
+  cudaGraphExec_t step_exec = nullptr;
+  bool step_warm = false;  // one direct step ran (lazy allocations / attributes done before any capture)
   float* d_halo[4] = {nullptr, nullptr, nullptr, nullptr};
   std::string err;
 };
@@ -371,6 +374,7 @@ extern "C" void se2m_default_params(se2m_params* p) {
   p->kappa_max = 0.1; p->phi_x_max = 0.52; p->phi_y_max = 0.52;
   p->world_size = 1;
   p->fe_z_min = -1.5; p->fe_z_max = 1.5; p->fe_gate = 2.0; p->fe_ray_eps = 0.05; p->fe_prior_var = 1e-4;
+  p->step_graph = 0;  // (measured: no gain on the stream step, whose device time is the assess kernel's)
 }
 
 static se2m_status validate(const se2m_params* p) {
@@ -684,6 +688,7 @@ extern "C" void se2m_destroy(se2m_map* m) {
   for (float* b : m->d_halo)
     if (b) cudaFree(b);
   if (m->comm) nccl_api().CommDestroy(m->comm);  // after the stream drained: no transfer in flight
+  if (m->step_exec) cudaGraphExecDestroy(m->step_exec);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }
@@ -803,20 +808,59 @@ extern "C" se2m_status se2m_step(se2m_map* m, double x, double y, const float* w
   recentre(m, x, y, &di, &dj, strips, &ns, &all);
   clamp_out(di, out_di);
   clamp_out(dj, out_dj);
+  FillArgs f;
   if (ns > 0) {
-    FillArgs f;
     f.h = m->d_h; f.var = m->d_var; f.prior_var = (float)m->prm.fe_prior_var; f.ldh = m->ldh;
     f.nx = m->prm.nx; f.ny = m->prm.ny; f.pxM = pmod(m->I_M, f.nx); f.pyM = pmod(m->J_M, f.ny);
     f.I_M = m->I_M; f.J_M = m->J_M;
     f.world = world; f.world_ld = world_ld; f.wI0 = world_I0; f.wJ0 = world_J0; f.ww = world_w; f.wh = world_h;
     f.n = ns;
     for (int q = 0; q < ns; ++q) f.rect[q] = strips[q];
-    CUDA_TRY(m, launch_fill_strips(f, m->stream), "fill strips");
-    m->launches++;
-    m->have_data = true;
   }
-  if (!m->have_data) return SE2M_OK;  // nothing to assess yet
-  return se2m_assess_se2(m, SE2M_INCREMENTAL);
+  // the step's launches: strip fill (H1 + H2), then INCREMENTAL assess (H9)
+  auto launches = [&]() -> se2m_status {
+    if (ns > 0) {
+      CUDA_TRY(m, launch_fill_strips(f, m->stream), "fill strips");
+      m->launches++;
+      m->have_data = true;
+    }
+    if (!m->have_data) return SE2M_OK;  // nothing to assess yet
+    return se2m_assess_se2(m, SE2M_INCREMENTAL);
+  };
+  const bool graph = m->prm.step_graph && !m->prm.inpaint && m->step_warm;
+  if (!graph) {  // direct launches (the first step also makes the lazy allocations no capture may contain)
+    const se2m_status st = launches();
+    if (st == SE2M_OK && m->have_data) m->step_warm = true;
+    return st;
+  }
+  if (!m->edge_stream) {  // the assess may fork onto the edge stream: create it outside the capture
+    CUDA_TRY(m, cudaStreamCreateWithFlags(&m->edge_stream, cudaStreamNonBlocking), "cudaStreamCreate(edge)");
+    CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  CUDA_TRY(m, cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+  const se2m_status st = launches();
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(m->stream, &g);
+  if (st != SE2M_OK || ec != cudaSuccess || !g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return st != SE2M_OK ? st : cuda_fail(m, ec, "end capture");
+  }
+  if (m->step_exec) {  // same topology as last step (the usual case): update the kernel parameters in place
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(m->step_exec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(m->step_exec);
+      m->step_exec = nullptr;
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!m->step_exec) e = cudaGraphInstantiate(&m->step_exec, g, 0);
+  if (e == cudaSuccess) e = cudaGraphLaunch(m->step_exec, m->stream);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(m, e, "step graph");
+  return SE2M_OK;
 }
 
 

@@ -48,7 +48,7 @@ class Params(ctypes.Structure):
                 ("chain_segments", ctypes.c_int32), ("cuda_stream", ctypes.c_void_p),
                 ("fe_z_min", ctypes.c_double), ("fe_z_max", ctypes.c_double), ("fe_gate", ctypes.c_double),
                 ("fe_ray_eps", ctypes.c_double), ("fe_prior_var", ctypes.c_double),
-                ("inpaint", ctypes.c_int32), ("reserved1", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
+                ("inpaint", ctypes.c_int32), ("step_graph", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
 
 
 class Pose(ctypes.Structure):

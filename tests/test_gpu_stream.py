@@ -186,7 +186,8 @@ def test_chain_map_incremental_and_sharded(n_yaw):
     assert rep["ok"], rep
 
 
-def test_step_equals_separate_calls():
+@pytest.mark.parametrize("step_graph", [0, 1])
+def test_step_equals_separate_calls(step_graph):
     """se2m_step (recentre + fill the entered cells from a device world plane + INCREMENTAL) gives the
     same state records, bit for bit, as shift_window + update_elevation(strips) + assess(INCREMENTAL),
     including cells outside the world plane (unknown) and a jump larger than the window."""
@@ -195,7 +196,7 @@ def test_step_equals_separate_calls():
     nx, ny, r, n_yaw = cfg["nx"], cfg["ny"], cfg["r"], cfg["n_yaw"]
     terrain = cfg["terrain"]
     a = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
-    b = make_map(nx, ny, r, n_yaw, robot=cfg["robot"])
+    b = make_map(nx, ny, r, n_yaw, robot=cfg["robot"], step_graph=step_graph)  # 1: the step as one CUDA graph
     I0, J0 = a.origin()
     WI0, WJ0, WW, WH = I0 - 40, J0 - 30, nx + 90, ny + 60          # world plane (partly smaller than the path)
     world = world_heights(terrain, WI0, WJ0, WW, WH, r)
