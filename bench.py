@@ -728,7 +728,7 @@ def small_configs(S, stream, torch):
                 out["paper_full_us"] = e0.elapsed_time(e1) * 10.0
                 out["paper_states"] = nx * ny * n_yaw
             else:
-                path = robot_path(cfg["path_seed"], 300, r, *cfg["robot"])
+                path = robot_path(cfg["path_seed"], cfg["n_steps"] + 20, r, *cfg["robot"])  # 20 warm + 1000 timed
                 # strips come from a pre-generated world patch covering the path
                 xs, ys = path[:, 0], path[:, 1]
                 I0 = int(math.floor(xs.min() / r)) - nx // 2 - 2
