@@ -499,7 +499,19 @@ struct BinC {
 
 // State s of a thread sits so_of(s, nw) tile rows (T-mode: columns) after its first one: pairs of neighbouring
 // rows spread 2 nw apart (nw warps per CTA), so every warp holds states in every part of the tile.
-__host__ __device__ constexpr int so_of(int s, int nw) { return (s & 1) + (s >> 1) * 2 * nw; }
+// Code-generation knobs (B200 A/B under bench conditions, large map): the spread pair layout and the
+// masked interior pass both measured slower there (1.124 / 1.125 vs 1.079 ms), and so did a replay loop split off
+// the bin loop (1.129 ms) although it spilled less — the defaults reproduce the best measured code.
+#ifndef SE2M_PAIR_SPREAD
+#define SE2M_PAIR_SPREAD 0
+#endif
+#ifndef SE2M_MASKED
+#define SE2M_MASKED 0
+#endif
+#ifndef SE2M_SPLIT_REPLAY
+#define SE2M_SPLIT_REPLAY 0
+#endif
+__host__ __device__ constexpr int so_of(int s, int nw) { return (s & 1) + (s >> 1) * (SE2M_PAIR_SPREAD ? 2 * nw : 2); }
 
 template <int R_T>
 struct Geom {
@@ -851,12 +863,12 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   // window edge, which take the general path) are shared by all warps instead of being the work of one or
   // two of them.  Row mode: lane = column; T-mode: lane = row.  State s of a thread is at offset so(s) =
   // (s & 1) + (s >> 1) PS from tr0 along the state direction.
-  constexpr int PS = 2 * NWARPS;
+  constexpr int PS = SE2M_PAIR_SPREAD ? 2 * NWARPS : 2;
   constexpr int NP = RPW / 2;
   const size_t plane = (size_t)p.nx * p.ny;
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
   const size_t twplane = (size_t)p.ny * p.trav_words;
-  const int tr0 = 2 * warp;
+  const int tr0 = SE2M_PAIR_SPREAD ? 2 * warp : RPW * warp;
   const int trow0 = tmode ? lane : tr0, tcol0 = tmode ? tr0 : lane;
   const float xs = (float)(tcol0 - TX / 2);  // x' of state 0 (T-mode: state s at xs + so(s))
   const long long li = TI * TX + lane - p.I_M;
@@ -949,8 +961,8 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
     constexpr int S8 = T ? 8 : RS8, S4 = T ? 4 : RS4;
     // (the per-bin output bases are formed where they are used, from the bin index: loop-carried 64-bit pointers
     // cost registers the epilogue needs)
-    const BinC* bc_k = bins_s;
-    for (int k = kb; k < ke; ++k, ++bc_k) {
+    // the moments of bin k from those of k - 1 (or from whole rows at a restart)
+    auto moments = [&](const BinC* bc_k) {
       const int4 meta = *reinterpret_cast<const int4*>(bc_k);  // (e0, npre, nr, restart)
       const int4* rk = tabc + meta.x;
       const int nr = meta.z;
@@ -1012,7 +1024,18 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
           SYp[q] = fma2(bc(sdj), h, SYp[q]);
         }
       }
+    };
+    const BinC* bc_k = bins_s;
+    int k = kb;
+#if SE2M_SPLIT_REPLAY
+    // chain replay only (a yaw shard starting inside a segment, AssessParams::k_store): nothing to store
+    for (const int kr = min(ke, p.k_store); k < kr; ++k, ++bc_k) moments(bc_k);
+#endif
+    for (; k < ke; ++k, ++bc_k) {
+      moments(bc_k);
+#if !SE2M_SPLIT_REPLAY
       if (k < p.k_store) continue;  // chain replay only (a yaw shard's first segment): nothing to store
+#endif
       const float4 gc = bc_k->gc, gd = bc_k->gd, ge = bc_k->ge, gf = bc_k->gf, gq = bc_k->gq;
       const float Gq1 = gq.x, Gq2 = gq.y, aG1 = gq.z, aG2 = gq.w;
       float4* const outk = p.out + (size_t)k * plane;
@@ -1267,10 +1290,11 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   if (lane == 0 && ph_slot >= 0 && ph_slot < kPhaseSlots)
     g_phase[ph_slot].flags = (fast ? 1 : 0) | (int)(pin << 8) | (int)(pfast << 16);
 #endif
-  if (fast) {
+  if (!SE2M_MASKED && !fast && pfast != (1u << NP) - 1u) pfast = 0;  // (A/B: all-or-nothing per warp)
+  if (fast || (!SE2M_MASKED && pfast == (1u << NP) - 1u)) {
     interior(std::integral_constant<bool, tmode>{}, std::false_type{});
   } else {
-    if (pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
+    if (SE2M_MASKED && pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
     if (pin & ~pfast) border(std::integral_constant<bool, tmode>{});
   }
   SE2M_PHASE(4);

@@ -1,0 +1,9 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in r01 d p1 p4 c1 c3 c4 sp spc4; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 600 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | sed "s#^#$v #"
+done
+done > gpurun_out/r_bench_ab.txt 2>&1
+echo "bench ab rc=$?"
