@@ -119,7 +119,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)   # ~2 ms: several samples even in a ~25 ms timed region
 
     def __enter__(self):
         if self.ok:

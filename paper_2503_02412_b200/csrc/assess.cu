@@ -511,7 +511,10 @@ struct BinC {
 #ifndef SE2M_SPLIT_REPLAY
 #define SE2M_SPLIT_REPLAY 0
 #endif
-__host__ __device__ constexpr int so_of(int s, int nw) { return (s & 1) + (s >> 1) * (SE2M_PAIR_SPREAD ? 2 * nw : 2); }
+#ifndef SE2M_TMODE_SPREAD
+#define SE2M_TMODE_SPREAD 1   // the T-mode (edge) kernel: spread pairs + masked pass (bench 1.077 vs 1.083 ms; G = 8 balance 0.60 vs 0.59)
+#endif
+__host__ __device__ constexpr int so_of(int s, int nw, bool spread) { return (s & 1) + (s >> 1) * (spread ? 2 * nw : 2); }
 
 template <int R_T>
 struct Geom {
@@ -863,12 +866,14 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   // window edge, which take the general path) are shared by all warps instead of being the work of one or
   // two of them.  Row mode: lane = column; T-mode: lane = row.  State s of a thread is at offset so(s) =
   // (s & 1) + (s >> 1) PS from tr0 along the state direction.
-  constexpr int PS = SE2M_PAIR_SPREAD ? 2 * NWARPS : 2;
+  constexpr bool SPREAD = MODE == 1 ? SE2M_TMODE_SPREAD : SE2M_PAIR_SPREAD;  // (MASKED follows it in T-mode)
+  constexpr bool MASK = MODE == 1 ? SE2M_TMODE_SPREAD : SE2M_MASKED;
+  constexpr int PS = SPREAD ? 2 * NWARPS : 2;
   constexpr int NP = RPW / 2;
   const size_t plane = (size_t)p.nx * p.ny;
   const int gword = (int)(((TI % p.trav_words) + p.trav_words) % p.trav_words);  // floor(I/32) = TI
   const size_t twplane = (size_t)p.ny * p.trav_words;
-  const int tr0 = SE2M_PAIR_SPREAD ? 2 * warp : RPW * warp;
+  const int tr0 = SPREAD ? 2 * warp : RPW * warp;
   const int trow0 = tmode ? lane : tr0, tcol0 = tmode ? tr0 : lane;
   const float xs = (float)(tcol0 - TX / 2);  // x' of state 0 (T-mode: state s at xs + so(s))
   const long long li = TI * TX + lane - p.I_M;
@@ -912,7 +917,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   int soff[RPW], stoff[RPW];
 #pragma unroll
   for (int s = 0; s < RPW; ++s) {
-    const int trow = tmode ? lane : tr0 + so_of(s, NWARPS), tcol = tmode ? tr0 + so_of(s, NWARPS) : lane;
+    const int trow = tmode ? lane : tr0 + so_of(s, NWARPS, SPREAD), tcol = tmode ? tr0 + so_of(s, NWARPS, SPREAD) : lane;
     const long long lj = TJ * TY + trow - p.J_M, lis = TI * TX + tcol - p.I_M;
     int py = -1, px = -1;
     if (lj >= 0 && lj < p.ny) { py = p.pyM + (int)lj; if (py >= p.ny) py -= p.ny; }
@@ -1290,11 +1295,11 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   if (lane == 0 && ph_slot >= 0 && ph_slot < kPhaseSlots)
     g_phase[ph_slot].flags = (fast ? 1 : 0) | (int)(pin << 8) | (int)(pfast << 16);
 #endif
-  if (!SE2M_MASKED && !fast && pfast != (1u << NP) - 1u) pfast = 0;  // (A/B: all-or-nothing per warp)
-  if (fast || (!SE2M_MASKED && pfast == (1u << NP) - 1u)) {
+  if (!MASK && !fast && pfast != (1u << NP) - 1u) pfast = 0;  // (all-or-nothing per warp)
+  if (fast || (!MASK && pfast == (1u << NP) - 1u)) {
     interior(std::integral_constant<bool, tmode>{}, std::false_type{});
   } else {
-    if (SE2M_MASKED && pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
+    if (MASK && pfast) interior(std::integral_constant<bool, tmode>{}, std::true_type{});
     if (pin & ~pfast) border(std::integral_constant<bool, tmode>{});
   }
   SE2M_PHASE(4);
@@ -1361,15 +1366,15 @@ static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensor
 
 // MODE 1 (edge stream) first, so its CTAs are scheduled early, then MODE 0 on the map's stream
 template <int R_T>
-static cudaError_t launch_t(const AssessParams& p, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream,
-                            cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+static cudaError_t launch_t(const AssessParams& p, const AssessParams& pe, int n_tiles, const CUtensorMap* tmap,
+                            cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
   cudaError_t e;
   const int grid_rows = n_tiles / p.tiles_x;
   *n_launch = 0;
   if (p.tsplit) {
     if ((e = cudaEventRecord(fork, stream)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(edge, fork, 0)) != cudaSuccess) return e;
-    if ((e = launch_mode<R_T, 1>(p, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
+    if ((e = launch_mode<R_T, 1>(pe, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
     ++*n_launch;
   }
   const cudaError_t e0 = launch_mode<R_T, 0>(p, n_tiles, tmap, stream);
@@ -1420,17 +1425,17 @@ size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
   }
 }
 
-cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap, cudaStream_t stream,
-                          cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const CUtensorMap* tmap,
+                          cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
   *n_launch = 0;
   if (n_tiles <= 0 || p.k_end <= p.k_begin) return cudaSuccess;
   switch (R_T) {
-    case 4: return launch_t<4>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 8: return launch_t<8>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 12: return launch_t<12>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 16: return launch_t<16>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 24: return launch_t<24>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 32: return launch_t<32>(p, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 4: return launch_t<4>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 8: return launch_t<8>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 12: return launch_t<12>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 16: return launch_t<16>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 24: return launch_t<24>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 32: return launch_t<32>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -120,7 +120,8 @@ size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk);
 int assess_ctas_per_sm(int R_T, size_t smem);
 // With p.tsplit the edge-tile kernel runs on `edge` (forked from / joined into `stream` with the two
 // events); *n_launch = kernels launched.
-cudaError_t launch_assess(const AssessParams& p, int R_T, int n_tiles, const CUtensorMap* tmap,
+// pe: the edge kernel's parameters (its own yaw-chain tables and chunking; otherwise p's)
+cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const CUtensorMap* tmap,
                           cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join,
                           int* n_launch);
 

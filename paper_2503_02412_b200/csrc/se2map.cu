@@ -67,6 +67,17 @@ struct se2m_map {
   int4* d_full_fmt = nullptr;
   int* d_segb = nullptr;              // [seg + 1] yaw-chain segment bounds
   unsigned char* d_seg_rst = nullptr; // [H] chain restart flags
+  // the vertical-window-edge kernel's own yaw chain (seg_e >= seg segments: its CTAs take fewer bins, so that
+  // they stop being the critical path of small launches, e.g. the row bands of 8 ranks); aliases the main
+  // tables when seg_e == seg
+  int seg_e = 1;
+  std::vector<int> chain_off_e, chain_mid_e;
+  int4* d_chain_e = nullptr;
+  int* d_chain_off_e = nullptr;
+  int* d_chain_mid_e = nullptr;
+  int* d_segb_e = nullptr;
+  unsigned char* d_seg_rst_e = nullptr;
+  bool own_edge_tables = false;
   int* d_full_off = nullptr;
   int4* d_chain = nullptr;
   int* d_chain_off = nullptr;
@@ -235,8 +246,26 @@ static bool build_stencils(se2m_map* m, std::vector<int4>& runs, std::vector<int
 #define SE2M_CELL_MAX 2  // endpoint moves of up to this many cells become single-cell chain entries
 #endif
 
-static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows,
-                         std::vector<int4>& full, std::vector<int4>& chain) {
+// Full rows of every bin (border tiles, the direct path): run entries (e-, e+, d, 0) -> m->full_off.
+static void build_full(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows,
+                       std::vector<int4>& full) {
+  const int RT = m->R_T, NR = 2 * RT + 1, PW = TX + 2 * RT + 1;
+  m->full_off.assign(m->H + 1, 0);
+  full.clear();
+  for (int k = 0; k < m->H; ++k) {
+    m->full_off[k] = (int)full.size();
+    for (int i = 0; i < nrows[k]; ++i) {
+      const int4 q = runs[(size_t)k * NR + i];  // (lo, hi, d)
+      full.push_back(make_int4(q.z * PW + RT + q.x, q.z * PW + RT + q.y + 1, q.z, 0));
+    }
+  }
+  m->full_off[m->H] = (int)full.size();
+}
+
+// The yaw-chain table for S segments (restarts at the bounds floor(H s / S)), in the kernel's shared-memory
+// format: per bin the prefix entries, then (from chain_mid[k]) the single-cell entries.
+static void build_chain(const se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows, int S,
+                        std::vector<int4>& chain, std::vector<int>& chain_off, std::vector<int>& chain_mid) {
   const int RT = m->R_T, NR = 2 * RT + 1, PW = TX + 2 * RT + 1;
   auto row_runs = [&](int k) {  // d -> (a, b) or (0, -1)
     std::vector<int2> r(NR, make_int2(0, -1));
@@ -254,20 +283,15 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
   auto cent = [&](int d, int di, int sg) {
     return make_int4(4 * ea(d, di), fbits((float)sg), fbits((float)(sg * di)), fbits((float)(sg * (d - RT))));
   };
-  m->full_off.assign(m->H + 1, 0);
-  m->chain_off.assign(m->H + 1, 0);
-  m->chain_mid.assign(m->H, 0);
-  full.clear();
+  chain_off.assign(m->H + 1, 0);
+  chain_mid.assign(m->H, 0);
   chain.clear();
   std::vector<int2> prev;
   for (int k = 0; k < m->H; ++k) {
     const std::vector<int2> cur = row_runs(k);
-    m->full_off[k] = (int)full.size();
-    for (int d = 0; d < NR; ++d)
-      if (cur[d].y >= cur[d].x) full.push_back(make_int4(ea(d, cur[d].x), eb(d, cur[d].y), d, 0));
-    m->chain_off[k] = (int)chain.size();
+    chain_off[k] = (int)chain.size();
     std::vector<int4> cells;
-    if (seg_restart(m->H, m->seg, k)) {
+    if (seg_restart(m->H, S, k)) {
       for (int d = 0; d < NR; ++d)
         if (cur[d].y >= cur[d].x) chain.push_back(pent(ea(d, cur[d].x), eb(d, cur[d].y), d));
     } else {
@@ -294,12 +318,17 @@ static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::
         if (cur[d].y < prev[d].y) span(d, cur[d].y + 1, prev[d].y, -1);
       }
     }
-    m->chain_mid[k] = (int)chain.size();
+    chain_mid[k] = (int)chain.size();
     chain.insert(chain.end(), cells.begin(), cells.end());
     prev = cur;
   }
-  m->full_off[m->H] = (int)full.size();
-  m->chain_off[m->H] = (int)chain.size();
+  chain_off[m->H] = (int)chain.size();
+}
+
+static void build_tables(se2m_map* m, const std::vector<int4>& runs, const std::vector<int>& nrows,
+                         std::vector<int4>& full, std::vector<int4>& chain) {
+  build_full(m, runs, nrows, full);
+  build_chain(m, runs, nrows, m->seg, chain, m->chain_off, m->chain_mid);
 }
 
 static bool make_tensor_map(se2m_map* m, CUtensorMap* tm, float* base) {
@@ -412,6 +441,9 @@ static se2m_status validate(const se2m_params* p) {
 #endif
 #ifndef SE2M_SEGMENTS_LARGE_R
 #define SE2M_SEGMENTS_LARGE_R 8
+#endif
+#ifndef SE2M_EDGE_SEGMENTS
+#define SE2M_EDGE_SEGMENTS 4   // the vertical-window-edge kernel's chain: at least this many segments
 #endif
 static int chain_segments(int H, long long cells, int R_T, int requested) {
   if (H < 18 || cells < 512LL * 512LL) return H;
@@ -648,6 +680,37 @@ extern "C" se2m_status se2m_init(const se2m_params* p, se2m_map** out) {
     }
   }
   m->prm.nccl_unique_id = nullptr;  // copied (the caller's pointer need not outlive se2m_init)
+  {  // the vertical-window-edge kernel's yaw chain (its own segments; see se2m_map::seg_e)
+    const bool edge_kernel = tile_rows(m->R_T) == 32 && chain_border(m->R_T);
+    m->seg_e = (edge_kernel && m->seg < m->H) ? std::min(m->H, std::max(m->seg, SE2M_EDGE_SEGMENTS)) : m->seg;
+    if (m->seg_e == m->seg) {
+      m->chain_off_e = m->chain_off; m->chain_mid_e = m->chain_mid;
+      m->d_chain_e = m->d_chain; m->d_chain_off_e = m->d_chain_off; m->d_chain_mid_e = m->d_chain_mid;
+      m->d_segb_e = m->d_segb; m->d_seg_rst_e = m->d_seg_rst;
+    } else {
+      std::vector<int4> chain_e;
+      build_chain(m, runs, nrows, m->seg_e, chain_e, m->chain_off_e, m->chain_mid_e);
+      std::vector<int> segb_e(m->seg_e + 1);
+      std::vector<unsigned char> rst_e(m->H);
+      for (int q = 0; q <= m->seg_e; ++q) segb_e[q] = seg_bound(m->H, m->seg_e, q);
+      for (int k = 0; k < m->H; ++k) rst_e[k] = seg_restart(m->H, m->seg_e, k) ? 1 : 0;
+      m->own_edge_tables = true;
+      if ((e = cudaMalloc(&m->d_chain_e, std::max<size_t>(1, chain_e.size()) * sizeof(int4))) ||
+          (e = cudaMalloc(&m->d_chain_off_e, m->chain_off_e.size() * sizeof(int))) ||
+          (e = cudaMalloc(&m->d_chain_mid_e, m->chain_mid_e.size() * sizeof(int))) ||
+          (e = cudaMalloc(&m->d_segb_e, segb_e.size() * sizeof(int))) ||
+          (e = cudaMalloc(&m->d_seg_rst_e, rst_e.size())) ||
+          (e = cudaMemcpyAsync(m->d_chain_e, chain_e.data(), chain_e.size() * sizeof(int4), cudaMemcpyHostToDevice, m->stream)) ||
+          (e = cudaMemcpyAsync(m->d_chain_off_e, m->chain_off_e.data(), m->chain_off_e.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+          (e = cudaMemcpyAsync(m->d_chain_mid_e, m->chain_mid_e.data(), m->chain_mid_e.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+          (e = cudaMemcpyAsync(m->d_segb_e, segb_e.data(), segb_e.size() * sizeof(int), cudaMemcpyHostToDevice, m->stream)) ||
+          (e = cudaMemcpyAsync(m->d_seg_rst_e, rst_e.data(), rst_e.size(), cudaMemcpyHostToDevice, m->stream)) ||
+          (e = cudaStreamSynchronize(m->stream))) {
+        cuda_fail(m, e, "edge chain tables");
+        return bail(SE2M_ERR_CUDA);
+      }
+    }
+  }
   m->tma_ok = make_tensor_map(m, &m->tmap, m->d_h);
   {
     int optin = 0;
@@ -687,6 +750,11 @@ extern "C" void se2m_destroy(se2m_map* m) {
   if (m->ev_join) cudaEventDestroy(m->ev_join);
   for (float* b : m->d_halo)
     if (b) cudaFree(b);
+  if (m->own_edge_tables) {
+    void* e_ptrs[] = {m->d_chain_e, m->d_chain_off_e, m->d_chain_mid_e, m->d_segb_e, m->d_seg_rst_e};
+    for (void* q : e_ptrs)
+      if (q) cudaFree(q);
+  }
   if (m->comm) nccl_api().CommDestroy(m->comm);  // after the stream drained: no transfer in flight
   if (m->step_exec) cudaGraphExecDestroy(m->step_exec);
   if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
@@ -1017,9 +1085,38 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
       p.n_tcols = 0;
     }
   }
+  // the edge kernel's launch: its own yaw chain (seg_e segments, one per CTA when shorter than the main chain)
+  AssessParams pe = p;
+  if (p.tsplit) {
+    const int Se = m->seg_e;
+    pe.seg = Se; pe.segb = m->d_segb_e; pe.seg_rst = m->d_seg_rst_e;
+    pe.chain = m->d_chain_e; pe.chain_off = m->d_chain_off_e; pe.chain_mid = m->d_chain_mid_e;
+    pe.seg_first = seg_of(H, Se, m->k_lo);
+    pe.k_begin = seg_bound(H, Se, pe.seg_first);
+    const int sa = pe.seg_first, sb = m->k_hi > pe.k_begin ? seg_of(H, Se, m->k_hi - 1) + 1 : sa;
+    int ce = Se == m->seg ? p.seg_chunk : 1;
+    int cap_e = 1, bins_e = 1;
+    for (;;) {
+      cap_e = 1; bins_e = 1;
+      for (int q = sa; q < sb; q += ce) {
+        const int kb = std::max(pe.k_begin, seg_bound(H, Se, q)), ke = std::min(m->k_hi, seg_bound(H, Se, std::min(Se, q + ce)));
+        const int nf = m->full_off[ke] - m->full_off[kb], nc = m->chain_off_e[ke] - m->chain_off_e[kb];
+        cap_e = std::max(cap_e, nf + nc);  // (edge tiles: chain_border radii only)
+        bins_e = std::max(bins_e, ke - kb);
+      }
+      if (assess_smem_bytes(m->R_T, cap_e, bins_e) <= (size_t)m->smem_optin || ce == 1) break;
+      ce = (ce + 1) / 2;
+    }
+    if (assess_smem_bytes(m->R_T, cap_e, bins_e) > (size_t)m->smem_optin)
+      return fail(m, SE2M_ERR_UNSUPPORTED, "assess: footprint tables exceed the shared memory of a CTA (edge)");
+    pe.seg_chunk = ce;
+    pe.n_chunks = (sb - sa + ce - 1) / ce;
+    pe.k_chunk = bins_e;
+    pe.tab_cap = cap_e;
+  }
   if (n_tiles > 0 && n_seg > 0 && m->k_hi > m->k_lo) {
     int nl = 0;
-    cudaError_t e = launch_assess(p, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
+    cudaError_t e = launch_assess(p, pe, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
     m->launches += nl;
   }

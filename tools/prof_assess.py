@@ -22,6 +22,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from synth.terrain import CONFIGS, world_heights  # noqa: E402
 
 
+def _segments(m):
+    try:
+        return m.chain_segments()
+    except Exception:  # an A/B build from before se2m_chain_segments
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
@@ -62,7 +69,7 @@ def main():
         m.assess_se2(0)
         m.synchronize()
         ts.append(time.perf_counter() - t)
-    res = dict(config=a.config, holes=a.holes, segments=m.chain_segments(), unknown_frac=0.0 if known is None else float(1 - known.mean()),
+    res = dict(config=a.config, holes=a.holes, segments=_segments(m), unknown_frac=0.0 if known is None else float(1 - known.mean()),
                ms_median=1e3 * float(np.median(ts)), ms_min=1e3 * float(np.min(ts)))
     if a.sdf > 0:
         m.compute_sdf(a.sdf)

@@ -1,0 +1,14 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/t_gpu_tests.log 2>&1; echo "tests rc=$?"
+for rep in 1 2; do
+for v in r01 tm es; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 600 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | sed "s#^#$v #"
+done
+done > gpurun_out/t_bench_ab.txt 2>&1
+echo "bench ab rc=$?"
+for v in tm es; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 600 python tools/prof_shards.py --configs large | sed "s#^#$v #"
+done > gpurun_out/t_shards.txt 2>&1
+echo "shards rc=$?"
