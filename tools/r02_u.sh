@@ -1,0 +1,13 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in es2 es es9 es18; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 600 python bench.py --steps 30 --warmup 5 --no-extras --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | sed "s#^#$v #"
+done
+done > gpurun_out/u_bench_ab.txt 2>&1
+echo "bench ab rc=$?"
+for v in es9 es18; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 600 python tools/prof_shards.py --configs large | sed "s#^#$v #"
+done > gpurun_out/u_shards.txt 2>&1
+echo "shards rc=$?"
