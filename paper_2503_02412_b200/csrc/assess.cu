@@ -1366,8 +1366,9 @@ static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensor
 
 // MODE 1 (edge stream) first, so its CTAs are scheduled early, then MODE 0 on the map's stream
 template <int R_T>
-static cudaError_t launch_t(const AssessParams& p, const AssessParams& pe, int n_tiles, const CUtensorMap* tmap,
-                            cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+static cudaError_t launch_t(const AssessParams& p, const AssessParams& pe, int n_tiles, const AssessParams* side,
+                            const int* side_tiles, int n_side, const CUtensorMap* tmap, cudaStream_t stream,
+                            cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
   cudaError_t e;
   const int grid_rows = n_tiles / p.tiles_x;
   *n_launch = 0;
@@ -1376,9 +1377,15 @@ static cudaError_t launch_t(const AssessParams& p, const AssessParams& pe, int n
     if ((e = cudaStreamWaitEvent(edge, fork, 0)) != cudaSuccess) return e;
     if ((e = launch_mode<R_T, 1>(pe, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
     ++*n_launch;
+    for (int q = 0; q < n_side; ++q) {  // the top / bottom border tile rows: main kernel, edge chain
+      if (side_tiles[q] <= 0) continue;
+      if ((e = launch_mode<R_T, 0>(side[q], side_tiles[q], tmap, edge)) != cudaSuccess) return e;
+      ++*n_launch;
+    }
   }
-  const cudaError_t e0 = launch_mode<R_T, 0>(p, n_tiles, tmap, stream);
-  if (e0 == cudaSuccess) ++*n_launch;
+  const int n_main = n_tiles - (n_side > 0 ? side_tiles[0] + (n_side > 1 ? side_tiles[1] : 0) : 0);
+  const cudaError_t e0 = n_main > 0 ? launch_mode<R_T, 0>(p, n_main, tmap, stream) : cudaSuccess;
+  if (e0 == cudaSuccess && n_main > 0) ++*n_launch;
   if (p.tsplit) {  // join the edge kernel even when the main launch failed: later work must not race it
     if ((e = cudaEventRecord(join, edge)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(stream, join, 0)) != cudaSuccess) return e;
@@ -1425,17 +1432,18 @@ size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk) {
   }
 }
 
-cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const CUtensorMap* tmap,
-                          cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
+cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const AssessParams* side,
+                          const int* side_tiles, int n_side, const CUtensorMap* tmap, cudaStream_t stream,
+                          cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch) {
   *n_launch = 0;
   if (n_tiles <= 0 || p.k_end <= p.k_begin) return cudaSuccess;
   switch (R_T) {
-    case 4: return launch_t<4>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 8: return launch_t<8>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 12: return launch_t<12>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 16: return launch_t<16>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 24: return launch_t<24>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
-    case 32: return launch_t<32>(p, pe, n_tiles, tmap, stream, edge, fork, join, n_launch);
+    case 4: return launch_t<4>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
+    case 8: return launch_t<8>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
+    case 12: return launch_t<12>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
+    case 16: return launch_t<16>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
+    case 24: return launch_t<24>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
+    case 32: return launch_t<32>(p, pe, n_tiles, side, side_tiles, n_side, tmap, stream, edge, fork, join, n_launch);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -120,10 +120,12 @@ size_t assess_smem_bytes(int R_T, int tab_cap, int k_chunk);
 int assess_ctas_per_sm(int R_T, size_t smem);
 // With p.tsplit the edge-tile kernel runs on `edge` (forked from / joined into `stream` with the two
 // events); *n_launch = kernels launched.
-// pe: the edge kernel's parameters (its own yaw-chain tables and chunking; otherwise p's)
-cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const CUtensorMap* tmap,
-                          cudaStream_t stream, cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join,
-                          int* n_launch);
+// pe: the edge kernel's parameters (its own yaw-chain tables and chunking; otherwise p's).  side[0 .. n_side):
+// extra launches of the main kernel on the edge stream (the window's top / bottom border tile rows, with the
+// edge chain), side_tiles[q] tiles each; the main launch p covers the other n_tiles - sum(side_tiles) tiles.
+cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T, int n_tiles, const AssessParams* side,
+                          const int* side_tiles, int n_side, const CUtensorMap* tmap, cudaStream_t stream,
+                          cudaStream_t edge, cudaEvent_t fork, cudaEvent_t join, int* n_launch);
 
 // SE2M_PHASES debug builds: per-warp phase timestamps of the assess kernel (PhaseRec in assess.cu: 6 x u64 + 4 x i32)
 cudaError_t debug_phases(void* out, long long max_records, int reset, long long* n, cudaStream_t s);

@@ -442,6 +442,10 @@ static se2m_status validate(const se2m_params* p) {
 #ifndef SE2M_SEGMENTS_LARGE_R
 #define SE2M_SEGMENTS_LARGE_R 8
 #endif
+#ifndef SE2M_BORDER_ROWS_EDGE
+#define SE2M_BORDER_ROWS_EDGE 0  // the top / bottom border tile rows with the edge chain as side launches on the
+                                 // edge stream: measured 1.127 vs 1.048 ms (large, bench conditions) — off
+#endif
 #ifndef SE2M_EDGE_SEGMENTS
 #define SE2M_EDGE_SEGMENTS 4   // the vertical-window-edge kernel's chain: at least this many segments
 #endif
@@ -989,8 +993,10 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
   const bool full = mode == SE2M_FULL || m->all_dirty;
   std::vector<int4> rects;
   if (!full) {
-    // H9: states within R (Chebyshev bound of every footprint) of a changed cell, as tile rectangles
-    const long long Rd = m->R;
+    // H9: states within R (Chebyshev bound of every footprint) of a changed cell, as tile rectangles — dilated by
+    // R_T >= R: a tile changes kernels (edge / border / main: different rounding) only when the window edge passes
+    // within R_T of it, i.e. within R_T of the entered or vacated cells, so INCREMENTAL == FULL bit for bit
+    const long long Rd = m->R_T;
     long long bx0 = gx1, bx1 = 0, by0 = gy1, by1 = 0;
     for (const Rect& d : m->dirty) {
       const long long I0 = std::max(d.I0 - Rd, m->I_M), I1 = std::min(d.I1 + Rd, m->I_M + nx);
@@ -1114,9 +1120,34 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
     pe.k_chunk = bins_e;
     pe.tab_cap = cap_e;
   }
+  // the window's top / bottom border tile rows (a prefix and a suffix of the grid rows: lj0 grows with the row)
+  // run on the edge stream with the edge chain — their general pairs make long CTAs, which shorter chunks
+  // keep off the critical path; the main launch covers the middle rows
+  AssessParams side[2] = {pe, pe};
+  int side_tiles[2] = {0, 0}, n_side = 0;
+  AssessParams p0 = p;
+  if (p.tsplit && m->seg_e != m->seg && SE2M_BORDER_ROWS_EDGE) {
+    const int HY = TY + 2 * m->R_T;
+    auto bedge = [&](int gr) {
+      const long long lj0 = (p.TJ0 + p.row_first + gr * p.row_mod) * TY - m->R_T - m->J_M;
+      return lj0 < 0 || lj0 + HY > ny;
+    };
+    int pre = 0, suf = 0;
+    while (pre < grid_rows && bedge(pre)) ++pre;
+    while (suf < grid_rows - pre && bedge(grid_rows - 1 - suf)) ++suf;
+    if (pre + suf > 0 && pre + suf < grid_rows) {
+      side[0].row_first = p.row_first;                                   // rows [0, pre)
+      side[1].row_first = p.row_first + (grid_rows - suf) * p.row_mod;   // rows [grid_rows - suf, grid_rows)
+      side_tiles[0] = pre * p.tiles_x;
+      side_tiles[1] = suf * p.tiles_x;
+      n_side = 2;
+      p0.row_first = p.row_first + pre * p.row_mod;                      // the main launch: the middle rows
+    }
+  }
   if (n_tiles > 0 && n_seg > 0 && m->k_hi > m->k_lo) {
     int nl = 0;
-    cudaError_t e = launch_assess(p, pe, m->R_T, n_tiles, tmap, m->stream, m->edge_stream, m->ev_fork, m->ev_join, &nl);
+    cudaError_t e = launch_assess(p0, pe, m->R_T, n_tiles, side, side_tiles, n_side, tmap, m->stream, m->edge_stream,
+                                  m->ev_fork, m->ev_join, &nl);
     if (e != cudaSuccess) return cuda_fail(m, e, "assess kernel");
     m->launches += nl;
   }
