@@ -1372,20 +1372,32 @@ static cudaError_t launch_t(const AssessParams& p, const AssessParams& pe, int n
   cudaError_t e;
   const int grid_rows = n_tiles / p.tiles_x;
   *n_launch = 0;
+  const int n_main = n_tiles - (n_side > 0 ? side_tiles[0] + (n_side > 1 ? side_tiles[1] : 0) : 0);
+  const bool main_first = p.main_first && p.tsplit;
   if (p.tsplit) {
     if ((e = cudaEventRecord(fork, stream)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(edge, fork, 0)) != cudaSuccess) return e;
-    if ((e = launch_mode<R_T, 1>(pe, p.n_tcols * grid_rows, tmap, edge)) != cudaSuccess) return e;
-    ++*n_launch;
-    for (int q = 0; q < n_side; ++q) {  // the top / bottom border tile rows: main kernel, edge chain
-      if (side_tiles[q] <= 0) continue;
-      if ((e = launch_mode<R_T, 0>(side[q], side_tiles[q], tmap, edge)) != cudaSuccess) return e;
-      ++*n_launch;
-    }
   }
-  const int n_main = n_tiles - (n_side > 0 ? side_tiles[0] + (n_side > 1 ? side_tiles[1] : 0) : 0);
-  const cudaError_t e0 = n_main > 0 ? launch_mode<R_T, 0>(p, n_main, tmap, stream) : cudaSuccess;
-  if (e0 == cudaSuccess && n_main > 0) ++*n_launch;
+  // (main_first: the main kernel is launched before the edge kernel; the fork above already orders the edge
+  // stream after the work before this call, not after the main kernel)
+  cudaError_t e0 = cudaSuccess;
+  if (main_first && n_main > 0) {
+    e0 = launch_mode<R_T, 0>(p, n_main, tmap, stream);
+    if (e0 == cudaSuccess) ++*n_launch;
+  }
+  if (p.tsplit && e0 == cudaSuccess) {
+    e = launch_mode<R_T, 1>(pe, p.n_tcols * grid_rows, tmap, edge);
+    if (e == cudaSuccess) ++*n_launch;
+    for (int q = 0; q < n_side && e == cudaSuccess; ++q) {  // the top / bottom border tile rows: main kernel, edge chain
+      if (side_tiles[q] <= 0) continue;
+      if ((e = launch_mode<R_T, 0>(side[q], side_tiles[q], tmap, edge)) == cudaSuccess) ++*n_launch;
+    }
+    if (e != cudaSuccess) e0 = e;
+  }
+  if (!main_first && e0 == cudaSuccess && n_main > 0) {
+    e0 = launch_mode<R_T, 0>(p, n_main, tmap, stream);
+    if (e0 == cudaSuccess) ++*n_launch;
+  }
   if (p.tsplit) {  // join the edge kernel even when the main launch failed: later work must not race it
     if ((e = cudaEventRecord(join, edge)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(stream, join, 0)) != cudaSuccess) return e;

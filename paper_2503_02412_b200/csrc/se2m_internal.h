@@ -97,6 +97,8 @@ struct AssessParams {
   // assess_kernel<R_T, 1>, on the edge stream (tsplit = 1); the main launch skips them
   int tsplit, n_tcols;
   int tcols[4];
+  int main_first;        // (host) launch the main kernel before the edge kernel: set when both grids fit one wave
+                         // together, so neither waits for slots and the main kernel's longer CTAs start first
   int use_tma;           // tensor map valid
   int force_general;     // some full stencil is degenerate (< 3 cells or collinear): no interior fast path
 };

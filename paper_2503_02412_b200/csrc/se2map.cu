@@ -446,6 +446,9 @@ static se2m_status validate(const se2m_params* p) {
 #define SE2M_BORDER_ROWS_EDGE 0  // the top / bottom border tile rows with the edge chain as side launches on the
                                  // edge stream: measured 1.127 vs 1.048 ms (large, bench conditions) — off
 #endif
+#ifndef SE2M_MAIN_FIRST
+#define SE2M_MAIN_FIRST 1      // launch order of the main / edge assess kernels on one-wave grids (AssessParams::main_first)
+#endif
 #ifndef SE2M_EDGE_SEGMENTS
 #define SE2M_EDGE_SEGMENTS 4   // the vertical-window-edge kernel's chain: at least this many segments
 #endif
@@ -1119,6 +1122,14 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
     pe.n_chunks = (sb - sa + ce - 1) / ce;
     pe.k_chunk = bins_e;
     pe.tab_cap = cap_e;
+  }
+  // small grids (both kernels' CTAs fit one wave): the main kernel launches first — its corner / border CTAs
+  // are the longest, and with free slots for every CTA the edge kernel loses nothing by starting second
+  p.main_first = 0;
+  if (p.tsplit && SE2M_MAIN_FIRST) {
+    const long long ctas = (long long)p.n_tcols * grid_rows * pe.n_chunks +
+                           (long long)(p.tiles_x - p.n_tcols) * grid_rows * p.n_chunks;
+    p.main_first = ctas <= (long long)m->n_sm * m->slots_per_sm ? 1 : 0;
   }
   // the window's top / bottom border tile rows (a prefix and a suffix of the grid rows: lj0 grows with the row)
   // run on the edge stream with the edge chain — their general pairs make long CTAs, which shorter chunks
