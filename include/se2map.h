@@ -235,6 +235,13 @@ se2m_status se2m_exchange_halo(se2m_map* m);
 /* Host-only: a fresh NCCL unique id (out, bytes >= 128) for params.nccl_unique_id; SE2M_ERR_NCCL when NCCL
  * cannot be loaded.  *version (may be NULL) = the loaded NCCL's version code (e.g. 22809). */
 se2m_status se2m_nccl_unique_id(void* out, int32_t bytes, int32_t* version);
+/* Diagnostic (the calls se2m_exchange_halo makes, on hardware with one GPU): a one-rank NCCL communicator on
+ * `device` (ncclGetUniqueId, ncclCommInitRank), one grouped ncclSend + ncclRecv of `count` floats from a
+ * device buffer to a second one on the same rank (ncclGroupStart / End on a private stream), the received
+ * floats compared with the sent ones on the host, ncclCommDestroy.  *version (may be NULL) = the loaded NCCL's
+ * version code.  SE2M_OK when the data arrived intact; SE2M_ERR_NCCL (NCCL missing, a call failed, or the data
+ * differ), SE2M_ERR_CUDA, SE2M_ERR_INVALID_ARG (count < 1).  Synchronous; leaves the current device as it was. */
+se2m_status se2m_nccl_selftest(int32_t device, int64_t count, int32_t* version);
 
 /* Host-only (no device): the slab list of rank `sender` for window origin row J_M: first_rows[q] = first
  * world row of slab q (slab_rows rows), or INT64_MIN past the end of the list; last = 0: the first rows of

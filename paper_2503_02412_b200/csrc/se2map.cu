@@ -1267,6 +1267,57 @@ extern "C" se2m_status se2m_nccl_unique_id(void* out, int32_t bytes, int32_t* ve
   return SE2M_OK;
 }
 
+extern "C" se2m_status se2m_nccl_selftest(int32_t device, int64_t count, int32_t* version) {
+  if (count < 1) return fail(nullptr, SE2M_ERR_INVALID_ARG, "nccl_selftest: count must be >= 1");
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return fail(nullptr, SE2M_ERR_NCCL, "NCCL: " + nc.err);
+  DevGuard guard(device);
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) return fail(nullptr, SE2M_ERR_CUDA, "nccl_selftest: cudaSetDevice");
+  if (version) {
+    int v = 0;
+    *version = nc.GetVersion(&v) == ncclSuccess ? v : 0;
+  }
+  std::vector<float> sent((size_t)count), got((size_t)count, 0.f);
+  for (int64_t i = 0; i < count; ++i) sent[(size_t)i] = (float)((i * 2654435761LL) % 1000003) * 0.5f - 7.25f;
+  ncclUniqueId id;
+  ncclComm_t comm = nullptr;
+  cudaStream_t st = nullptr;
+  float *a = nullptr, *b = nullptr;
+  std::string err;
+  se2m_status rc = SE2M_OK;
+  auto cu = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && rc == SE2M_OK) { rc = SE2M_ERR_CUDA; err = std::string(what) + ": " + cudaGetErrorString(e); }
+    return rc == SE2M_OK;
+  };
+  auto nk = [&](ncclResult_t r, const char* what) {
+    if (r != ncclSuccess && rc == SE2M_OK) { rc = SE2M_ERR_NCCL; err = std::string(what) + ": " + nc.GetErrorString(r); }
+    return rc == SE2M_OK;
+  };
+  const size_t bytes = (size_t)count * sizeof(float);
+  if (nk(nc.GetUniqueId(&id), "ncclGetUniqueId") && nk(nc.CommInitRank(&comm, 1, id, 0), "ncclCommInitRank") &&
+      cu(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate") &&
+      cu(cudaMalloc(&a, bytes), "cudaMalloc") && cu(cudaMalloc(&b, bytes), "cudaMalloc") &&
+      cu(cudaMemcpy(a, sent.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy") &&
+      cu(cudaMemset(b, 0, bytes), "cudaMemset") && nk(nc.GroupStart(), "ncclGroupStart")) {
+    ncclResult_t q = nc.Send(a, (size_t)count, ncclFloat32, 0, comm, st);
+    if (q == ncclSuccess) q = nc.Recv(b, (size_t)count, ncclFloat32, 0, comm, st);
+    const ncclResult_t r = nc.GroupEnd();
+    if (nk(q, "ncclSend/ncclRecv") && nk(r, "ncclGroupEnd") && cu(cudaStreamSynchronize(st), "transfer") &&
+        cu(cudaMemcpy(got.data(), b, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy") &&
+        memcmp(got.data(), sent.data(), bytes) != 0) {
+      rc = SE2M_ERR_NCCL;
+      err = "the received floats differ from the sent ones";
+    }
+  }
+  if (comm) nc.CommDestroy(comm);
+  if (a) cudaFree(a);
+  if (b) cudaFree(b);
+  if (st) cudaStreamDestroy(st);
+  if (rc != SE2M_OK) return fail(nullptr, rc, "nccl_selftest: " + err);
+  return SE2M_OK;
+}
+
 extern "C" se2m_status se2m_chain_segments(const se2m_map* m, int32_t* segments) {
   if (!m || !segments) return SE2M_ERR_INVALID_ARG;
   *segments = m->seg;

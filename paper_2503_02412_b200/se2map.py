@@ -34,7 +34,7 @@ EXPORTS = ["se2m_default_params", "se2m_init", "se2m_destroy", "se2m_update_elev
            "se2m_download_inpainted", "se2m_download_compact_rep", "se2m_step",
            "se2m_owned_rows", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack", "se2m_halo_plan",
            "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo", "se2m_nccl_unique_id",
-           "se2m_query_trilinear_async", "se2m_debug_phases"]
+           "se2m_query_trilinear_async", "se2m_debug_phases", "se2m_nccl_selftest"]
 
 
 class Params(ctypes.Structure):
@@ -128,6 +128,7 @@ _lib.se2m_exchange_halo.argtypes = [_vp]
 _lib.se2m_debug_phases.argtypes = [_vp, _vp, _i64, _i32, ctypes.POINTER(_i64)]
 _lib.se2m_query_trilinear_async.argtypes = [_vp, _i64, _vp, _i32, _vp, _i32]
 _lib.se2m_nccl_unique_id.argtypes = [_vp, _i32, ctypes.POINTER(_i32)]
+_lib.se2m_nccl_selftest.argtypes = [_i32, _i64, ctypes.POINTER(_i32)]
 _lib.se2m_launch_count.argtypes = [_vp]
 _lib.se2m_launch_count.restype = _i64
 _lib.se2m_last_error.argtypes = [_vp]
@@ -138,7 +139,7 @@ for _name in ("se2m_init", "se2m_update_elevation", "se2m_shift_window", "se2m_a
               "se2m_sdf_from_mask", "se2m_query_trilinear", "se2m_integrate_scan",
               "se2m_download_elevation", "se2m_halo_size", "se2m_halo_pack", "se2m_halo_unpack",
               "se2m_halo_plan", "se2m_chain_segments", "se2m_query_async", "se2m_exchange_halo",
-              "se2m_nccl_unique_id", "se2m_query_trilinear_async", "se2m_debug_phases"):
+              "se2m_nccl_unique_id", "se2m_query_trilinear_async", "se2m_debug_phases", "se2m_nccl_selftest"):
     getattr(_lib, _name).restype = ctypes.c_int
 
 
@@ -177,6 +178,16 @@ def nccl_unique_id():
     if st != SE2M_OK:
         raise Se2mError(st, _lib.se2m_last_error(None).decode())
     return buf.raw, ver.value
+
+
+def nccl_selftest(device=0, count=1 << 20):
+    """se2m_nccl_selftest: a one-rank NCCL communicator on `device` sends `count` floats to itself through the
+    calls se2m_exchange_halo makes; returns the loaded NCCL's version code, raises Se2mError on any failure."""
+    ver = _i32()
+    st = _lib.se2m_nccl_selftest(int(device), int(count), ctypes.byref(ver))
+    if st != SE2M_OK:
+        raise Se2mError(st, _lib.se2m_last_error(None).decode())
+    return ver.value
 
 
 def _ptr(a):
