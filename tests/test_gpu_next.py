@@ -18,9 +18,11 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("shape,r,d_max,density", [((3, 70, 90), 0.1, 2.0, 0.1), ((2, 41, 37), 0.05, 0.8, 0.03),
                                                   ((1, 130, 64), 0.1, 9.6, 0.002), ((2, 20, 25), 0.1, 0.55, 0.5),
-                                                  # several 256-column x TH-row tiles with ragged tails, both
-                                                  # tile heights (W <= 24: 32 rows, else 64)
-                                                  ((2, 100, 530), 0.1, 2.0, 0.02), ((1, 140, 300), 0.1, 7.0, 0.005)])
+                                                  # column-pass segments (128 rows) and row-pass spans with
+                                                  # ragged tails, W from 6 to 96 cells
+                                                  ((2, 100, 530), 0.1, 2.0, 0.02), ((1, 140, 300), 0.1, 7.0, 0.005),
+                                                  # rows longer than one row-pass CTA (1024 columns), ragged
+                                                  ((1, 40, 2100), 0.1, 2.0, 0.02), ((1, 24, 1300), 0.1, 9.6, 0.002)])
 def test_sdf_from_mask_matches_oracle(shape, r, d_max, density):
     from paper_2503_02412_b200 import se2map as S
     rng = np.random.default_rng(int(d_max * 100))

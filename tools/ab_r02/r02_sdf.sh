@@ -1,0 +1,16 @@
+#!/bin/bash
+# SDF row pass with ballot flag words (no serial prefix count) and 4 cells per thread; column pass reading its
+# segment's class bits back from shared memory — vs the previous kernels
+set -u
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in sdf4 sdf5; do
+  SE2M_LIB=abx/libse2map_$v.so timeout 300 python tools/prof_assess.py --config large --reps 3 --sdf 2.0 | sed "s#^#$v #"
+  SE2M_LIB=abx/libse2map_$v.so timeout 300 python tools/prof_assess.py --config highres --reps 3 --sdf 1.0 | sed "s#^#$v #"
+done
+done > gpurun_out/sdf_ab.txt 2>&1
+SE2M_LIB=abx/libse2map_sdf5.so timeout 900 python -m pytest tests/test_gpu_next.py tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/sdf_tests.log 2>&1
+echo "tests rc=$?"
+SE2M_LIB=abx/libse2map_sdf5.so timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:sdf --csv \
+  --log-file gpurun_out/sdf_launches.csv python tools/prof_assess.py --config large --reps 1 --sdf 2.0 > gpurun_out/sdf_ncu.log 2>&1
+echo "ncu rc=$?"
