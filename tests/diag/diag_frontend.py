@@ -1,6 +1,6 @@
 """Diagnostics: GPU-vs-oracle errors on a scan-built map (front-end + Alg. 1), binned by gap and |P|."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import oracle
 from oracle.frontend import FrontendParams, Pose, integrate_scan

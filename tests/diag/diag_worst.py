@@ -1,6 +1,6 @@
 """Diagnostics: the worst GPU-vs-oracle states of a config (run on the GPU box)."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from synth.terrain import CONFIGS
 from tests.gpu_common import run_config

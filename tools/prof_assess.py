@@ -40,14 +40,15 @@ def main():
                     help="the bench's paper_pipeline map instead: 180x180x30 built from 4 LiDAR frames")
     a = ap.parse_args()
     from paper_2503_02412_b200.se2map import Se2Map
-    import oracle
 
     if a.scan:
         return scan_map(a, Se2Map)
     c = CONFIGS[a.config]
     nx, ny, r = c["nx"], c["ny"], c["r"]
     x, y = c["robot"]
-    I_M, J_M = oracle.window_origin(x, y, r, nx, ny)
+    m = Se2Map(nx=nx, ny=ny, n_yaw=c["n_yaw"], resolution=r, ellipse_ex=c["ex"], ellipse_ey=c["ey"],
+               robot_x=x, robot_y=y, chain_segments=a.segments)
+    I_M, J_M = m.origin()  # the library's Eq. 4 window origin
     h = world_heights(c["terrain"], I_M, J_M, nx, ny, r)
     known = None
     if a.holes > 0:
@@ -58,8 +59,6 @@ def main():
         for di in (-1, 0, 1):
             for dj in (-1, 0, 1):
                 known[cj + dj, ci + di] = 0
-    m = Se2Map(nx=nx, ny=ny, n_yaw=c["n_yaw"], resolution=r, ellipse_ex=c["ex"], ellipse_ey=c["ey"],
-               robot_x=x, robot_y=y, chain_segments=a.segments)
     m.update_elevation(h, known)
     m.assess_se2(0)
     m.synchronize()
