@@ -149,6 +149,23 @@ __device__ __forceinline__ float frsqrt(float x) { float r; asm("rsqrt.approx.ft
 // F2 = (state a, state b) in one 64-bit register pair; the CUDA 12.9 sm_100 builtins __fadd2_rn /
 // __fmul2_rn / __ffma2_rn keep the operations visible to the compiler (negations and constants fold
 // into the FADD2 / FMUL2 / FFMA2 operand modifiers).
+// Programmatic dependent launch (sm_90+): the short map-update kernels let the assess grid launch as soon as
+// they start (its CTAs become resident and compute their tile indices while the update runs); the assess
+// kernel waits for their completion and memory visibility before it reads the heights (SE2M_PDL = 0: off).
+#ifndef SE2M_PDL
+#define SE2M_PDL 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if SE2M_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if SE2M_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 typedef float2 F2;
 __device__ __forceinline__ F2 pk(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ F2 bc(float a) { return make_float2(a, a); }
@@ -615,6 +632,10 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
   if (MODE == 0 && p.tsplit && tedge) return;
   if (MODE == 1 && !tedge) return;
   constexpr bool tmode = MODE == 1 && TMODE_OK;
+
+  // programmatic dependent launch: everything above reads only launch parameters and the tables written at
+  // init; the heights (and the records this grid overwrites) belong to the kernels before it on the stream
+  pdl_wait();
 
   // ---- 1. halo -> shared memory ----------------------------------------------------------
   const bool box_in = li0 >= 0 && li0 + HX <= p.nx && lj0 >= 0 && lj0 + HY <= p.ny;
@@ -1359,8 +1380,21 @@ static cudaError_t launch_mode(const AssessParams& p, int grid_x, const CUtensor
     }
     configured_bytes = (int)smem;
   }
-  dim3 grid(grid_x, p.n_chunks);
-  assess_kernel<R_T, MODE><<<grid, nthreads(R_T), smem, stream>>>(p, *tmap);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_x, p.n_chunks);
+  cfg.blockDim = dim3(nthreads(R_T));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (no effect after a non-kernel operation)
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = SE2M_PDL ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, assess_kernel<R_T, MODE>, p, *tmap);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return e;
+  }
   return cudaGetLastError();
 }
 
@@ -1464,6 +1498,7 @@ cudaError_t launch_assess(const AssessParams& p, const AssessParams& pe, int R_T
 // Ring-buffer helpers: clear (H1), scatter (H2), logical gather (download), query (H10).
 // ------------------------------------------------------------------------------------------
 __global__ void clear_rect_kernel(float* h, int ldh, int x0, int y0, int w, int hgt, int nx, int ny) {
+  pdl_trigger();
   // (x0, y0): physical start; the rectangle wraps modulo (nx, ny)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
@@ -1481,6 +1516,7 @@ cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt,
 }
 
 __global__ void fill_strips_kernel(const FillArgs f) {
+  pdl_trigger();
   const int4 rc = f.rect[blockIdx.z];
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
   if (i >= rc.z || j >= rc.w) return;
@@ -1505,6 +1541,7 @@ cudaError_t launch_fill_strips(const FillArgs& f, cudaStream_t s) {
 __global__ void scatter_rect_kernel(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
                                     int w, int hgt, const float* __restrict__ src, long long ld,
                                     const uint8_t* __restrict__ known) {
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y;
   if (i >= w || j >= hgt) return;
@@ -1528,6 +1565,7 @@ cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, 
 // row-band halo exchange: pack this rank's outgoing slabs into a contiguous device buffer, or write the
 // slabs received from a neighbour into the ring (one thread per cell; coalesced along the row)
 __global__ void halo_kernel(const HaloArgs a) {
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y, q = blockIdx.z;
   if (i >= a.nx) return;
