@@ -427,6 +427,9 @@ __device__ __forceinline__ Cov2 cov_general(F2 N, F2 Sx, F2 Sy, const Shape& sl,
 // normalisation, adj(M) eigenvector (best-conditioned column) for the FP32 trigonometric lam0, refined
 // by Rayleigh-quotient iteration in FP64, Eqs. 2-3 angles (libdevice asin), risk and thresholds.
 // C: covariance in metres (c00, c01, c11, c02, c12, c22); (mx, my): centroid offset (m); zz: mean height.
+#ifndef SE2M_DIRECT_RQI
+#define SE2M_DIRECT_RQI 2
+#endif
 struct StateOut1 {
   float risk, pitch, roll, z;
   unsigned trav;
@@ -460,7 +463,10 @@ __device__ __noinline__ StateOut1 solve1_fp64(double C00, double C01, double C11
   if (nw > nv) { v0 = w0; v1 = w1; v2 = w2; nv = nw; }
   double s = rsqrt(nv);
   double n0 = v0 * s, n1 = v1 * s, n2 = v2 * s;
-  for (int iter = 0; iter < 3; ++iter) {  // Rayleigh-quotient iteration (cubic convergence)
+  // Rayleigh-quotient iteration (cubic convergence): the seed is good to ~1e-6 of the trace, so two steps reach
+  // FP64 rounding for every eigen-gap the parity classes compare (>= 1e-3)
+#pragma unroll 1
+  for (int iter = 0; iter < SE2M_DIRECT_RQI; ++iter) {
     const double rho = n0 * (c00 * n0 + c01 * n1 + c02 * n2) + n1 * (c01 * n0 + c11 * n1 + c12 * n2) +
                        n2 * (c02 * n0 + c12 * n1 + c22 * n2);
     m00 = c00 - rho; m11 = c11 - rho; m22 = c22 - rho;
@@ -480,7 +486,9 @@ __device__ __noinline__ StateOut1 solve1_fp64(double C00, double C01, double C11
   const double cs = csk.x, sn = csk.y;
   const double u = n0 * cs + n1 * sn, t = n0 * sn - n1 * cs;
   const double rs = rsqrt(n2 * n2 + t * t);
-  const double pitch = asin(-(n2 * u) * rs), roll = asin(t * rs);
+  // the angles' arguments in FP64, asin in FP32: ~1e-7 rad, far inside the 1e-4 rad tolerance and the 1e-5
+  // near-threshold band (the states' outputs are FP32)
+  const double pitch = asinf((float)(-(n2 * u) * rs)), roll = asinf((float)(t * rs));
   const double ax = fabs(pitch), ay = fabs(roll);
   StateOut1 o;
   const bool valid = n2 > 0.0;  // NaN fails: unknown (reading R11)
