@@ -427,6 +427,10 @@ __device__ __forceinline__ Cov2 cov_general(F2 N, F2 Sx, F2 Sy, const Shape& sl,
 // normalisation, adj(M) eigenvector (best-conditioned column) for the FP32 trigonometric lam0, refined
 // by Rayleigh-quotient iteration in FP64, Eqs. 2-3 angles (libdevice asin), risk and thresholds.
 // C: covariance in metres (c00, c01, c11, c02, c12, c22); (mx, my): centroid offset (m); zz: mean height.
+#ifndef SE2M_BORDER_UNROLL
+#define SE2M_BORDER_UNROLL 4  // unroll of the border / unknown pairs' entry loops (A/B: profiles/r02_ab.md)
+#endif
+constexpr int kBorderUnroll = SE2M_BORDER_UNROLL;
 #ifndef SE2M_DIRECT_RQI
 #define SE2M_DIRECT_RQI 2
 #endif
@@ -1149,7 +1153,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
         const float2 csk = make_float2(bk->cs.x, bk->cs.y);
         const bool restart = meta.w != 0 || !G::CB;
         if (restart) S0g = S2g = SXHg = SYHg = Nv = Sxv = Syv = Sxxv = Sxyv = Syyv = bc(0.f);
-  #pragma unroll 1
+  #pragma unroll kBorderUnroll
         for (int d = 0; d < npre; ++d) {
           const int4 o = rk[d];
           const float dj = __int_as_float(o.w);
@@ -1188,7 +1192,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
           Syyv = fma2(bc(dj * dj), cnt, Syyv);
           Sxyv = fma2(bc(dj), sdi, Sxyv);
         }
-  #pragma unroll 1
+  #pragma unroll kBorderUnroll
         for (int d = npre; d < nr; ++d) {  // single cells (exact integer geometry terms)
           const int4 o = rk[d];
           const float sg = __int_as_float(o.y), sdi = __int_as_float(o.z), sdj = __int_as_float(o.w);
