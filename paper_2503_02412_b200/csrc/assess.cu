@@ -431,6 +431,10 @@ __device__ __forceinline__ Cov2 cov_general(F2 N, F2 Sx, F2 Sy, const Shape& sl,
 #define SE2M_BORDER_UNROLL 4  // unroll of the border / unknown pairs' entry loops (A/B: profiles/r02_ab.md)
 #endif
 constexpr int kBorderUnroll = SE2M_BORDER_UNROLL;
+#ifndef SE2M_DIRECT_UNROLL
+#define SE2M_DIRECT_UNROLL 1  // unroll of the direct path's stencil-row loop
+#endif
+constexpr int kDirectUnroll = SE2M_DIRECT_UNROLL;
 #ifndef SE2M_DIRECT_RQI
 #define SE2M_DIRECT_RQI 2
 #endif
@@ -1244,7 +1248,7 @@ __global__ void __launch_bounds__(nthreads(R_T), SE2M_MINB(R_T))
               // the state's top-left footprint-box cell: halo (row, column) = its tile (row, column)
               const float* rb = T ? raw + src * HX + tr0 + sq + s : raw + (tr0 + sq + s) * HX + src;
               float a0 = 0.f, a2 = 0.f, ax = 0.f, ay = 0.f;
-#pragma unroll 1
+#pragma unroll kDirectUnroll
               for (int d = 0; d < nf; ++d) {
                 const int4 o = rkf[d];
                 const float dj = __int_as_float(o.w);

@@ -48,7 +48,7 @@ def summarize(rec, label):
         imb = np.array([max(v[3]) / max(1, min(v[3])) for v in ctas.values() if len(v[3]) > 1])
         if imb.size:  # slowest / fastest warp of a CTA in the states phase
             d["warp_imbalance"] = {"median": float(np.median(imb)), "p90": float(np.percentile(imb, 90)),
-                                   "mean_busy_frac": float(np.mean([np.mean(v[3]) / max(v[3]) for v in ctas.values()]))}
+                                   "mean_busy_frac": float(np.mean([np.mean(v[3]) / max(v[3]) for v in ctas.values() if max(v[3]) > 0]))}
         d["ctas"] = len(ctas)
         d["cta_median_us"] = durs[len(durs) // 2][0]
         d["slowest"] = [{"us": u, "bx": k // 100000, "by": k % 100000, "fast": f & 1, "pin": (f >> 8) & 255,
