@@ -33,7 +33,7 @@
 #include "se2m_internal.h"
 
 #ifndef SE2M_UNROLL_PRE
-#define SE2M_UNROLL_PRE 2
+#define SE2M_UNROLL_PRE 4  // interior prefix-entry loop (A/B: profiles/r02_ab.md)
 #endif
 #ifndef SE2M_UNROLL_CELL
 #define SE2M_UNROLL_CELL 2
