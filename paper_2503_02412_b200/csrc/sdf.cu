@@ -25,9 +25,15 @@
 
 namespace se2m {
 
-constexpr int SDF_SEG = 128;    // rows per column-pass thread
-constexpr int SDF_ROWT = 256;   // threads per row-pass CTA
-constexpr int SDF_CPT = 4;      // cells per row-pass thread (a CTA: SDF_ROWT * SDF_CPT columns of one row)
+#ifndef SE2M_SDF_SEG
+#define SE2M_SDF_SEG 128
+#endif
+#ifndef SE2M_SDF_CPT
+#define SE2M_SDF_CPT 4
+#endif
+constexpr int SDF_SEG = SE2M_SDF_SEG;  // rows per column-pass thread
+constexpr int SDF_ROWT = 256;          // threads per row-pass CTA
+constexpr int SDF_CPT = SE2M_SDF_CPT;  // cells per row-pass thread (a CTA: SDF_ROWT * SDF_CPT columns of one row)
 
 template <bool MAP>  // class source: MAP = the map's traversable bits, else an obstacle-byte mask
 __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
