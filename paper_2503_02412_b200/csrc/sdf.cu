@@ -11,7 +11,7 @@
 //                    consecutive columns: the words are shared); the downward sweep is kept in shared
 //                    memory (so each cell's (dO | dF << 8) is written to HBM once, and the upward sweep
 //                    reads the segment's class bits back from it: dO = 0 <=> obstacle);
-//   sdf_rows_kernel  SDF_CPT cells per thread, SDF_ROWT * SDF_CPT columns of one row per CTA: min over
+//   sdf_rows_kernel  4 or 8 cells per thread, 1024 or 2048 columns of one row per CTA: min over
 //                    |dx| <= W of dx^2 + g(x + dx)^2 with g the column distance to the other class
 //                    (squares staged in shared memory, "none" = a large sentinel, so the loop is
 //                    branch-free; four offsets per step), stopping once dx^2 reaches the best; one flag
@@ -28,12 +28,10 @@ namespace se2m {
 #ifndef SE2M_SDF_SEG
 #define SE2M_SDF_SEG 128
 #endif
-#ifndef SE2M_SDF_CPT
-#define SE2M_SDF_CPT 4
-#endif
 constexpr int SDF_SEG = SE2M_SDF_SEG;  // rows per column-pass thread
 constexpr int SDF_ROWT = 256;          // threads per row-pass CTA
-constexpr int SDF_CPT = SE2M_SDF_CPT;  // cells per row-pass thread (a CTA: SDF_ROWT * SDF_CPT columns of one row)
+// cells per row-pass thread (a CTA: SDF_ROWT * CPT columns of one row): 8 on rows wider than 1536 columns, else 4
+// (one CTA per row segment amortises the staging; A/B in profiles/r02_ab.md)
 
 template <bool MAP>  // class source: MAP = the map's traversable bits, else an obstacle-byte mask
 __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
@@ -95,6 +93,7 @@ __global__ void __launch_bounds__(128) sdf_cols_kernel(const SdfParams p) {
   }
 }
 
+template <int SDF_CPT>
 __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
   extern __shared__ unsigned char sm[];
   // the region reaches P = W + 3 columns past the CTA's span on either side, so the scan below can test four
@@ -189,10 +188,13 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   else sdf_cols_kernel<false><<<gc, 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  constexpr int SPAN = SDF_ROWT * SDF_CPT;
+  const int cpt = p.nx > 1536 ? 8 : 4;
+  const int SPAN = SDF_ROWT * cpt;
   const int RW = SPAN + 2 * (p.W + 3);
   const size_t smem = (size_t)RW * 8 + 2 * (size_t)((RW + 31) / 32 + 1) * 4;
-  sdf_rows_kernel<<<dim3((p.nx + SPAN - 1) / SPAN, p.ny, p.layers), SDF_ROWT, smem, s>>>(p);
+  const dim3 gr((p.nx + SPAN - 1) / SPAN, p.ny, p.layers);
+  if (cpt == 8) sdf_rows_kernel<8><<<gr, SDF_ROWT, smem, s>>>(p);
+  else sdf_rows_kernel<4><<<gr, SDF_ROWT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
