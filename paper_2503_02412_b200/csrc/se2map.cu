@@ -869,6 +869,19 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
   return SE2M_OK;
 }
 
+// The vertical-window-edge kernel's stream.  SE2M_EDGE_PRIORITY: created at the device's greatest priority, so
+// the block scheduler hands freed SM slots to its (longer) CTAs before the main grid's.
+#ifndef SE2M_EDGE_PRIORITY
+#define SE2M_EDGE_PRIORITY 1
+#endif
+static cudaError_t create_edge_stream(cudaStream_t* s) {
+  int lo = 0, hi = 0;
+  if (SE2M_EDGE_PRIORITY && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess)
+    return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, hi);
+  cudaGetLastError();
+  return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+
 extern "C" se2m_status se2m_step(se2m_map* m, double x, double y, const float* world, int64_t world_ld,
                                  int64_t world_I0, int64_t world_J0, int32_t world_w, int32_t world_h,
                                  int32_t mem, int32_t* out_di, int32_t* out_dj) {
@@ -909,7 +922,7 @@ extern "C" se2m_status se2m_step(se2m_map* m, double x, double y, const float* w
     return st;
   }
   if (!m->edge_stream) {  // the assess may fork onto the edge stream: create it outside the capture
-    CUDA_TRY(m, cudaStreamCreateWithFlags(&m->edge_stream, cudaStreamNonBlocking), "cudaStreamCreate(edge)");
+    CUDA_TRY(m, create_edge_stream(&m->edge_stream), "cudaStreamCreate(edge)");
     CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
     CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming), "cudaEventCreate");
   }
@@ -1085,7 +1098,7 @@ extern "C" se2m_status se2m_assess_se2(se2m_map* m, int32_t mode) {
     }
     if (p.n_tcols > 0) {
       if (!m->edge_stream) {
-        CUDA_TRY(m, cudaStreamCreateWithFlags(&m->edge_stream, cudaStreamNonBlocking), "cudaStreamCreate(edge)");
+        CUDA_TRY(m, create_edge_stream(&m->edge_stream), "cudaStreamCreate(edge)");
         CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
         CUDA_TRY(m, cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming), "cudaEventCreate");
       }
