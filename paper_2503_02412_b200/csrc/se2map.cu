@@ -869,10 +869,11 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
   return SE2M_OK;
 }
 
-// The vertical-window-edge kernel's stream.  SE2M_EDGE_PRIORITY: created at the device's greatest priority, so
-// the block scheduler hands freed SM slots to its (longer) CTAs before the main grid's.
+// The vertical-window-edge kernel's stream.  SE2M_EDGE_PRIORITY = 1 creates it at the device's greatest priority
+// (the block scheduler then hands freed SM slots to its CTAs first): measured slower on the large map (1.032 vs
+// 1.023 ms, profiles/r02_ab.md), so off.
 #ifndef SE2M_EDGE_PRIORITY
-#define SE2M_EDGE_PRIORITY 1
+#define SE2M_EDGE_PRIORITY 0
 #endif
 static cudaError_t create_edge_stream(cudaStream_t* s) {
   int lo = 0, hi = 0;
