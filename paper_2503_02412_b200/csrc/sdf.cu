@@ -28,6 +28,9 @@ namespace se2m {
 #ifndef SE2M_SDF_SEG
 #define SE2M_SDF_SEG 128
 #endif
+#ifndef SE2M_SDF_PAIRS
+#define SE2M_SDF_PAIRS 1  // row pass over pairs of neighbouring cells (sdf_rows_pair_kernel)
+#endif
 constexpr int SDF_SEG = SE2M_SDF_SEG;  // rows per column-pass thread
 constexpr int SDF_ROWT = 256;          // threads per row-pass CTA
 // cells per row-pass thread (a CTA: SDF_ROWT * CPT columns of one row): 8 on rows wider than 1536 columns, else 4
@@ -181,6 +184,105 @@ __global__ void __launch_bounds__(SDF_ROWT) sdf_rows_kernel(const SdfParams p) {
   }
 }
 
+// Row pass over PAIRS of neighbouring cells (x, x + 1): when both are of one class they scan one set of candidate
+// columns — a candidate d columns left of x is d + 1 left of x + 1, one right of x + 1 is one further from x — so
+// each candidate load serves both cells; a pair of mixed classes is two cells at distance 1 from the other class.
+// Same results as sdf_rows_kernel (candidates past W clamp to d_max either way).
+template <int PPT>
+__global__ void __launch_bounds__(SDF_ROWT) sdf_rows_pair_kernel(const SdfParams p) {
+  extern __shared__ unsigned char sm[];
+  constexpr int SPAN = SDF_ROWT * 2 * PPT;
+  const int W = p.W, P = W + 4, RW = SPAN + 2 * P, NWD = (RW + 31) / 32 + 1;
+  int* g2O = reinterpret_cast<int*>(sm);
+  int* g2F = g2O + RW;
+  unsigned* bO = reinterpret_cast<unsigned*>(g2F + RW);
+  if (threadIdx.x < 2) bO[threadIdx.x * NWD + NWD - 1] = 0u;
+  unsigned* bF = bO + NWD;
+  constexpr int kFar = 1 << 24;
+  const int L = blockIdx.z, j = blockIdx.y, x0 = blockIdx.x * SPAN - P;
+  const int lane = threadIdx.x & 31;
+  const uint16_t* grow = p.g + ((size_t)L * p.ny + j) * p.nx;
+  for (int c0 = threadIdx.x & ~31; c0 < RW; c0 += SDF_ROWT) {
+    const int c = c0 + lane, x = x0 + c;
+    const uint16_t v = (c < RW && x >= 0 && x < p.nx) ? grow[x] : (uint16_t)0xffff;
+    const int o = v & 0xff, f = v >> 8;
+    if (c < RW) {
+      g2O[c] = o != 255 ? o * o : kFar;
+      g2F[c] = f != 255 ? f * f : kFar;
+    }
+    const unsigned wo = __ballot_sync(0xffffffffu, o != 255), wf = __ballot_sync(0xffffffffu, f != 255);
+    if (lane == 0) { bO[c0 >> 5] = wo; bF[c0 >> 5] = wf; }
+  }
+  __syncthreads();
+  const int py = p.trav ? (p.pyM + j >= p.ny ? p.pyM + j - p.ny : p.pyM + j) : 0;
+#pragma unroll 1
+  for (int i = 0; i < PPT; ++i) {
+    const int c = P + 2 * (threadIdx.x + i * SDF_ROWT);  // the pair's left cell (region column)
+    const int x = x0 + c;
+    if (x0 + P + 2 * i * SDF_ROWT >= p.nx) break;  // (CTA-uniform)
+    const bool va = x < p.nx, vb = x + 1 < p.nx;
+    const bool oa = g2O[c] == 0, ob = g2O[c + 1] == 0;
+    const bool mixed = vb && oa != ob;
+    const int* g2 = oa ? g2F : g2O;
+    const unsigned* bw = oa ? bF : bO;
+    // some column in [c - W, c + 1 + W] has a cell of the other class within W rows?
+    const int a = c - W, b = c + 1 + W, wa = a >> 5, wb = b >> 5;
+    unsigned long long any;
+    if (W <= 30) {  // the 2W + 2 window bits lie in words wa, wa + 1
+      const unsigned long long w64 = ((unsigned long long)bw[wa + 1] << 32) | bw[wa];
+      any = (w64 >> (a & 31)) & ((4ull << (2 * W)) - 1ull);
+    } else {
+      any = 0;
+#pragma unroll 1
+      for (int w = wa; w <= wb; ++w) {
+        unsigned m = bw[w];
+        if (w == wa) m &= 0xffffffffu << (a & 31);
+        if (w == wb) m &= 0xffffffffu >> (31 - (b & 31));
+        any |= m;
+      }
+    }
+    const bool scan = va && !mixed && any != 0ull;
+    int ba = scan ? min(g2[c], 1 + g2[c + 1]) : kFar;
+    int bb = scan ? min(g2[c + 1], 1 + g2[c]) : kFar;
+    if (mixed) ba = bb = 1;
+    const int* pl = g2 + (c - 1);  // candidates d .. d + 3 left of x
+    const int* pr = g2 + (c + 2);  // ... right of x + 1
+    int s0 = 1, t = 3;             // d^2, 2 d + 1
+#pragma unroll 1
+    for (int d = 1; d <= W; d += 4, pl -= 4, pr += 4) {
+      if (!__any_sync(0xffffffffu, scan && s0 < max(ba, bb))) break;
+      const int s1 = s0 + t, s2 = s1 + t + 2, s3 = s2 + t + 4, s4 = s3 + t + 6;  // (d + 1)^2 .. (d + 4)^2
+      const int l0 = pl[0], l1 = pl[-1], l2 = pl[-2], l3 = pl[-3];
+      const int r0 = pr[0], r1 = pr[1], r2 = pr[2], r3 = pr[3];
+      ba = min(min(ba, s0 + l0), s1 + r0);
+      bb = min(min(bb, s0 + r0), s1 + l0);
+      ba = min(min(ba, s1 + l1), s2 + r1);
+      bb = min(min(bb, s1 + r1), s2 + l1);
+      ba = min(min(ba, s2 + l2), s3 + r2);
+      bb = min(min(bb, s2 + r2), s3 + l2);
+      ba = min(min(ba, s3 + l3), s4 + r3);
+      bb = min(min(bb, s3 + r3), s4 + l3);
+      s0 = s4;
+      t += 8;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!(h ? vb : va)) continue;
+      const int best = h ? bb : ba;
+      float d = best >= kFar ? p.d_max : fminf(p.d_max, sqrtf((float)best) * p.r);
+      if (h ? ob : oa) d = -d;
+      size_t o;
+      if (p.trav) {
+        int px = p.pxM + x + h; if (px >= p.nx) px -= p.nx;
+        o = ((size_t)L * p.ny + py) * p.nx + px;
+      } else {
+        o = ((size_t)L * p.ny + j) * p.nx + x + h;
+      }
+      p.out[o] = d;
+    }
+  }
+}
+
 cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   if (p.layers <= 0 || p.nx <= 0 || p.ny <= 0) return cudaSuccess;
   const dim3 gc((p.nx + 127) / 128, (p.ny + SDF_SEG - 1) / SDF_SEG, p.layers);
@@ -190,6 +292,14 @@ cudaError_t launch_sdf(const SdfParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const int cpt = p.nx > 1536 ? 8 : 4;
   const int SPAN = SDF_ROWT * cpt;
+  if (SE2M_SDF_PAIRS) {
+    const int RW = SPAN + 2 * (p.W + 4);
+    const size_t smem = (size_t)RW * 8 + 2 * (size_t)((RW + 31) / 32 + 1) * 4;
+    const dim3 gr((p.nx + SPAN - 1) / SPAN, p.ny, p.layers);
+    if (cpt == 8) sdf_rows_pair_kernel<4><<<gr, SDF_ROWT, smem, s>>>(p);
+    else sdf_rows_pair_kernel<2><<<gr, SDF_ROWT, smem, s>>>(p);
+    return cudaGetLastError();
+  }
   const int RW = SPAN + 2 * (p.W + 3);
   const size_t smem = (size_t)RW * 8 + 2 * (size_t)((RW + 31) / 32 + 1) * 4;
   const dim3 gr((p.nx + SPAN - 1) / SPAN, p.ny, p.layers);
