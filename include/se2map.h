@@ -167,8 +167,9 @@ se2m_status se2m_query(se2m_map* m, int64_t n, const double* xyt, float* risk, f
 
 /* Asynchronous query (the planner's pipelined read): the same lookups as se2m_query, written to
  * out = 5 x n floats, planar: risk[n], pitch[n], roll[n], z[n], trav[n] (1.0 / 0.0); states outside the
- * window (or not owned) give NaN / risk 1 / trav 0.  xyt and out are host (mem = SE2M_MEM_HOST; use
- * pinned memory for a truly asynchronous copy) or device pointers.  Queued on the map's stream and not
+ * window (or not owned) give NaN / risk 1 / trav 0.  xyt and out are host (mem = SE2M_MEM_HOST) or device
+ * pointers.  Pinned (page-locked) host buffers are read and written in place by the query kernel (zero copy);
+ * pageable ones are staged through device memory with copies on the stream.  Queued on the map's stream and not
  * synchronised: out is valid after se2m_synchronize (or an event recorded on the stream); xyt must stay
  * untouched until then.  No out-of-range status (read the NaNs). */
 se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xyt, float* out, int32_t mem);
@@ -309,7 +310,8 @@ se2m_status se2m_query_trilinear(se2m_map* m, int64_t n, const double* xyt, int3
 
 /* Asynchronous form (the planner's pipelined access): the same interpolation written to out = 4 x n floats,
  * planar: value[n], d/dx[n], d/dy[n], d/dtheta[n] (NaN where a corner is outside / not owned).  xyt and out
- * are host (pinned for a truly asynchronous copy) or device pointers per mem; queued on the map's stream, not
+ * are host or device pointers per mem (pinned host buffers are read and written in place by the kernel, pageable
+ * ones staged); queued on the map's stream, not
  * synchronised (out valid after se2m_synchronize; xyt untouched until then). */
 se2m_status se2m_query_trilinear_async(se2m_map* m, int64_t n, const double* xyt, int32_t field, float* out,
                                        int32_t mem);

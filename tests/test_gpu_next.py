@@ -98,6 +98,20 @@ def test_map_sdf_and_trilinear_risk():
         if all(ok[c] for c in corners):
             assert abs(vsg[t] - vs_o[t]) <= 1e-5
             assert np.all(np.abs(gsg[t] - gs_o[t]) <= 1e-4 / np.array([r, r, dth]))
+    # the asynchronous form with pinned host buffers (read / written in place by the kernel) and with device
+    # buffers returns exactly the synchronous values
+    import torch
+    for field, (v_ref, g_ref) in ((0, (vg, gg)), (1, (vsg, gsg))):
+        for dev in ("cpu", "cuda"):
+            xt = torch.from_numpy(q.copy())
+            xt = xt.pin_memory() if dev == "cpu" else xt.cuda()
+            out = torch.full((4, nq), 7.0, dtype=torch.float32)
+            out = out.pin_memory() if dev == "cpu" else out.cuda()
+            m.query_trilinear_async(xt, out, field)
+            m.synchronize()
+            o = out.cpu().numpy()
+            assert np.array_equal(o[0], v_ref, equal_nan=True), (field, dev)
+            assert np.array_equal(o[1:].T, g_ref, equal_nan=True), (field, dev)
     assert n_cmp > 0.8 * nq
 
 
