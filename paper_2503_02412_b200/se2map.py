@@ -370,9 +370,9 @@ class Se2Map:
         return out
 
     def query_async(self, xyt, out):
-        """Queue the lookups of xyt (n x 3 float64: pinned host tensor / NumPy view of one, or CUDA tensor)
-        into out (5 x n float32, same memory kind: risk, pitch, roll, z, trav as rows); valid after
-        synchronize().  Both buffers must stay alive and untouched until then."""
+        """Queue the lookups of xyt (n x 3 float64: host array — pinned buffers are read / written in place by the
+        kernel, pageable ones staged — or CUDA tensor) into out (5 x n float32, same memory kind: risk, pitch,
+        roll, z, trav as rows); valid after synchronize().  Both buffers must stay alive and untouched until then."""
         _check_async_buffers(xyt, out, 5)
         xp, mem, _ = _ptr_nocopy(xyt)
         op, _, _ = _ptr_nocopy(out)
@@ -462,9 +462,10 @@ class Se2Map:
         return v, g, st
 
     def query_trilinear_async(self, xyt, out, field: int = 0):
-        """Queue trilinear lookups of xyt (n x 3 float64, C-contiguous: pinned host tensor / NumPy view of one, or
-        CUDA tensor) into out (4 x n float32, same memory kind: value, d/dx, d/dy, d/dtheta); valid after
-        synchronize().  Both buffers must stay alive and untouched until then."""
+        """Queue trilinear lookups of xyt (n x 3 float64, C-contiguous: host array — pinned buffers are read /
+        written in place by the kernel, pageable ones staged — or CUDA tensor) into out (4 x n float32, same memory
+        kind: value, d/dx, d/dy, d/dtheta); valid after synchronize().  Both buffers must stay alive and untouched
+        until then."""
         _check_async_buffers(xyt, out, 4)
         xp, mem, _ = _ptr_nocopy(xyt)
         op, _, _ = _ptr_nocopy(out)

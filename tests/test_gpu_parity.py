@@ -139,16 +139,20 @@ def test_query_matches_download_and_oracle_index():
         assert q["trav"][t] == g["trav"][k, j, i]
         assert (q["pitch"][t] == g["pitch"][k, j, i]) or (np.isnan(q["pitch"][t]) and np.isnan(g["pitch"][k, j, i]))
     assert q["status"] != 0  # some queries were outside
-    # the asynchronous form (pinned host buffers, then device buffers) returns the same values
+    # the asynchronous form (pinned host buffers: read / written in place by the kernel; pageable NumPy buffers:
+    # staged through device memory; device buffers) returns the same values
     import torch
-    for dev in ("cpu", "cuda"):
-        xt = torch.from_numpy(xyt.copy())
-        xt = xt.pin_memory() if dev == "cpu" else xt.cuda()
-        out = torch.full((5, n), 7.0, dtype=torch.float32)
-        out = out.pin_memory() if dev == "cpu" else out.cuda()
+    for dev in ("cpu", "numpy", "cuda"):
+        if dev == "numpy":
+            xt, out = xyt.copy(), np.full((5, n), 7.0, np.float32)
+        else:
+            xt = torch.from_numpy(xyt.copy())
+            xt = xt.pin_memory() if dev == "cpu" else xt.cuda()
+            out = torch.full((5, n), 7.0, dtype=torch.float32)
+            out = out.pin_memory() if dev == "cpu" else out.cuda()
         m.query_async(xt, out)
         m.synchronize()
-        o = out.cpu().numpy()
+        o = out if dev == "numpy" else out.cpu().numpy()
         for row, f in enumerate(("risk", "pitch", "roll", "z")):
             assert np.array_equal(o[row], q[f], equal_nan=True), (dev, f)
         assert np.array_equal(o[4] > 0.5, q["trav"] == 1), dev
