@@ -620,12 +620,21 @@ def highres_update(S, stream, torch, reps=10):
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6450.6)
     bytes_state = 16.0 + 1.0 / 8.0 + (4.0 + 1.0 / 8.0) / n_yaw
+    W_state = 4 * stencil_cells(cfg) + 200
     out = {"highres_ms": t, "highres_states": n, "highres_states_per_s": n / (t * 1e-3),
-           "highres_W_ops_per_state": 4 * stencil_cells(cfg) + 200}
+           "highres_W_ops_per_state": W_state}
     # the binding bound of this config is the kernels' own instruction issue, not HBM: its floor is
     # the warp instructions of one assess call (ncu, profiles/) at one instruction per cycle per scheduler
     roof = {"hbm": {"achieved_gbs": n * bytes_state / (t * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                     "frac": n * bytes_state / (t * 1e-3) / 1e9 / hbm_peak, "bytes_per_state": bytes_state}}
+    # SURVEY.md §8(d)'s gate (>= 60 % of the FP32 roofline of the paper-algorithm work W per state), "effective"
+    # as for the large map: the kernel does fewer operations than W by prefix differences and the yaw chain
+    sm_mhz = peaks.get("sm_max_mhz") or 1965.0
+    n_sm_dev = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    alu_peak = n_sm_dev * 128 * sm_mhz * 1e6 / 1e12
+    alu = n * W_state / (t * 1e-3) / 1e12
+    roof["alu"] = {"achieved": alu, "peak": alu_peak, "unit": "Tops/s (FP32-pipe ops, FMA=1)",
+                   "frac_effective": alu / alu_peak, "ops_per_state": W_state}
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ncu_highres.json")))
         n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
