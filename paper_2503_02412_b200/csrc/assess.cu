@@ -1531,11 +1531,16 @@ cudaError_t launch_clear_rect(float* h, int ldh, int x0, int y0, int w, int hgt,
   return cudaGetLastError();
 }
 
-__global__ void fill_strips_kernel(const FillArgs f) {
+// One thread per cell of the concatenated rectangles (a column strip and a row strip have very different shapes:
+// a 2-D grid over their bounding sizes would be mostly idle blocks)
+__global__ void fill_strips_kernel(const FillArgs f, long long n0, long long n_all) {
   pdl_trigger();
-  const int4 rc = f.rect[blockIdx.z];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  if (i >= rc.z || j >= rc.w) return;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_all) return;
+  const int q = t < n0 ? 0 : 1;
+  const int4 rc = f.rect[q];
+  const long long u = q ? t - n0 : t;
+  const int j = (int)(u / rc.z), i = (int)(u - (long long)j * rc.z);
   const int li = rc.x + i, lj = rc.y + j;  // logical window cell
   const long long wi = f.I_M + li - f.wI0, wj = f.J_M + lj - f.wJ0;
   float v = __int_as_float(0x7fc00000);
@@ -1547,33 +1552,56 @@ __global__ void fill_strips_kernel(const FillArgs f) {
 }
 
 cudaError_t launch_fill_strips(const FillArgs& f, cudaStream_t s) {
-  int w = 0, hgt = 0;
-  for (int q = 0; q < f.n; ++q) { w = max(w, f.rect[q].z); hgt = max(hgt, f.rect[q].w); }
-  if (w <= 0 || hgt <= 0) return cudaSuccess;
-  fill_strips_kernel<<<dim3((w + 127) / 128, hgt, f.n), 128, 0, s>>>(f);
+  long long cnt[2] = {0, 0};
+  for (int q = 0; q < f.n && q < 2; ++q)
+    if (f.rect[q].z > 0 && f.rect[q].w > 0) cnt[q] = (long long)f.rect[q].z * f.rect[q].w;
+  const long long n_all = cnt[0] + cnt[1];
+  if (n_all <= 0) return cudaSuccess;
+  FillArgs g = f;
+  if (cnt[0] == 0) { g.rect[0] = f.rect[1]; cnt[0] = cnt[1]; cnt[1] = 0; }  // (an empty first rectangle)
+  fill_strips_kernel<<<(unsigned)((n_all + 255) / 256), 256, 0, s>>>(g, cnt[0], n_all);
   return cudaGetLastError();
 }
 
+// SE2M_SCATTER_EPT cells per thread (strided by the block width): the loads of a thread are all issued before its
+// stores, so a short, memory-bound update keeps more reads in flight
+#ifndef SE2M_SCATTER_EPT
+#define SE2M_SCATTER_EPT 4
+#endif
 __global__ void scatter_rect_kernel(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0,
                                     int w, int hgt, const float* __restrict__ src, long long ld,
                                     const uint8_t* __restrict__ known) {
   pdl_trigger();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int EPT = SE2M_SCATTER_EPT;
   const int j = blockIdx.y;
-  if (i >= w || j >= hgt) return;
-  int px = px0 + i; if (px >= nx) px -= nx;
+  if (j >= hgt) return;
   int py = py0 + j; if (py >= ny) py -= ny;
-  const size_t si = (size_t)j * ld + i;
-  float v = src[si];
-  if (known && !known[si]) v = __int_as_float(0x7fc00000);
-  h[(size_t)py * ldh + px] = v;
-  if (var) var[(size_t)py * ldh + px] = prior_var;
+  const int i0 = blockIdx.x * blockDim.x * EPT + threadIdx.x;
+  float v[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = i0 + e * blockDim.x;
+    v[e] = 0.f;
+    if (i < w) {
+      const size_t si = (size_t)j * ld + i;
+      v[e] = src[si];
+      if (known && !known[si]) v[e] = __int_as_float(0x7fc00000);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < EPT; ++e) {
+    const int i = i0 + e * blockDim.x;
+    if (i >= w) break;
+    int px = px0 + i; if (px >= nx) px -= nx;
+    h[(size_t)py * ldh + px] = v[e];
+    if (var) var[(size_t)py * ldh + px] = prior_var;
+  }
 }
 
 cudaError_t launch_scatter_rect(float* h, float* var, float prior_var, int ldh, int nx, int ny, int px0, int py0, int w,
                                 int hgt, const float* src, long long ld, const uint8_t* known, cudaStream_t s) {
   if (w <= 0 || hgt <= 0) return cudaSuccess;
-  dim3 grid((w + 255) / 256, hgt);
+  dim3 grid((w + 256 * SE2M_SCATTER_EPT - 1) / (256 * SE2M_SCATTER_EPT), hgt);
   scatter_rect_kernel<<<grid, 256, 0, s>>>(h, var, prior_var, ldh, nx, ny, px0, py0, w, hgt, src, ld, known);
   return cudaGetLastError();
 }

@@ -860,12 +860,19 @@ extern "C" se2m_status se2m_shift_window(se2m_map* m, double x, double y, int32_
   recentre(m, x, y, &di, &dj, strips, &ns, &all);
   clamp_out(di, out_di);
   clamp_out(dj, out_dj);
-  const int nx = m->prm.nx, ny = m->prm.ny, pxM = pmod(m->I_M, nx), pyM = pmod(m->J_M, ny);
-  for (int q = 0; q < ns; ++q) {  // cells entering the window (their slots held cells that left): unknown
-    CUDA_TRY(m, launch_clear_rect(m->d_h, m->ldh, (pxM + strips[q].x) % nx, (pyM + strips[q].y) % ny, strips[q].z,
-                                  strips[q].w, nx, ny, m->stream), "clear");
-    m->launches++;
-  }
+  if (ns == 0) return SE2M_OK;
+  // cells entering the window (their slots held cells that left): unknown — both strips in one launch (the strip
+  // fill of se2m_step with an empty world: every cell NaN, variances untouched)
+  FillArgs f;
+  memset(&f, 0, sizeof f);
+  f.h = m->d_h; f.var = nullptr; f.ldh = m->ldh;
+  f.nx = m->prm.nx; f.ny = m->prm.ny; f.pxM = pmod(m->I_M, f.nx); f.pyM = pmod(m->J_M, f.ny);
+  f.I_M = m->I_M; f.J_M = m->J_M;
+  f.world = nullptr; f.ww = 0; f.wh = 0;
+  f.n = ns;
+  for (int q = 0; q < ns; ++q) f.rect[q] = strips[q];
+  CUDA_TRY(m, launch_fill_strips(f, m->stream), "clear");
+  m->launches++;
   return SE2M_OK;
 }
 
@@ -1426,8 +1433,8 @@ extern "C" se2m_status se2m_query_async(se2m_map* m, int64_t n, const double* xy
   void* zx = mem == SE2M_MEM_HOST ? mapped_host(xyt) : nullptr;
   void* zo = zx ? mapped_host(out) : nullptr;
   if (zx && zo) {  // pinned host buffers: the kernel reads and writes them in place
+    // (the miss counter is not reported by the async form: no reset on the stream)
     if (!m->d_qcnt) CUDA_TRY(m, cudaMalloc(&m->d_qcnt, sizeof(int)), "cudaMalloc(query)");
-    CUDA_TRY(m, cudaMemsetAsync(m->d_qcnt, 0, sizeof(int), m->stream), "query counter");
     CUDA_TRY(m, launch_query(p, query_geo(m), (int)n, static_cast<const double*>(zx), static_cast<float*>(zo), m->d_qcnt,
                              m->stream), "query kernel");
     m->launches++;
@@ -1859,9 +1866,8 @@ extern "C" se2m_status se2m_query_trilinear_async(se2m_map* m, int64_t n, const 
   const float* f = field == 0 ? reinterpret_cast<const float*>(m->d_out) : m->d_sdf;
   void* zx = mem == SE2M_MEM_HOST ? mapped_host(xyt) : nullptr;
   void* zo = zx ? mapped_host(out) : nullptr;
-  if (zx && zo) {  // pinned host buffers: read and written in place by the kernel
+  if (zx && zo) {  // pinned host buffers: read and written in place by the kernel (miss counter not reported)
     if (!m->d_qcnt) CUDA_TRY(m, cudaMalloc(&m->d_qcnt, sizeof(int)), "cudaMalloc(query)");
-    CUDA_TRY(m, cudaMemsetAsync(m->d_qcnt, 0, sizeof(int), m->stream), "query counter");
     CUDA_TRY(m, launch_trilinear(f, field == 0 ? 4 : 1, field, query_geo(m), (int)n, static_cast<const double*>(zx),
                                  static_cast<float*>(zo), m->d_qcnt, m->stream), "trilinear kernel");
     m->launches++;
